@@ -1,0 +1,168 @@
+/*
+ * ams.h -- C ABI of the B200-native action-context matcher (AMS, arXiv 2508.10259).
+ *
+ * The hot path this library implements is the action-context pool lookup of AMS:
+ *   PAPER.md:486 (3.2.1)   a context holds "data from the robot's joints and the output
+ *                           embedding obtained from the final inference";
+ *   PAPER.md:489 (3.2.1)   "During each inference, the system first checks the action
+ *                           context pool to see if any similar and reusable intermediate
+ *                           states exist";
+ *   PAPER.md:494 (3.2.1)   "After one single inference, AMS adds the unseen vector ... into
+ *                           the context pool" (-> ams_pool_append);
+ *   PAPER.md:865 (4)       replay retrieves "stored contexts from the context pool one by
+ *                           one" (-> the ranked top-k list);
+ *   SPEC.md:186-190        lookup: best match "or none below threshold";
+ *   BASELINE.json north_star: cosine similarity over the embedding, gated by the L2
+ *                           distance between joint states, per-query top-k, a cosine
+ *                           threshold giving the replay hit/miss flag, ties to the
+ *                           lowest index; ams_pool_create / ams_pool_append /
+ *                           ams_match / ams_pool_destroy.
+ * The exact definition (and every reading where the paper is silent) is in DESIGN.md
+ * "Method" / "Readings"; the CPU oracle in oracle/ computes the same definition.
+ *
+ * Conventions (all entry points):
+ *   - Every call returns ams_status_t and never throws or aborts.
+ *   - The library owns pool storage and all workspace; the caller owns every buffer it
+ *     passes.  Input buffers may be host or device pointers (detected through UVA);
+ *     output buffers of ams_match must be DEVICE pointers.
+ *   - Work is enqueued on the caller's stream `stream` (a cudaStream_t passed as void*;
+ *     NULL = legacy default stream); calls return after enqueue.  Inputs must stay
+ *     valid until the stream reaches that point.  An append is visible to every later
+ *     match on the same stream.
+ *   - A pool is NOT thread-safe; callers serialise calls on one pool ("a
+ *     single pool serializes writers").
+ *   - Argument errors are detected synchronously and nothing is enqueued.
+ *   - After AMS_ERR_CUDA / AMS_ERR_NCCL the pool is unusable and must be destroyed.
+ *   - Multi-GPU (world > 1): one process per GPU; create / append / match / destroy are
+ *     collective (every rank calls them in the same order with identical arguments).
+ */
+#ifndef AMS_H_
+#define AMS_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AMS_ABI_VERSION 1
+
+typedef struct ams_pool_s* ams_pool_t; /* opaque, library-owned */
+
+typedef enum {
+  AMS_OK = 0,
+  AMS_ERR_INVALID_ARGUMENT = 1,
+  AMS_ERR_CAPACITY = 2,      /* SPEC.md:181 CapacityError: append would exceed capacity */
+  AMS_ERR_OUT_OF_MEMORY = 3,
+  AMS_ERR_CUDA = 4,          /* sticky device error; destroy the pool */
+  AMS_ERR_NCCL = 5,          /* collective failure; destroy the pool */
+  AMS_ERR_UNSUPPORTED = 6,   /* e.g. no sm_100 device, d not a multiple of 64 */
+  AMS_ERR_INTERNAL = 7
+} ams_status_t;
+
+typedef enum { AMS_DTYPE_BF16 = 0, AMS_DTYPE_FP32 = 1 } ams_dtype_t;
+
+typedef struct {
+  int32_t dim;            /* d, embedding width; multiple of 64, 64 <= d <= 16384 */
+  int32_t joint_dim;      /* J in [1, 16] joint DoF (7-DoF output action) */
+  ams_dtype_t dtype;      /* storage type of pool AND query embeddings (reading R10).
+                             BF16: tensor-core path, fp32 accumulate (tolerance 2e-3);
+                             FP32: canonical-order path, bit-exact vs the oracle */
+  int64_t capacity;       /* max global rows; storage is preallocated at create */
+  int32_t max_queries;    /* >= every nq passed to ams_match (workspace sizing) */
+  int32_t max_k;          /* >= every k passed to ams_match; 1 <= max_k <= 64 */
+  int32_t device;         /* CUDA ordinal used by this rank */
+  int32_t rank, world;    /* world == 1: single GPU, no NCCL; world <= 64 */
+  const void* nccl_id;    /* 128-byte ncclUniqueId, identical on all ranks (NULL if world == 1) */
+  int64_t shard_block;    /* rows per block of the block-cyclic row map (global append
+                             ordinal o lives on rank (o / B) % world);
+                             0 -> contiguous: B = ceil(capacity / world) */
+} ams_pool_config_t;
+
+/* Writes a fresh 128-byte NCCL unique id to out128 (rank 0 calls it; the harness
+ * broadcasts the bytes to the other ranks, e.g. through torch.distributed). */
+ams_status_t ams_get_nccl_unique_id(void* out128);
+
+/* Creates a pool on cfg->device: allocates the rank's shard (bf16 or fp32 embeddings
+ * [cap_shard, d] row-major, fp32 inverse norms [cap_shard], fp32 joints [cap_shard, JP]
+ * with JP = J rounded up to 4, 8 or 16 and zero padding) plus every workspace
+ * ams_match needs (ams_match never allocates).  Collective over NCCL if world > 1.
+ * Errors: AMS_ERR_INVALID_ARGUMENT (null pointers, bad sizes), AMS_ERR_UNSUPPORTED
+ * (device is not sm_100), AMS_ERR_OUT_OF_MEMORY, AMS_ERR_CUDA, AMS_ERR_NCCL. */
+ams_status_t ams_pool_create(const ams_pool_config_t* cfg, ams_pool_t* out);
+
+/* Record: appends n contexts.  emb is [n, d] (bf16 bits as uint16, or
+ * fp32, per cfg.dtype) row-major, joints is [n, J] fp32 row-major; host or device.
+ * Rows receive the global append ordinals [size, size + n); *first_index (host, may
+ * be NULL) receives `size`.  Each rank keeps the rows its shard map owns and computes
+ * their inverse L2 norms from the STORED values (bf16: fp64 sum, rounded once to fp32;
+ * fp32: canonical in-order fmaf chain, IEEE sqrt and division).
+ * Errors: AMS_ERR_INVALID_ARGUMENT (null pool, n < 0, null data with n > 0),
+ * AMS_ERR_CAPACITY (size + n > capacity; nothing is appended), AMS_ERR_CUDA. */
+ams_status_t ams_pool_append(ams_pool_t pool, const void* emb, const float* joints, int64_t n,
+                             int64_t* first_index, void* stream);
+
+/* Lookup: for each of nq queries (q_emb [nq, d] in the
+ * pool dtype, q_joints [nq, J] fp32; host or device):
+ *   score(i, j)  = (dot(q_i, e_j) * inv_q_i) * inv_e_j                    (cosine)
+ *   eligible(i,j) = sum_t (r_it - p_jt)^2 <= fp32(gate_radius^2), canonical fp32
+ *                   (the joint gate; gate_radius = +inf disables it)
+ *   out_index[i, 0..k)  global append ordinals of the k best eligible rows ordered by
+ *                       (score desc, index asc); -1 padding when fewer are eligible
+ *   out_score[i, 0..k)  their fp32 scores; -inf padding
+ *   out_hit[i]          1 iff out_index[i,0] >= 0 and out_score[i,0] >= threshold
+ * Outputs are DEVICE buffers: out_index int64 [nq, k], out_score fp32 [nq, k],
+ * out_hit uint8 [nq].  With world > 1 every rank receives identical outputs.
+ * Errors: AMS_ERR_INVALID_ARGUMENT (null pool/pointers, nq < 1 or > max_queries,
+ * k < 1 or > max_k, NaN threshold, NaN or negative gate_radius), AMS_ERR_CUDA,
+ * AMS_ERR_NCCL.  k larger than the pool is legal (padded). */
+ams_status_t ams_match(ams_pool_t pool, const void* q_emb, const float* q_joints, int32_t nq,
+                       int32_t k, float threshold, float gate_radius, int64_t* out_index,
+                       float* out_score, uint8_t* out_hit, void* stream);
+
+/* Number of rows appended so far (global).  Host-side counter, no sync. */
+ams_status_t ams_pool_size(ams_pool_t pool, int64_t* n);
+
+/* Synchronises the device, destroys the NCCL communicator (collective if world > 1)
+ * and frees everything.  NULL is a no-op. */
+ams_status_t ams_pool_destroy(ams_pool_t pool);
+
+/* Static string for a status code. */
+const char* ams_status_string(ams_status_t st);
+
+/* ---- instrumentation (bench / tests; not part of the matching semantics) ---- */
+
+/* enable != 0: ams_match records CUDA events (on the caller's stream) around its
+ * dominant kernel (the tcgen05 match kernel for bf16, the exact SIMT kernel for fp32). */
+ams_status_t ams_pool_set_profiling(ams_pool_t pool, int32_t enable);
+
+/* Waits for the recorded events and returns the summed duration (ms) and number of
+ * dominant-kernel launches since the last read, then clears them. */
+ams_status_t ams_pool_read_profile(ams_pool_t pool, double* kernel_ms, int64_t* kernel_launches);
+
+/* Total number of CUDA kernels this pool has launched (all entry points). */
+ams_status_t ams_pool_launch_count(ams_pool_t pool, int64_t* launches);
+
+/* Describes the last ams_match launch plan: number of row splits, partial lists per
+ * query, grid size, dominant-kernel id (0 = fp32 SIMT, 1 = tcgen05). Any pointer may
+ * be NULL. */
+ams_status_t ams_pool_last_plan(ams_pool_t pool, int32_t* splits, int32_t* partials,
+                                int32_t* grid, int32_t* kernel_id);
+
+/* Shard map (host-only, no device work): owner rank and local row of a global ordinal,
+ * for a pool of `capacity` rows over `world` ranks with block size `shard_block`
+ * (0 = contiguous).  Returns AMS_ERR_INVALID_ARGUMENT on bad arguments. */
+ams_status_t ams_shard_locate(int64_t capacity, int32_t world, int64_t shard_block,
+                              int64_t global_index, int32_t* owner, int64_t* local_row);
+
+/* Rows of the global range [0, capacity) owned by `rank` (its shard capacity). */
+ams_status_t ams_shard_capacity(int64_t capacity, int32_t world, int64_t shard_block,
+                                int32_t rank, int64_t* rows);
+
+int32_t ams_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* AMS_H_ */

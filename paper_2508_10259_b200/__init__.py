@@ -1,0 +1,251 @@
+"""B200-native action-context matching (AMS, arXiv 2508.10259) -- Python binding.
+
+A thin ctypes layer over ``libams.so`` (include/ams.h).  Functions carry the C ABI
+names and only marshal arguments: every step of the path runs in the CUDA kernels
+of the library.  There is no CPU fallback: importing this package without the built
+library raises, and every call that fails raises ``AmsError``.
+
+Buffers may be passed as torch tensors (host or CUDA), numpy arrays (host) or raw
+integer pointers.  Streams are torch.cuda.Stream objects, raw ``cudaStream_t``
+integers, or None (the current torch stream when torch is importable, else the
+legacy default stream).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libams.so")
+
+AMS_OK = 0
+AMS_DTYPE_BF16 = 0
+AMS_DTYPE_FP32 = 1
+STATUS = {0: "AMS_OK", 1: "AMS_ERR_INVALID_ARGUMENT", 2: "AMS_ERR_CAPACITY", 3: "AMS_ERR_OUT_OF_MEMORY",
+          4: "AMS_ERR_CUDA", 5: "AMS_ERR_NCCL", 6: "AMS_ERR_UNSUPPORTED", 7: "AMS_ERR_INTERNAL"}
+
+# Every symbol include/ams.h declares (tests check the library exports all of them).
+EXPORTS = ("ams_get_nccl_unique_id", "ams_pool_create", "ams_pool_append", "ams_match", "ams_pool_size",
+           "ams_pool_destroy", "ams_status_string", "ams_pool_set_profiling", "ams_pool_read_profile",
+           "ams_pool_launch_count", "ams_pool_last_plan", "ams_shard_locate", "ams_shard_capacity",
+           "ams_abi_version")
+
+
+class AmsError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        super().__init__(f"{what} failed: {STATUS.get(status, status)}")
+        self.status = status
+
+
+class ams_pool_config_t(ctypes.Structure):
+    _fields_ = [("dim", ctypes.c_int32), ("joint_dim", ctypes.c_int32), ("dtype", ctypes.c_int32),
+                ("capacity", ctypes.c_int64), ("max_queries", ctypes.c_int32), ("max_k", ctypes.c_int32),
+                ("device", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
+                ("nccl_id", ctypes.c_void_p), ("shard_block", ctypes.c_int64)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2508_10259_b200.build` "
+                          "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    V, I32, I64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+    sig = {
+        "ams_get_nccl_unique_id": [V],
+        "ams_pool_create": [ctypes.POINTER(ams_pool_config_t), ctypes.POINTER(V)],
+        "ams_pool_append": [V, V, V, I64, ctypes.POINTER(I64), V],
+        "ams_match": [V, V, V, I32, I32, ctypes.c_float, ctypes.c_float, V, V, V, V],
+        "ams_pool_size": [V, ctypes.POINTER(I64)],
+        "ams_pool_destroy": [V],
+        "ams_pool_set_profiling": [V, I32],
+        "ams_pool_read_profile": [V, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64)],
+        "ams_pool_launch_count": [V, ctypes.POINTER(I64)],
+        "ams_pool_last_plan": [V, ctypes.POINTER(I32), ctypes.POINTER(I32), ctypes.POINTER(I32),
+                               ctypes.POINTER(I32)],
+        "ams_shard_locate": [I64, I32, I64, I64, ctypes.POINTER(I32), ctypes.POINTER(I64)],
+        "ams_shard_capacity": [I64, I32, I64, I32, ctypes.POINTER(I64)],
+    }
+    for name, args in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = ctypes.c_int
+    L.ams_status_string.argtypes = [ctypes.c_int]
+    L.ams_status_string.restype = ctypes.c_char_p
+    L.ams_abi_version.argtypes = []
+    L.ams_abi_version.restype = ctypes.c_int32
+    return L
+
+
+lib = _load()
+
+
+def _check(st: int, what: str):
+    if st != AMS_OK:
+        raise AmsError(st, what)
+
+
+def _ptr(x) -> Optional[int]:
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    if hasattr(x, "data_ptr"):          # torch.Tensor
+        if not x.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return x.data_ptr()
+    if hasattr(x, "ctypes"):            # numpy.ndarray
+        if not x.flags["C_CONTIGUOUS"]:
+            raise ValueError("array must be C-contiguous")
+        return x.ctypes.data
+    raise TypeError(f"cannot take a pointer of {type(x)}")
+
+
+def _stream(s) -> Optional[int]:
+    if s is None:
+        try:
+            import torch
+            if torch.cuda.is_available() and torch.cuda.is_initialized():
+                return torch.cuda.current_stream().cuda_stream
+        except Exception:
+            pass
+        return None
+    if isinstance(s, int):
+        return s
+    return s.cuda_stream
+
+
+# ----------------------------------------------------------------------------- C ABI
+def ams_abi_version() -> int:
+    return int(lib.ams_abi_version())
+
+
+def ams_status_string(st: int) -> str:
+    return lib.ams_status_string(st).decode()
+
+
+def ams_get_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib.ams_get_nccl_unique_id(buf), "ams_get_nccl_unique_id")
+    return buf.raw
+
+
+def ams_pool_create(dim: int, joint_dim: int, capacity: int, max_queries: int, max_k: int,
+                    dtype: int = AMS_DTYPE_BF16, device: int = 0, rank: int = 0, world: int = 1,
+                    nccl_id: Optional[bytes] = None, shard_block: int = 0) -> int:
+    cfg = ams_pool_config_t(dim, joint_dim, dtype, capacity, max_queries, max_k, device, rank, world, None,
+                            shard_block)
+    idbuf = None
+    if nccl_id is not None:
+        idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+        cfg.nccl_id = ctypes.cast(idbuf, ctypes.c_void_p)
+    out = ctypes.c_void_p()
+    _check(lib.ams_pool_create(ctypes.byref(cfg), ctypes.byref(out)), "ams_pool_create")
+    return out.value
+
+
+def ams_pool_append(pool: int, emb, joints, n: int, stream=None) -> int:
+    first = ctypes.c_int64(-1)
+    _check(lib.ams_pool_append(pool, _ptr(emb), _ptr(joints), n, ctypes.byref(first), _stream(stream)),
+           "ams_pool_append")
+    return first.value
+
+
+def ams_match(pool: int, q_emb, q_joints, nq: int, k: int, threshold: float, gate_radius: float,
+              out_index, out_score, out_hit, stream=None) -> None:
+    _check(lib.ams_match(pool, _ptr(q_emb), _ptr(q_joints), nq, k, threshold, gate_radius, _ptr(out_index),
+                         _ptr(out_score), _ptr(out_hit), _stream(stream)), "ams_match")
+
+
+def ams_pool_size(pool: int) -> int:
+    n = ctypes.c_int64()
+    _check(lib.ams_pool_size(pool, ctypes.byref(n)), "ams_pool_size")
+    return n.value
+
+
+def ams_pool_destroy(pool: int) -> None:
+    _check(lib.ams_pool_destroy(pool), "ams_pool_destroy")
+
+
+def ams_pool_set_profiling(pool: int, enable: bool) -> None:
+    _check(lib.ams_pool_set_profiling(pool, 1 if enable else 0), "ams_pool_set_profiling")
+
+
+def ams_pool_read_profile(pool: int):
+    ms = ctypes.c_double()
+    n = ctypes.c_int64()
+    _check(lib.ams_pool_read_profile(pool, ctypes.byref(ms), ctypes.byref(n)), "ams_pool_read_profile")
+    return ms.value, n.value
+
+
+def ams_pool_launch_count(pool: int) -> int:
+    n = ctypes.c_int64()
+    _check(lib.ams_pool_launch_count(pool, ctypes.byref(n)), "ams_pool_launch_count")
+    return n.value
+
+
+def ams_pool_last_plan(pool: int):
+    v = [ctypes.c_int32() for _ in range(4)]
+    _check(lib.ams_pool_last_plan(pool, *[ctypes.byref(x) for x in v]), "ams_pool_last_plan")
+    return {"splits": v[0].value, "partials": v[1].value, "grid": v[2].value, "kernel_id": v[3].value}
+
+
+def ams_shard_locate(capacity: int, world: int, shard_block: int, global_index: int):
+    o, l = ctypes.c_int32(), ctypes.c_int64()
+    _check(lib.ams_shard_locate(capacity, world, shard_block, global_index, ctypes.byref(o), ctypes.byref(l)),
+           "ams_shard_locate")
+    return o.value, l.value
+
+
+def ams_shard_capacity(capacity: int, world: int, shard_block: int, rank: int) -> int:
+    n = ctypes.c_int64()
+    _check(lib.ams_shard_capacity(capacity, world, shard_block, rank, ctypes.byref(n)), "ams_shard_capacity")
+    return n.value
+
+
+# ----------------------------------------------------------------------------- convenience
+class Pool:
+    """RAII handle over an ams pool with torch CUDA output allocation (marshalling only)."""
+
+    def __init__(self, dim, joint_dim, capacity, max_queries, max_k, dtype="bf16", device=0, rank=0, world=1,
+                 nccl_id=None, shard_block=0):
+        self.dim, self.joint_dim, self.device = dim, joint_dim, device
+        self.dtype = AMS_DTYPE_BF16 if dtype in ("bf16", AMS_DTYPE_BF16) else AMS_DTYPE_FP32
+        self.handle = ams_pool_create(dim, joint_dim, capacity, max_queries, max_k, self.dtype, device, rank,
+                                      world, nccl_id, shard_block)
+
+    def append(self, emb, joints, n=None, stream=None) -> int:
+        n = emb.shape[0] if n is None else n
+        return ams_pool_append(self.handle, emb, joints, n, stream)
+
+    def match(self, q_emb, q_joints, k, threshold, gate_radius, out=None, stream=None):
+        import torch
+        nq = q_emb.shape[0]
+        if out is None:
+            dev = torch.device("cuda", self.device)
+            out = (torch.empty(nq, k, dtype=torch.int64, device=dev),
+                   torch.empty(nq, k, dtype=torch.float32, device=dev),
+                   torch.empty(nq, dtype=torch.uint8, device=dev))
+        ams_match(self.handle, q_emb, q_joints, nq, k, threshold, gate_radius, out[0], out[1], out[2], stream)
+        return out
+
+    @property
+    def size(self) -> int:
+        return ams_pool_size(self.handle)
+
+    def close(self):
+        if self.handle:
+            h, self.handle = self.handle, None
+            ams_pool_destroy(h)
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

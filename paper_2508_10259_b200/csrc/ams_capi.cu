@@ -1,0 +1,496 @@
+// ams_capi.cu -- the C ABI (include/ams.h): pool lifecycle, record, match, shard
+// exchange over NCCL, instrumentation.  Every entry point returns ams_status_t and
+// never throws.
+#include <nccl.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "ams_internal.cuh"
+
+using ams::Pool;
+
+struct ams_pool_s {
+  Pool p;
+};
+
+namespace {
+
+#define AMS_CUDA_TRY(expr)                    \
+  do {                                        \
+    cudaError_t e_ = (expr);                  \
+    if (e_ != cudaSuccess) {                  \
+      if (getenv("AMS_LOG"))                  \
+        fprintf(stderr, "[ams] %s:%d %s: %s\n", __FILE__, __LINE__, #expr, cudaGetErrorString(e_)); \
+      return fail(pool, AMS_ERR_CUDA);        \
+    }                                         \
+  } while (0)
+
+inline ams_status_t fail(ams_pool_s* pool, ams_status_t st) {
+  if (pool != nullptr && (st == AMS_ERR_CUDA || st == AMS_ERR_NCCL)) pool->p.broken = true;
+  return st;
+}
+
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                       const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                       CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                       CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled_t get_encode() {
+  static PFN_encodeTiled_t fn = nullptr;
+  if (fn == nullptr) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled_t>(f);
+  }
+  return fn;
+}
+
+// 2-D bf16 K-major tile map: rows x d, box {64, box_rows}, 128-B swizzle, OOB -> 0
+bool encode_bf16_map(CUtensorMap* m, void* base, int64_t rows, int32_t d, uint32_t box_rows) {
+  PFN_encodeTiled_t enc = get_encode();
+  if (enc == nullptr) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)d * 2};
+  cuuint32_t box[2] = {(cuuint32_t)ams::kBlockK, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+bool is_device_ptr(const void* ptr) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+size_t esize(const Pool& p) { return p.cfg.dtype == AMS_DTYPE_BF16 ? 2 : 4; }
+
+// Plan of the tcgen05 kernel: number of row splits S (units = n_qt * S, static
+// round-robin over `grid` persistent CTAs).  Minimises the busiest CTA's tile count
+// ceil(U / grid) * ceil(n_pt / S); ties -> fewer splits (fewer partial lists).
+void plan_tc(const Pool& p, int nq, int KT, int& S, int& grid) {
+  const int n_qt = (nq + ams::kBlockM - 1) / ams::kBlockM;
+  const int64_t n_pt = (p.local + ams::kBlockN - 1) / ams::kBlockN;
+  const int sms = p.num_sms;
+  const int64_t nq_pad = (int64_t)n_qt * ams::kBlockM;
+  int64_t s_cap = std::max<int64_t>(1, p.part_cap / (nq_pad * ams::kEpiHalves * KT));
+  s_cap = std::min<int64_t>(s_cap, std::max<int64_t>(1, n_pt));
+  s_cap = std::min<int64_t>(s_cap, std::max<int64_t>(1, (int64_t)64 * sms / n_qt + 1));
+  int64_t best_cost = LLONG_MAX;
+  int best = 1;
+  for (int64_t s = 1; s <= s_cap; ++s) {
+    const int64_t U = (int64_t)n_qt * s;
+    const int64_t waves = (U + sms - 1) / sms;
+    const int64_t per = (n_pt + s - 1) / s;
+    const int64_t cost = waves * per * 64 + s;  // + small penalty per split (merge work)
+    if (cost < best_cost) {
+      best_cost = cost;
+      best = (int)s;
+    }
+  }
+  S = best;
+  grid = (int)std::min<int64_t>((int64_t)n_qt * S, sms);
+}
+
+void plan_simt(const Pool& p, int nq, int KT, int& S) {
+  const int64_t per_split = (int64_t)nq * ams::kSimtThreads * KT;
+  int64_t s_cap = std::max<int64_t>(1, p.part_cap / per_split);
+  int64_t want = std::max<int64_t>(1, (2 * p.num_sms + nq - 1) / nq);
+  want = std::min<int64_t>(want, std::max<int64_t>(1, p.local / ams::kSimtThreads));
+  S = (int)std::max<int64_t>(1, std::min(want, s_cap));
+}
+
+void free_all(Pool& p) {
+  void* ptrs[] = {p.emb, p.inv_norm, p.joints, p.q_stage, p.q_inv, p.q_joints, p.q_joints_raw,
+                  p.part_s, p.part_i, p.shard_s, p.shard_i, p.gath_s, p.gath_i, p.stage_emb,
+                  p.stage_joints};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+  for (auto& e : p.ev_free) cudaEventDestroy(e);
+  for (auto& e : p.ev_pending) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  p.ev_free.clear();
+  p.ev_pending.clear();
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t ams_abi_version(void) { return AMS_ABI_VERSION; }
+
+const char* ams_status_string(ams_status_t st) {
+  switch (st) {
+    case AMS_OK: return "AMS_OK";
+    case AMS_ERR_INVALID_ARGUMENT: return "AMS_ERR_INVALID_ARGUMENT";
+    case AMS_ERR_CAPACITY: return "AMS_ERR_CAPACITY";
+    case AMS_ERR_OUT_OF_MEMORY: return "AMS_ERR_OUT_OF_MEMORY";
+    case AMS_ERR_CUDA: return "AMS_ERR_CUDA";
+    case AMS_ERR_NCCL: return "AMS_ERR_NCCL";
+    case AMS_ERR_UNSUPPORTED: return "AMS_ERR_UNSUPPORTED";
+    case AMS_ERR_INTERNAL: return "AMS_ERR_INTERNAL";
+  }
+  return "AMS_ERR_UNKNOWN";
+}
+
+ams_status_t ams_shard_locate(int64_t capacity, int32_t world, int64_t shard_block, int64_t global_index,
+                              int32_t* owner, int64_t* local_row) {
+  if (capacity < 0 || world < 1 || shard_block < 0 || global_index < 0 || global_index >= capacity)
+    return AMS_ERR_INVALID_ARGUMENT;
+  const int64_t B = ams::shard_block_size(capacity, world, shard_block);
+  if (owner) *owner = ams::shard_owner(global_index, world, B);
+  if (local_row) *local_row = ams::shard_local(global_index, world, B);
+  return AMS_OK;
+}
+
+ams_status_t ams_shard_capacity(int64_t capacity, int32_t world, int64_t shard_block, int32_t rank,
+                                int64_t* rows) {
+  if (capacity < 0 || world < 1 || shard_block < 0 || rank < 0 || rank >= world || rows == nullptr)
+    return AMS_ERR_INVALID_ARGUMENT;
+  const int64_t B = ams::shard_block_size(capacity, world, shard_block);
+  *rows = ams::shard_count(capacity, rank, world, B);
+  return AMS_OK;
+}
+
+ams_status_t ams_get_nccl_unique_id(void* out128) {
+  if (out128 == nullptr) return AMS_ERR_INVALID_ARGUMENT;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return AMS_ERR_NCCL;
+  memcpy(out128, &id, sizeof id);
+  return AMS_OK;
+}
+
+ams_status_t ams_pool_create(const ams_pool_config_t* cfg, ams_pool_t* out) {
+  ams_pool_s* pool = nullptr;
+  if (cfg == nullptr || out == nullptr) return AMS_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  const auto& c = *cfg;
+  if (c.dim < 64 || c.dim > 16384 || c.dim % 64 != 0) return AMS_ERR_INVALID_ARGUMENT;
+  if (c.joint_dim < 1 || c.joint_dim > 16) return AMS_ERR_INVALID_ARGUMENT;
+  if (c.dtype != AMS_DTYPE_BF16 && c.dtype != AMS_DTYPE_FP32) return AMS_ERR_INVALID_ARGUMENT;
+  if (c.capacity < 0 || c.max_queries < 1 || c.max_k < 1 || c.max_k > 64) return AMS_ERR_INVALID_ARGUMENT;
+  if (c.world < 1 || c.world > 64 || c.rank < 0 || c.rank >= c.world || c.shard_block < 0)
+    return AMS_ERR_INVALID_ARGUMENT;
+  if (c.world > 1 && c.nccl_id == nullptr) return AMS_ERR_INVALID_ARGUMENT;
+
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || c.device < 0 || c.device >= ndev) {
+    cudaGetLastError();
+    return AMS_ERR_INVALID_ARGUMENT;
+  }
+  cudaDeviceProp prop{};
+  if (cudaGetDeviceProperties(&prop, c.device) != cudaSuccess) return AMS_ERR_CUDA;
+  if (prop.major != 10 || prop.minor != 0) return AMS_ERR_UNSUPPORTED;  // built for sm_100a only
+  if (cudaSetDevice(c.device) != cudaSuccess) return AMS_ERR_CUDA;
+
+  pool = new (std::nothrow) ams_pool_s;
+  if (pool == nullptr) return AMS_ERR_OUT_OF_MEMORY;
+  Pool& p = pool->p;
+  p.cfg = c;
+  p.cfg.nccl_id = nullptr;
+  p.num_sms = prop.multiProcessorCount;
+  p.JP = c.joint_dim <= 4 ? 4 : c.joint_dim <= 8 ? 8 : 16;
+  p.B = ams::shard_block_size(c.capacity, c.world, c.shard_block);
+  p.cap_shard = ams::shard_count(c.capacity, c.rank, c.world, p.B);
+  if (p.cap_shard >= ((int64_t)1 << 31) - ams::kRowAlign) {
+    delete pool;
+    return AMS_ERR_INVALID_ARGUMENT;  // local row ids are int32 inside the kernels
+  }
+  p.cap_pad = round_up(std::max<int64_t>(p.cap_shard, 1), ams::kRowAlign);
+  p.KT_max = ams::pick_KT(c.max_k);
+  p.q_pad = (int32_t)round_up(c.max_queries, ams::kBlockM);
+  const size_t es = esize(p);
+  const int32_t d = c.dim;
+
+  auto alloc = [&](void** ptr, size_t bytes) -> bool {
+    if (cudaMalloc(ptr, std::max<size_t>(bytes, 16)) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return cudaMemset(*ptr, 0, std::max<size_t>(bytes, 16)) == cudaSuccess;
+  };
+  // partial-list workspace: tcgen05 path needs q_pad * 2 * S * KT, S bounded by the
+  // pool's tile count and by ~64 waves of units; SIMT path q * 128 * S * KT.
+  const int64_t n_pt_max = p.cap_pad / ams::kBlockN;
+  int64_t part = 0;
+  if (c.dtype == AMS_DTYPE_BF16) {
+    const int64_t s_max = std::min<int64_t>(n_pt_max, (int64_t)64 * p.num_sms + 1);
+    part = std::min<int64_t>((int64_t)p.q_pad * s_max, (int64_t)ams::kBlockM * 64 * p.num_sms + p.q_pad) *
+           ams::kEpiHalves * p.KT_max;
+  } else {
+    const int64_t s_max = std::max<int64_t>(1, std::min<int64_t>(p.cap_pad / ams::kSimtThreads, 2 * p.num_sms));
+    part = std::min<int64_t>((int64_t)c.max_queries * s_max, (int64_t)c.max_queries + 2 * p.num_sms) *
+           ams::kSimtThreads * p.KT_max;
+  }
+  p.part_cap = part;
+  p.stage_rows = std::min<int64_t>(std::max<int64_t>(c.capacity, 1), 65536);
+  bool ok = alloc(&p.emb, (size_t)p.cap_pad * d * es) && alloc((void**)&p.inv_norm, (size_t)p.cap_pad * 4) &&
+            alloc((void**)&p.joints, (size_t)p.cap_pad * p.JP * 4) &&
+            alloc(&p.q_stage, (size_t)p.q_pad * d * es) && alloc((void**)&p.q_inv, (size_t)p.q_pad * 4) &&
+            alloc((void**)&p.q_joints, (size_t)p.q_pad * p.JP * 4) &&
+            alloc((void**)&p.q_joints_raw, (size_t)c.max_queries * c.joint_dim * 4) &&
+            alloc((void**)&p.part_s, (size_t)part * 4) && alloc((void**)&p.part_i, (size_t)part * 4) &&
+            alloc((void**)&p.shard_s, (size_t)c.max_queries * c.max_k * 4) &&
+            alloc((void**)&p.shard_i, (size_t)c.max_queries * c.max_k * 8) &&
+            alloc(&p.stage_emb, (size_t)p.stage_rows * d * es) &&
+            alloc((void**)&p.stage_joints, (size_t)p.stage_rows * c.joint_dim * 4);
+  if (ok && c.world > 1)
+    ok = alloc((void**)&p.gath_s, (size_t)c.world * c.max_queries * c.max_k * 4) &&
+         alloc((void**)&p.gath_i, (size_t)c.world * c.max_queries * c.max_k * 8);
+  if (!ok) {
+    free_all(p);
+    delete pool;
+    return AMS_ERR_OUT_OF_MEMORY;
+  }
+  if (c.dtype == AMS_DTYPE_BF16) {
+    if (!encode_bf16_map(&p.tmap_pool, p.emb, p.cap_pad, d, ams::kBlockN) ||
+        !encode_bf16_map(&p.tmap_q, p.q_stage, p.q_pad, d, ams::kBlockM)) {
+      free_all(p);
+      delete pool;
+      return AMS_ERR_CUDA;
+    }
+  }
+  if (cudaDeviceSynchronize() != cudaSuccess) {
+    free_all(p);
+    delete pool;
+    return AMS_ERR_CUDA;
+  }
+  if (c.world > 1) {
+    ncclUniqueId id;
+    memcpy(&id, c.nccl_id, sizeof id);
+    ncclComm_t comm;
+    if (ncclCommInitRank(&comm, c.world, id, c.rank) != ncclSuccess) {
+      free_all(p);
+      delete pool;
+      return AMS_ERR_NCCL;
+    }
+    p.nccl_comm = comm;
+  }
+  *out = pool;
+  return AMS_OK;
+}
+
+ams_status_t ams_pool_append(ams_pool_t pool, const void* emb, const float* joints, int64_t n,
+                             int64_t* first_index, void* stream) {
+  if (pool == nullptr || n < 0) return AMS_ERR_INVALID_ARGUMENT;
+  Pool& p = pool->p;
+  if (p.broken) return AMS_ERR_CUDA;
+  if (n > 0 && (emb == nullptr || joints == nullptr)) return AMS_ERR_INVALID_ARGUMENT;
+  if (n > p.cfg.capacity - p.size) return AMS_ERR_CAPACITY;
+  if (first_index) *first_index = p.size;
+  if (n == 0) return AMS_OK;
+  AMS_CUDA_TRY(cudaSetDevice(p.cfg.device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t es = esize(p);
+  const size_t row_bytes = (size_t)p.cfg.dim * es;
+  const bool dev_e = is_device_ptr(emb), dev_j = is_device_ptr(joints);
+  for (int64_t off = 0; off < n;) {
+    const int64_t m = (dev_e && dev_j) ? n - off : std::min<int64_t>(n - off, p.stage_rows);
+    const void* e_src = static_cast<const uint8_t*>(emb) + off * row_bytes;
+    const float* j_src = joints + off * p.cfg.joint_dim;
+    if (!dev_e) {
+      AMS_CUDA_TRY(cudaMemcpyAsync(p.stage_emb, e_src, m * row_bytes, cudaMemcpyDefault, s));
+      e_src = p.stage_emb;
+    }
+    if (!dev_j) {
+      AMS_CUDA_TRY(cudaMemcpyAsync(p.stage_joints, j_src, m * p.cfg.joint_dim * 4, cudaMemcpyDefault, s));
+      j_src = p.stage_joints;
+    }
+    AMS_CUDA_TRY(ams::launch_append(p, e_src, j_src, m, p.size + off, s));
+    off += m;
+  }
+  p.size += n;
+  p.local = ams::shard_count(p.size, p.cfg.rank, p.cfg.world, p.B);
+  return AMS_OK;
+}
+
+ams_status_t ams_match(ams_pool_t pool, const void* q_emb, const float* q_joints, int32_t nq, int32_t k,
+                       float threshold, float gate_radius, int64_t* out_index, float* out_score,
+                       uint8_t* out_hit, void* stream) {
+  if (pool == nullptr) return AMS_ERR_INVALID_ARGUMENT;
+  Pool& p = pool->p;
+  if (p.broken) return AMS_ERR_CUDA;
+  if (q_emb == nullptr || q_joints == nullptr || out_index == nullptr || out_score == nullptr ||
+      out_hit == nullptr)
+    return AMS_ERR_INVALID_ARGUMENT;
+  if (nq < 1 || nq > p.cfg.max_queries || k < 1 || k > p.cfg.max_k) return AMS_ERR_INVALID_ARGUMENT;
+  if (std::isnan(threshold) || std::isnan(gate_radius) || gate_radius < 0.0f) return AMS_ERR_INVALID_ARGUMENT;
+  AMS_CUDA_TRY(cudaSetDevice(p.cfg.device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+
+  ams::MatchArgs a{};
+  a.nq = nq;
+  a.k = k;
+  a.KT = ams::pick_KT(k);
+  {
+    volatile float g = gate_radius;
+    a.g2 = g * g;  // fp32(gamma^2), reading R3
+  }
+  a.gated = std::isinf(a.g2) ? 0 : 1;
+  a.threshold = threshold;
+
+  // stage queries (host sources are copied first; device sources are read in place)
+  const size_t es = esize(p);
+  const void* q_src = q_emb;
+  const float* qj_src = q_joints;
+  if (!is_device_ptr(q_emb)) {
+    AMS_CUDA_TRY(cudaMemcpyAsync(p.q_stage, q_emb, (size_t)nq * p.cfg.dim * es, cudaMemcpyDefault, s));
+    q_src = p.q_stage;
+  }
+  if (!is_device_ptr(q_joints)) {
+    AMS_CUDA_TRY(cudaMemcpyAsync(p.q_joints_raw, q_joints, (size_t)nq * p.cfg.joint_dim * 4, cudaMemcpyDefault, s));
+    qj_src = p.q_joints_raw;
+  }
+  AMS_CUDA_TRY(ams::launch_query_prep(p, q_src, qj_src, nq, s));
+
+  const bool multi = p.cfg.world > 1;
+  float* shard_s = multi ? p.shard_s : out_score;
+  int64_t* shard_i = multi ? p.shard_i : out_index;
+  uint8_t* shard_hit = multi ? nullptr : out_hit;
+
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (p.profiling) {
+    for (int t = 0; t < 2; ++t) {
+      cudaEvent_t ev;
+      if (!p.ev_free.empty()) {
+        ev = p.ev_free.back();
+        p.ev_free.pop_back();
+      } else {
+        AMS_CUDA_TRY(cudaEventCreate(&ev));
+      }
+      (t == 0 ? e0 : e1) = ev;
+    }
+  }
+
+  int32_t P = 0;
+  if (p.local > 0) {
+    if (p.cfg.dtype == AMS_DTYPE_FP32) {
+      int S;
+      plan_simt(p, nq, a.KT, S);
+      P = S * ams::kSimtThreads;
+      if (e0) AMS_CUDA_TRY(cudaEventRecord(e0, s));
+      AMS_CUDA_TRY(ams::launch_match_simt(p, a, S, s));
+      if (e1) AMS_CUDA_TRY(cudaEventRecord(e1, s));
+      p.last_splits = S;
+      p.last_grid = nq * S;
+      p.last_kernel = 0;
+    } else {
+      int S, grid;
+      plan_tc(p, nq, a.KT, S, grid);
+      P = S * ams::kEpiHalves;
+      if (e0) AMS_CUDA_TRY(cudaEventRecord(e0, s));
+      AMS_CUDA_TRY(ams::launch_match_tc(p, a, S, grid, s));
+      if (e1) AMS_CUDA_TRY(cudaEventRecord(e1, s));
+      p.last_splits = S;
+      p.last_grid = grid;
+      p.last_kernel = 1;
+    }
+    p.last_partials = P;
+  }
+  if (e0) {
+    if (p.local > 0) {
+      p.ev_pending.emplace_back(e0, e1);
+    } else {
+      p.ev_free.push_back(e0);
+      p.ev_free.push_back(e1);
+    }
+  }
+  AMS_CUDA_TRY(ams::launch_merge_partials(p, a, P, shard_s, shard_i, shard_hit, s));
+
+  if (multi) {
+    ncclComm_t comm = static_cast<ncclComm_t>(p.nccl_comm);
+    const size_t cnt = (size_t)nq * k;
+    if (ncclGroupStart() != ncclSuccess) return fail(pool, AMS_ERR_NCCL);
+    if (ncclAllGather(p.shard_s, p.gath_s, cnt, ncclFloat32, comm, s) != ncclSuccess ||
+        ncclAllGather(p.shard_i, p.gath_i, cnt, ncclInt64, comm, s) != ncclSuccess) {
+      ncclGroupEnd();
+      return fail(pool, AMS_ERR_NCCL);
+    }
+    if (ncclGroupEnd() != ncclSuccess) return fail(pool, AMS_ERR_NCCL);
+    AMS_CUDA_TRY(ams::launch_merge_shards(p, a, p.cfg.world, k, p.gath_s, p.gath_i, out_score, out_index,
+                                          out_hit, s));
+  }
+  return AMS_OK;
+}
+
+ams_status_t ams_pool_size(ams_pool_t pool, int64_t* n) {
+  if (pool == nullptr || n == nullptr) return AMS_ERR_INVALID_ARGUMENT;
+  *n = pool->p.size;
+  return AMS_OK;
+}
+
+ams_status_t ams_pool_destroy(ams_pool_t pool) {
+  if (pool == nullptr) return AMS_OK;
+  Pool& p = pool->p;
+  ams_status_t st = AMS_OK;
+  cudaSetDevice(p.cfg.device);
+  if (cudaDeviceSynchronize() != cudaSuccess) st = AMS_ERR_CUDA;
+  if (p.nccl_comm != nullptr) {
+    if (ncclCommDestroy(static_cast<ncclComm_t>(p.nccl_comm)) != ncclSuccess && st == AMS_OK) st = AMS_ERR_NCCL;
+  }
+  free_all(p);
+  delete pool;
+  return st;
+}
+
+ams_status_t ams_pool_set_profiling(ams_pool_t pool, int32_t enable) {
+  if (pool == nullptr) return AMS_ERR_INVALID_ARGUMENT;
+  pool->p.profiling = enable != 0;
+  return AMS_OK;
+}
+
+ams_status_t ams_pool_read_profile(ams_pool_t pool, double* kernel_ms, int64_t* kernel_launches) {
+  if (pool == nullptr) return AMS_ERR_INVALID_ARGUMENT;
+  Pool& p = pool->p;
+  double tot = 0.0;
+  int64_t n = 0;
+  for (auto& e : p.ev_pending) {
+    if (cudaEventSynchronize(e.second) != cudaSuccess) return fail(pool, AMS_ERR_CUDA);
+    float ms = 0.0f;
+    if (cudaEventElapsedTime(&ms, e.first, e.second) != cudaSuccess) return fail(pool, AMS_ERR_CUDA);
+    tot += ms;
+    ++n;
+    p.ev_free.push_back(e.first);
+    p.ev_free.push_back(e.second);
+  }
+  p.ev_pending.clear();
+  if (kernel_ms) *kernel_ms = tot;
+  if (kernel_launches) *kernel_launches = n;
+  return AMS_OK;
+}
+
+ams_status_t ams_pool_launch_count(ams_pool_t pool, int64_t* launches) {
+  if (pool == nullptr || launches == nullptr) return AMS_ERR_INVALID_ARGUMENT;
+  *launches = pool->p.launches;
+  return AMS_OK;
+}
+
+ams_status_t ams_pool_last_plan(ams_pool_t pool, int32_t* splits, int32_t* partials, int32_t* grid,
+                                int32_t* kernel_id) {
+  if (pool == nullptr) return AMS_ERR_INVALID_ARGUMENT;
+  const Pool& p = pool->p;
+  if (splits) *splits = p.last_splits;
+  if (partials) *partials = p.last_partials;
+  if (grid) *grid = p.last_grid;
+  if (kernel_id) *kernel_id = p.last_kernel;
+  return AMS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,126 @@
+// ams_internal.cuh -- pool state, shard map and kernel launchers shared by the
+// C ABI (ams_capi.cu) and the kernels (ams_kernels.cu, ams_match_tc.cu).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <vector>
+
+#include "../../include/ams.h"
+
+namespace ams {
+
+// --------------------------------------------------------------------------- tiling
+constexpr int kBlockM = 128;     // queries per tcgen05 tile (TMEM lanes)
+constexpr int kBlockN = 256;     // pool rows per tcgen05 tile (TMEM columns per buffer)
+constexpr int kBlockK = 64;      // bf16 elements per stage row = one 128-B swizzle atom
+constexpr int kRowAlign = 256;   // shard storage is padded to a multiple of this
+constexpr int kEpiHalves = 2;    // epilogue warps per TMEM lane group (column halves)
+constexpr int kSimtThreads = 128;
+
+// --------------------------------------------------------------------------- shard map
+// Block-cyclic: global ordinal o -> block b = o / B, owner b % G, local (b / G) * B + o % B.
+// The contiguous map is the special case B = ceil(capacity / G).
+__host__ __device__ inline int64_t shard_block_size(int64_t capacity, int32_t world, int64_t block) {
+  if (block > 0) return block;
+  int64_t b = (capacity + world - 1) / world;
+  return b > 0 ? b : 1;
+}
+__host__ __device__ inline int32_t shard_owner(int64_t o, int32_t world, int64_t B) {
+  return static_cast<int32_t>((o / B) % world);
+}
+__host__ __device__ inline int64_t shard_local(int64_t o, int32_t world, int64_t B) {
+  return (o / B / world) * B + o % B;
+}
+__host__ __device__ inline int64_t shard_global(int64_t l, int32_t rank, int32_t world, int64_t B) {
+  return ((l / B) * world + rank) * B + l % B;
+}
+// rows of [0, n) owned by rank
+__host__ __device__ inline int64_t shard_count(int64_t n, int32_t rank, int32_t world, int64_t B) {
+  int64_t full = n / B, rem = n % B;
+  int64_t blocks = full / world + ((full % world) > rank ? 1 : 0);
+  return blocks * B + ((full % world) == rank ? rem : 0);
+}
+
+// --------------------------------------------------------------------------- pool
+struct Pool {
+  ams_pool_config_t cfg{};
+  int32_t JP = 4;             // padded joint stride (4, 8 or 16)
+  int64_t B = 1;              // shard block
+  int64_t cap_shard = 0;      // rows this rank can hold
+  int64_t cap_pad = 0;        // allocated rows (multiple of kRowAlign)
+  int64_t size = 0;           // global rows appended
+  int64_t local = 0;          // rows held by this rank
+  int32_t num_sms = 148;
+  int32_t KT_max = 8;
+  bool broken = false;
+
+  // shard storage
+  void* emb = nullptr;        // [cap_pad, d] bf16 or fp32
+  float* inv_norm = nullptr;  // [cap_pad]
+  float* joints = nullptr;    // [cap_pad, JP]
+
+  // query workspace
+  int32_t q_pad = 0;          // max_queries rounded up to kBlockM
+  void* q_stage = nullptr;    // [q_pad, d]
+  float* q_inv = nullptr;     // [q_pad]
+  float* q_joints = nullptr;  // [q_pad, JP]
+  float* q_joints_raw = nullptr;  // [max_queries, J] host-staged joints
+
+  // partial top-k lists [nq][P][KT]
+  int64_t part_cap = 0;       // entries
+  float* part_s = nullptr;
+  int32_t* part_i = nullptr;
+  int32_t P_max = 0;
+
+  // shard top-k and the all-gathered lists
+  float* shard_s = nullptr;      // [max_q, max_k]
+  int64_t* shard_i = nullptr;
+  float* gath_s = nullptr;       // [world, max_q, max_k]
+  int64_t* gath_i = nullptr;
+
+  // append staging (host sources)
+  int64_t stage_rows = 0;
+  void* stage_emb = nullptr;
+  float* stage_joints = nullptr;
+
+  CUtensorMap tmap_pool{};   // bf16 pool [cap_pad, d], box {64, 256}, SW128
+  CUtensorMap tmap_q{};      // bf16 queries [q_pad, d], box {64, 128}, SW128
+
+  void* nccl_comm = nullptr;  // ncclComm_t
+
+  // instrumentation
+  bool profiling = false;
+  std::vector<cudaEvent_t> ev_free;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pending;
+  int64_t launches = 0;
+  int32_t last_splits = 0, last_partials = 0, last_grid = 0, last_kernel = -1;
+};
+
+// --------------------------------------------------------------------------- launchers
+// All return cudaError_t of the launch; `launches` is incremented per kernel launched.
+struct MatchArgs {
+  int32_t nq, k, KT;
+  float g2;           // fp32(gate_radius^2); +inf disables the gate
+  int32_t gated;      // g2 < +inf
+  float threshold;
+};
+
+cudaError_t launch_append(Pool& p, const void* emb_src, const float* joints_src, int64_t n_src,
+                          int64_t first_global, cudaStream_t s);
+cudaError_t launch_query_prep(Pool& p, const void* q_src, const float* qj_src, int32_t nq, cudaStream_t s);
+cudaError_t launch_match_simt(Pool& p, const MatchArgs& a, int32_t splits, cudaStream_t s);
+cudaError_t launch_match_tc(Pool& p, const MatchArgs& a, int32_t splits, int32_t grid, cudaStream_t s);
+// merge [nq][P][KT] local lists -> [nq][k] (fp32, global int64); writes hit if out_hit != null
+cudaError_t launch_merge_partials(Pool& p, const MatchArgs& a, int32_t P, float* out_s, int64_t* out_i,
+                                  uint8_t* out_hit, cudaStream_t s);
+// merge [G][nq][kin] global lists -> [nq][k] + hit
+cudaError_t launch_merge_shards(Pool& p, const MatchArgs& a, int32_t G, int32_t kin, const float* in_s,
+                                const int64_t* in_i, float* out_s, int64_t* out_i, uint8_t* out_hit,
+                                cudaStream_t s);
+
+int pick_KT(int k);
+int tc_stages(int JP);
+size_t tc_smem_bytes(int JP);
+
+}  // namespace ams

@@ -1,0 +1,342 @@
+// ams_kernels.cu -- record (append), query prep, the exact fp32 SIMT matcher and the
+// k-way merges of AMS action-context matching (3.2.1).
+#include <cuda_bf16.h>
+#include <math_constants.h>
+
+#include "ams_internal.cuh"
+#include "ams_topk.cuh"
+
+namespace ams {
+
+namespace {
+
+__device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+
+__device__ __forceinline__ double warp_sum_f64(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ---------------------------------------------------------------------------------
+// Record ("adds the unseen vector ... into the context pool").
+// One warp per source row; the rank keeps only the rows its shard map owns.
+// bf16: inv_norm = fp32(1 / sqrt(sum x^2 in fp64)) over the STORED values.
+// fp32: canonical ss = fmaf(x_t, x_t, ss), t ascending; inv = 1.0f / sqrtf(ss).
+// ---------------------------------------------------------------------------------
+template <bool BF16>
+__global__ void append_kernel(const void* __restrict__ src, const float* __restrict__ jsrc, int64_t n,
+                              int64_t first_global, int32_t d, int32_t J, int32_t JP, int32_t rank,
+                              int32_t world, int64_t B, void* __restrict__ emb, float* __restrict__ inv_norm,
+                              float* __restrict__ joints) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= n) return;
+  const int64_t o = first_global + r;
+  if (shard_owner(o, world, B) != rank) return;
+  const int64_t l = shard_local(o, world, B);
+  if (BF16) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(src) + r * d);
+    uint4* d4 = reinterpret_cast<uint4*>(static_cast<uint16_t*>(emb) + l * d);
+    double ss = 0.0;
+    for (int c = lane; c < d / 8; c += 32) {
+      const uint4 w = s4[c];
+      d4[c] = w;
+      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double a = bf16_lo(ws[q]), b = bf16_hi(ws[q]);
+        ss += a * a;
+        ss += b * b;
+      }
+    }
+    ss = warp_sum_f64(ss);
+    if (lane == 0) inv_norm[l] = ss > 0.0 ? __double2float_rn(1.0 / sqrt(ss)) : 0.0f;
+  } else {
+    const float* s = static_cast<const float*>(src) + r * d;
+    float* e = static_cast<float*>(emb) + l * d;
+    for (int c = lane; c < d; c += 32) e[c] = s[c];
+    if (lane == 0) {
+      float ss = 0.0f;
+      for (int t = 0; t < d; ++t) ss = __fmaf_rn(s[t], s[t], ss);
+      inv_norm[l] = ss > 0.0f ? __fdiv_rn(1.0f, __fsqrt_rn(ss)) : 0.0f;
+    }
+  }
+  if (lane < JP) joints[l * JP + lane] = lane < J ? jsrc[r * J + lane] : 0.0f;
+}
+
+// ---------------------------------------------------------------------------------
+// Query prep: stage the query rows, inv_q, zero-padded joints.  One warp per query.
+// ---------------------------------------------------------------------------------
+template <bool BF16>
+__global__ void query_prep_kernel(const void* __restrict__ src, const float* __restrict__ jsrc, int32_t nq,
+                                  int32_t d, int32_t J, int32_t JP, void* __restrict__ q_stage,
+                                  float* __restrict__ q_inv, float* __restrict__ q_joints) {
+  const int lane = threadIdx.x & 31;
+  const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (q >= nq) return;
+  if (BF16) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(src) + (int64_t)q * d);
+    uint4* d4 = reinterpret_cast<uint4*>(static_cast<uint16_t*>(q_stage) + (int64_t)q * d);
+    double ss = 0.0;
+    for (int c = lane; c < d / 8; c += 32) {
+      const uint4 w = s4[c];
+      if (s4 != d4) d4[c] = w;
+      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const double a = bf16_lo(ws[k]), b = bf16_hi(ws[k]);
+        ss += a * a;
+        ss += b * b;
+      }
+    }
+    ss = warp_sum_f64(ss);
+    if (lane == 0) q_inv[q] = ss > 0.0 ? __double2float_rn(1.0 / sqrt(ss)) : 0.0f;
+  } else {
+    const float* s = static_cast<const float*>(src) + (int64_t)q * d;
+    float* e = static_cast<float*>(q_stage) + (int64_t)q * d;
+    if (s != e)
+      for (int c = lane; c < d; c += 32) e[c] = s[c];
+    if (lane == 0) {
+      float ss = 0.0f;
+      for (int t = 0; t < d; ++t) ss = __fmaf_rn(s[t], s[t], ss);
+      q_inv[q] = ss > 0.0f ? __fdiv_rn(1.0f, __fsqrt_rn(ss)) : 0.0f;
+    }
+  }
+  if (lane < JP) q_joints[(int64_t)q * JP + lane] = lane < J ? jsrc[(int64_t)q * J + lane] : 0.0f;
+}
+
+// ---------------------------------------------------------------------------------
+// Exact fp32 matcher (the bit-exact config, BASELINE.json configs[0]).
+// Block = (query, row split); thread t scans rows lo+t, lo+t+128, ... in increasing
+// order: canonical gate (fp32 RN sub, fmaf chain), canonical dot (fmaf chain, t
+// ascending), s = (acc * inv_q) * inv_e; running top-k in registers.  Partial list
+// p = split * 128 + t of query q lands at part[(q * P + p) * KT].
+// ---------------------------------------------------------------------------------
+template <int KT>
+__global__ void __launch_bounds__(kSimtThreads)
+    match_simt_f32_kernel(const float* __restrict__ emb, const float* __restrict__ inv_e,
+                          const float* __restrict__ pj, int64_t L, const float* __restrict__ q,
+                          const float* __restrict__ inv_q, const float* __restrict__ qj, int32_t d, int32_t JP,
+                          int32_t S, int32_t k, float g2, int32_t gated, float* __restrict__ part_s,
+                          int32_t* __restrict__ part_i, int32_t P) {
+  extern __shared__ float qs[];
+  const int qi = blockIdx.x / S;
+  const int sp = blockIdx.x % S;
+  for (int t = threadIdx.x; t < d; t += blockDim.x) qs[t] = q[(int64_t)qi * d + t];
+  float r[16];
+#pragma unroll
+  for (int t = 0; t < 16; ++t) r[t] = t < JP ? qj[(int64_t)qi * JP + t] : 0.0f;
+  const float iq = inv_q[qi];
+  __syncthreads();
+  const int64_t lo = L * sp / S, hi = L * (sp + 1) / S;
+  TopK<KT, int32_t> top;
+  top.init(true);
+  for (int64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) {
+    if (gated) {
+      float ds = 0.0f;
+      const float* p = pj + j * JP;
+#pragma unroll
+      for (int t = 0; t < 16; ++t)
+        if (t < JP) {
+          const float df = __fsub_rn(r[t], p[t]);
+          ds = __fmaf_rn(df, df, ds);
+        }
+      if (!(ds <= g2)) continue;
+    }
+    const float* e = emb + j * d;
+    float acc = 0.0f;
+    for (int t = 0; t < d; ++t) acc = __fmaf_rn(qs[t], e[t], acc);
+    const float s = __fmul_rn(__fmul_rn(acc, iq), inv_e[j]);
+    if (s > top.kth_s) top.insert_monotone(s, (int32_t)j, k);
+  }
+  const int64_t base = ((int64_t)qi * P + (int64_t)sp * blockDim.x + threadIdx.x) * KT;
+#pragma unroll
+  for (int t = 0; t < KT; ++t) {
+    part_s[base + t] = top.s[t];
+    part_i[base + t] = top.i[t];
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// Warp-cooperative k-way merge: lanes build register top-k lists from a strided subset
+// of the input lists (sorted lists: stop at the first entry that cannot enter), then k
+// rounds of a butterfly arg-max by (score desc, index asc) emit the merged list.
+// ---------------------------------------------------------------------------------
+template <int KT, typename I>
+__device__ __forceinline__ void warp_emit(TopK<KT, I>& t, int k, int lane, float* out_s, int64_t* out_i,
+                                         uint8_t* out_hit, float threshold, int32_t rank, int32_t world,
+                                         int64_t B, bool to_global) {
+  float s0 = -CUDART_INF_F;
+  int64_t i0 = -1;
+  for (int r = 0; r < k; ++r) {
+    float bs = t.s[0];
+    I bi = t.i[0];
+    int bl = lane;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float os = __shfl_xor_sync(0xffffffffu, bs, o);
+      const I oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+      if (better(os, oi, bs, bi) || (!better(bs, bi, os, oi) && ol < bl)) {
+        bs = os;
+        bi = oi;
+        bl = ol;
+      }
+    }
+    int64_t gi = -1;
+    if (bi >= 0) gi = to_global ? shard_global((int64_t)bi, rank, world, B) : (int64_t)bi;
+    if (lane == 0) {
+      out_s[r] = bi >= 0 ? bs : -CUDART_INF_F;
+      out_i[r] = gi;
+    }
+    if (r == 0) {
+      s0 = bs;
+      i0 = gi;
+    }
+    if (lane == bl) t.pop_front();
+  }
+  if (out_hit != nullptr && lane == 0) *out_hit = (i0 >= 0 && s0 >= threshold) ? 1 : 0;
+}
+
+template <int KT>
+__global__ void merge_partials_kernel(const float* __restrict__ part_s, const int32_t* __restrict__ part_i,
+                                      int32_t nq, int32_t P, int32_t k, float* __restrict__ out_s,
+                                      int64_t* __restrict__ out_i, uint8_t* __restrict__ out_hit,
+                                      float threshold, int32_t rank, int32_t world, int64_t B) {
+  const int lane = threadIdx.x & 31;
+  const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (q >= nq) return;
+  TopK<KT, int32_t> t;
+  t.init(true);
+  for (int p = lane; p < P; p += 32) {
+    const int64_t base = ((int64_t)q * P + p) * KT;
+    for (int r = 0; r < k; ++r) {
+      const int32_t j = part_i[base + r];
+      const float v = part_s[base + r];
+      if (j < 0 || !better(v, j, t.kth_s, t.kth_i)) break;
+      t.insert(v, j, k);
+    }
+  }
+  warp_emit(t, k, lane, out_s + (int64_t)q * k, out_i + (int64_t)q * k,
+            out_hit ? out_hit + q : nullptr, threshold, rank, world, B, true);
+}
+
+template <int KT>
+__global__ void merge_shards_kernel(const float* __restrict__ in_s, const int64_t* __restrict__ in_i,
+                                    int32_t G, int32_t nq, int32_t kin, int32_t k, float* __restrict__ out_s,
+                                    int64_t* __restrict__ out_i, uint8_t* __restrict__ out_hit,
+                                    float threshold) {
+  const int lane = threadIdx.x & 31;
+  const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (q >= nq) return;
+  TopK<KT, int64_t> t;
+  t.init(true);
+  for (int g = lane; g < G; g += 32) {
+    const int64_t base = ((int64_t)g * nq + q) * kin;
+    for (int r = 0; r < kin; ++r) {
+      const int64_t j = in_i[base + r];
+      const float v = in_s[base + r];
+      if (j < 0 || !better(v, j, t.kth_s, t.kth_i)) break;
+      t.insert(v, j, k);
+    }
+  }
+  warp_emit(t, k, lane, out_s + (int64_t)q * k, out_i + (int64_t)q * k, out_hit + q, threshold, 0, 1, 1,
+            false);
+}
+
+inline unsigned blocks_for(int64_t n, int per_block) { return (unsigned)((n + per_block - 1) / per_block); }
+
+}  // namespace
+
+int pick_KT(int k) { return k <= 8 ? 8 : k <= 16 ? 16 : k <= 32 ? 32 : 64; }
+
+cudaError_t launch_append(Pool& p, const void* emb_src, const float* joints_src, int64_t n_src,
+                          int64_t first_global, cudaStream_t s) {
+  if (n_src <= 0) return cudaSuccess;
+  const int wpb = 8;
+  const auto& c = p.cfg;
+  if (c.dtype == AMS_DTYPE_BF16)
+    append_kernel<true><<<blocks_for(n_src, wpb), wpb * 32, 0, s>>>(
+        emb_src, joints_src, n_src, first_global, c.dim, c.joint_dim, p.JP, c.rank, c.world, p.B, p.emb,
+        p.inv_norm, p.joints);
+  else
+    append_kernel<false><<<blocks_for(n_src, wpb), wpb * 32, 0, s>>>(
+        emb_src, joints_src, n_src, first_global, c.dim, c.joint_dim, p.JP, c.rank, c.world, p.B, p.emb,
+        p.inv_norm, p.joints);
+  ++p.launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_query_prep(Pool& p, const void* q_src, const float* qj_src, int32_t nq, cudaStream_t s) {
+  const int wpb = 8;
+  const auto& c = p.cfg;
+  if (c.dtype == AMS_DTYPE_BF16)
+    query_prep_kernel<true><<<blocks_for(nq, wpb), wpb * 32, 0, s>>>(q_src, qj_src, nq, c.dim, c.joint_dim,
+                                                                     p.JP, p.q_stage, p.q_inv, p.q_joints);
+  else
+    query_prep_kernel<false><<<blocks_for(nq, wpb), wpb * 32, 0, s>>>(q_src, qj_src, nq, c.dim, c.joint_dim,
+                                                                      p.JP, p.q_stage, p.q_inv, p.q_joints);
+  ++p.launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_match_simt(Pool& p, const MatchArgs& a, int32_t S, cudaStream_t s) {
+  const int32_t P = S * kSimtThreads;
+  const size_t smem = (size_t)p.cfg.dim * sizeof(float);
+  const dim3 grid((unsigned)(a.nq * S));
+#define AMS_SIMT(KT_)                                                                                  \
+  match_simt_f32_kernel<KT_><<<grid, kSimtThreads, smem, s>>>(                                        \
+      static_cast<const float*>(p.emb), p.inv_norm, p.joints, p.local, static_cast<const float*>(p.q_stage), \
+      p.q_inv, p.q_joints, p.cfg.dim, p.JP, S, a.k, a.g2, a.gated, p.part_s, p.part_i, P)
+  switch (a.KT) {
+    case 8: AMS_SIMT(8); break;
+    case 16: AMS_SIMT(16); break;
+    case 32: AMS_SIMT(32); break;
+    default: AMS_SIMT(64); break;
+  }
+#undef AMS_SIMT
+  ++p.launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_merge_partials(Pool& p, const MatchArgs& a, int32_t P, float* out_s, int64_t* out_i,
+                                  uint8_t* out_hit, cudaStream_t s) {
+  const int wpb = 4;
+  const auto& c = p.cfg;
+  const unsigned g = blocks_for(a.nq, wpb);
+#define AMS_MERGE(KT_)                                                                                 \
+  merge_partials_kernel<KT_><<<g, wpb * 32, 0, s>>>(p.part_s, p.part_i, a.nq, P, a.k, out_s, out_i, out_hit, \
+                                                     a.threshold, c.rank, c.world, p.B)
+  switch (a.KT) {
+    case 8: AMS_MERGE(8); break;
+    case 16: AMS_MERGE(16); break;
+    case 32: AMS_MERGE(32); break;
+    default: AMS_MERGE(64); break;
+  }
+#undef AMS_MERGE
+  ++p.launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_merge_shards(Pool& p, const MatchArgs& a, int32_t G, int32_t kin, const float* in_s,
+                                const int64_t* in_i, float* out_s, int64_t* out_i, uint8_t* out_hit,
+                                cudaStream_t s) {
+  const int wpb = 4;
+  const unsigned g = blocks_for(a.nq, wpb);
+#define AMS_MS(KT_)                                                                                   \
+  merge_shards_kernel<KT_><<<g, wpb * 32, 0, s>>>(in_s, in_i, G, a.nq, kin, a.k, out_s, out_i, out_hit, \
+                                                   a.threshold)
+  switch (a.KT) {
+    case 8: AMS_MS(8); break;
+    case 16: AMS_MS(16); break;
+    case 32: AMS_MS(32); break;
+    default: AMS_MS(64); break;
+  }
+#undef AMS_MS
+  ++p.launches;
+  return cudaGetLastError();
+}
+
+}  // namespace ams

@@ -1,0 +1,59 @@
+"""Agreement criteria of the GPU path against the oracle (north_star).
+
+Per query:
+  1. the number of valid slots is equal (the gate is bit-exact);
+  2. |s_gpu[r] - s_orc[r]| <= 2e-3 for every valid rank r (bf16 inputs, fp32 accumulate);
+  3. index sets are equal at every rank r whose oracle gap s[r] - s[r+1] exceeds 4e-3
+     (reading R20; r = k is north_star's literal rule, using the (k+1)-th score);
+  4. hit flags are equal wherever |s_orc_top1 - theta| > 2e-3 (reading R19);
+  5. fp32 config: every output byte-identical.
+"""
+import numpy as np
+
+SCORE_TOL = 2e-3
+GAP = 4e-3
+
+
+def check_bf16(gpu_idx, gpu_score, gpu_hit, orc, theta, score_tol=SCORE_TOL, gap=GAP, labels=None):
+    gpu_idx = np.asarray(gpu_idx)
+    gpu_score = np.asarray(gpu_score)
+    gpu_hit = np.asarray(gpu_hit)
+    nq, k = orc.idx.shape
+    assert gpu_idx.shape == (nq, k)
+    stats = {"rank_checks": 0, "queries": nq}
+    valid_o = orc.idx >= 0
+    valid_g = gpu_idx >= 0
+    bad = np.nonzero(valid_o.sum(1) != valid_g.sum(1))[0]
+    assert bad.size == 0, f"valid-slot count differs for queries {bad[:10]}"
+    assert np.all(np.isneginf(gpu_score[~valid_g])), "padding scores must be -inf"
+    diff = np.abs(gpu_score[valid_o].astype(np.float64) - orc.key[valid_o])
+    assert diff.size == 0 or diff.max() <= score_tol, f"max score diff {diff.max()}"
+    # per-rank index-set equality where the oracle gap is large
+    keys = np.concatenate([orc.key, orc.next[:, None]], axis=1)
+    for i in range(nq):
+        n = int(valid_o[i].sum())
+        for r in range(1, n + 1):
+            if keys[i, r - 1] - keys[i, r] > gap:
+                stats["rank_checks"] += 1
+                a = set(orc.idx[i, :r].tolist())
+                b = set(gpu_idx[i, :r].tolist())
+                assert a == b, f"query {i}: top-{r} index sets differ {sorted(a)} vs {sorted(b)}"
+    sure = np.abs(np.where(valid_o[:, 0], orc.key[:, 0], -np.inf) - theta) > score_tol
+    mism = np.nonzero(sure & (gpu_hit.astype(bool) != orc.hit.astype(bool)))[0]
+    assert mism.size == 0, f"hit flags differ for queries {mism[:10]}"
+    # the GPU's own list must be sorted by (score desc, index asc)
+    for i in range(nq):
+        n = int(valid_g[i].sum())
+        s, j = gpu_score[i, :n], gpu_idx[i, :n]
+        ok = (s[:-1] > s[1:]) | ((s[:-1] == s[1:]) & (j[:-1] < j[1:]))
+        assert ok.all(), f"query {i}: GPU list not ordered"
+        assert len(set(j.tolist())) == n, f"query {i}: duplicate indices"
+    if labels is not None:
+        stats["label_top1"] = float(np.mean(gpu_idx[labels >= 0, 0] == labels[labels >= 0]))
+    return stats
+
+
+def check_exact(gpu_idx, gpu_score, gpu_hit, orc):
+    assert np.array_equal(np.asarray(gpu_idx), orc.idx)
+    assert np.asarray(gpu_score).tobytes() == orc.score.tobytes()
+    assert np.array_equal(np.asarray(gpu_hit), orc.hit)

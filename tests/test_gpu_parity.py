@@ -1,0 +1,159 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Every test is @pytest.mark.gpu.  Inputs come from ams_gen (seeded); expected values
+come only from oracle/ (never from the CUDA path).
+"""
+import itertools
+import json
+import os
+
+import numpy as np
+import pytest
+
+import ams_gen
+import oracle
+from tests.parity import check_bf16, check_exact
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+INF = float("inf")
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def ams():
+    import paper_2508_10259_b200 as m
+    return m
+
+
+def dev():
+    return torch.device("cuda", 0)
+
+
+def to_dev(a):
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    return t.to(dev())
+
+
+def run_gpu(ams, w_emb, w_joints, q, qj, k, theta, gamma, dtype, max_k=None, host_inputs=False, pool=None):
+    """Create a pool, append, match; returns numpy (idx, score, hit)."""
+    M, d = w_emb.shape
+    J = w_joints.shape[1]
+    nq = q.shape[0]
+    own = pool is None
+    if own:
+        pool = ams.Pool(d, J, max(M, 1), max(nq, 1), max_k or k, dtype=dtype)
+        if M:
+            if host_inputs:
+                pool.append(np.ascontiguousarray(w_emb), np.ascontiguousarray(w_joints, np.float32), M)
+            else:
+                pool.append(to_dev(w_emb), to_dev(w_joints.astype(np.float32)), M)
+    if host_inputs:
+        out = pool.match(np.ascontiguousarray(q), np.ascontiguousarray(qj, np.float32), k, theta, gamma)
+    else:
+        out = pool.match(to_dev(q), to_dev(qj.astype(np.float32)), k, theta, gamma)
+    torch.cuda.synchronize()
+    res = tuple(t.cpu().numpy() for t in out)
+    if own:
+        pool.close()
+    return res
+
+
+def pad_d(x, d=64):
+    out = np.zeros((x.shape[0], d), x.dtype)
+    out[:, : x.shape[1]] = x
+    return out
+
+
+# ---------------------------------------------------------------------------- C1 exact
+@pytest.mark.parametrize("gamma", [0.3, INF])
+@pytest.mark.parametrize("host_inputs", [False, True])
+def test_c1_fp32_bit_exact(ams, gamma, host_inputs):
+    cfg = ams_gen.CONFIGS["c1"]
+    w = ams_gen.generate_host(cfg)
+    orc = oracle.match(w.emb, w.joints, w.q_emb, w.q_joints, cfg.k, cfg.theta, gamma)
+    g = run_gpu(ams, w.emb, w.joints, w.q_emb, w.q_joints, cfg.k, cfg.theta, gamma, "fp32",
+                host_inputs=host_inputs)
+    check_exact(*g, orc)
+
+
+# ---------------------------------------------------------------------------- golden / P1
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_golden_fixtures_gpu(ams, dtype):
+    for name in ("spec_select_context_order.json", "spec_lookup_threshold.json"):
+        fx = json.load(open(os.path.join(GOLDEN, name)))
+        e = pad_d(np.array(fx["pool_emb"], np.float32))
+        q = pad_d(np.array(fx["queries_emb"], np.float32))
+        if dtype == "bf16":
+            e, q = ams_gen.f32_to_bf16_bits(e), ams_gen.f32_to_bf16_bits(q)
+        pj = np.array(fx["pool_joints"], np.float32)
+        qj = np.array(fx["queries_joints"], np.float32)
+        idx, s, hit = run_gpu(ams, e, pj, q, qj, fx["k"], fx["theta"], fx["gamma"], dtype)
+        assert idx.tolist() == fx["expect"]["idx"], name
+        assert hit.tolist() == fx["expect"]["hit"], name
+    fx = json.load(open(os.path.join(GOLDEN, "gate_boundary.json")))
+    e = pad_d(np.array(fx["pool_emb"], np.float32))
+    q = pad_d(np.array(fx["queries_emb"], np.float32))
+    if dtype == "bf16":
+        e, q = ams_gen.f32_to_bf16_bits(e), ams_gen.f32_to_bf16_bits(q)
+    for case in fx["cases"]:
+        g = float(case["gamma"])
+        idx, s, hit = run_gpu(ams, e, np.array(fx["pool_joints"], np.float32), q,
+                              np.array(fx["queries_joints"], np.float32), fx["k"], fx["theta"], g, dtype)
+        assert idx.tolist() == case["expect"]["idx"], g
+        assert hit.tolist() == case["expect"]["hit"], g
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_p1_exhaustive_gpu(ams, dtype):
+    rows = np.array(list(itertools.product([-1.0, 1.0], repeat=4)), np.float32)
+    rng = np.random.Generator(np.random.PCG64(11))
+    joints = rng.integers(-2, 3, (16, 2)).astype(np.float32)
+    qj = np.array([[0, 0], [1, -1], [2, 2], [-2, 1]] * 4, np.float32)
+    e = pad_d(rows)
+    if dtype == "bf16":
+        e = ams_gen.f32_to_bf16_bits(e)
+    pool = ams.Pool(64, 2, 16, 16, 32, dtype=dtype)
+    pool.append(to_dev(e), to_dev(joints), 16)
+    for gamma in (0.0, 1.0, 2.0, INF):
+        for k in (1, 3, 5, 16, 17):
+            for theta in (1.0, 0.5, 0.0, -1.0):
+                orc = oracle.match(e, joints, e, qj, k, theta, gamma)
+                g = run_gpu(ams, e, joints, e, qj, k, theta, gamma, dtype, pool=pool)
+                check_exact(*g, orc)   # every score is exact in both paths
+    pool.close()
+
+
+# ---------------------------------------------------------------------------- bf16 parity
+SMALL = [
+    # (config, M, Q) -- tile-spanning sizes with ragged tails, oracle finishes in seconds
+    ("c2", 20011, 300),
+    ("c3", 9001, 130),
+    ("c4", 12345, 129),
+    ("c5", 3001, 70),
+]
+
+
+@pytest.mark.parametrize("name,M,Q", SMALL)
+@pytest.mark.parametrize("gated", [True, False])
+def test_bf16_parity_small(ams, name, M, Q, gated):
+    cfg = ams_gen.small_variant(name, M, Q)
+    w = ams_gen.generate_host(cfg)
+    gamma = cfg.gamma if gated else INF
+    orc = oracle.match(w.emb, w.joints, w.q_emb, w.q_joints, cfg.k, cfg.theta, gamma)
+    g = run_gpu(ams, w.emb, w.joints, w.q_emb, w.q_joints, cfg.k, cfg.theta, gamma, "bf16")
+    stats = check_bf16(*g, orc, cfg.theta, labels=w.labels)
+    if gated:
+        nd = w.labels >= 0
+        assert np.array_equal(g[2].astype(bool), nd)   # P10 by construction
+    assert stats["label_top1"] == 1.0
+
+
+def test_bf16_host_vs_device_inputs_identical(ams):
+    cfg = ams_gen.small_variant("c2", 5000, 64)
+    w = ams_gen.generate_host(cfg)
+    a = run_gpu(ams, w.emb, w.joints, w.q_emb, w.q_joints, cfg.k, cfg.theta, INF, "bf16")
+    b = run_gpu(ams, w.emb, w.joints, w.q_emb, w.q_joints, cfg.k, cfg.theta, INF, "bf16", host_inputs=True)
+    for x, y in zip(a, b):
+        assert x.tobytes() == y.tobytes()
