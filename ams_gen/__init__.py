@@ -283,3 +283,72 @@ def batch_sizes(total: int, seed: int):
         out.append(b)
         left -= b
     return out
+
+
+def build_device_workload(cfg: Config, device, append_fn, Q: Optional[int] = None, salt: int = 0,
+                          chunk_needed=None, host_copy: bool = False):
+    """Stream the pool of a device-generated config through ``append_fn(emb, joints)``
+    chunk by chunk (never holding the whole pool), then draw the queries.
+
+    ``chunk_needed(lo, hi) -> bool`` may skip generating chunks whose rows the caller
+    ignores (a rank that owns none of them); append_fn then receives ``None`` for that
+    chunk's arrays and must still account for ``hi - lo`` rows.  Near-duplicate source
+    rows are always regenerated.  Returns (q bf16 [Q,d], qj f32 [Q,J], labels i64 [Q]) on
+    `device`, plus the host copy of the pool (emb uint16 bits, joints) if host_copy.
+    """
+    torch = _torch()
+    Q = cfg.Q if Q is None else Q
+    g = torch.Generator(device="cpu").manual_seed(cfg.seed * 1_000_003 + 999 + salt * 7919)
+    n_nd = min(int(round(Q * cfg.near_dup_frac)), cfg.M)
+    src = torch.randperm(cfg.M, generator=g)[:n_nd] if cfg.M <= (1 << 24) else \
+        torch.unique(torch.randint(0, cfg.M, (2 * n_nd + 64,), generator=g))[:n_nd]
+    src = src.to(torch.int64)
+    order = torch.argsort(src)
+    src_sorted = src[order]
+    means = device_means(cfg, device)
+    src_emb = torch.empty(n_nd, cfg.d, dtype=torch.bfloat16, device=device)
+    src_j = torch.empty(n_nd, cfg.J, dtype=torch.float32, device=device)
+    host_e = host_j = None
+    if host_copy:
+        host_e = np.empty((cfg.M, cfg.d), np.uint16)
+        host_j = np.empty((cfg.M, cfg.J), np.float32)
+    nchunks = (cfg.M + CHUNK_ROWS - 1) // CHUNK_ROWS
+    for c in range(nchunks):
+        lo = c * CHUNK_ROWS
+        hi = min(cfg.M, lo + CHUNK_ROWS)
+        a = int(torch.searchsorted(src_sorted, lo))
+        b = int(torch.searchsorted(src_sorted, hi))
+        need = chunk_needed is None or chunk_needed(lo, hi)
+        if need or b > a or host_copy:
+            e, j = device_pool_chunk(cfg, c, means, device)
+            if b > a:
+                rows = (src_sorted[a:b] - lo).to(device)
+                src_emb[a:b] = e[rows]
+                src_j[a:b] = j[rows]
+            if host_copy:
+                host_e[lo:hi] = e.view(torch.int16).cpu().numpy().view(np.uint16)
+                host_j[lo:hi] = j.cpu().numpy()
+            append_fn(e if need else None, j if need else None, hi - lo)
+        else:
+            append_fn(None, None, hi - lo)
+    # undo the sort: sources in draw order
+    inv = torch.empty_like(order)
+    inv[order] = torch.arange(n_nd)
+    src_emb = src_emb[inv.to(device)]
+    src_j = src_j[inv.to(device)]
+    gq = torch.Generator(device=device).manual_seed(cfg.seed * 1_000_003 + 4242 + salt * 7919)
+    sigma = 0.05 / math.sqrt(cfg.d)
+    q_nd = src_emb.float() + sigma * torch.randn(n_nd, cfg.d, generator=gq, device=device)
+    qj_nd = src_j + 0.02 * torch.randn(n_nd, cfg.J, generator=gq, device=device)
+    n_fr = Q - n_nd
+    comp = torch.randint(0, cfg.components, (n_fr,), generator=gq, device=device)
+    q_fr = means[comp] + 0.1 * torch.randn(n_fr, cfg.d, generator=gq, device=device)
+    qj_fr = torch.rand(n_fr, cfg.J, generator=gq, device=device) * (2 * PI) - PI
+    q = torch.cat([_unit_t(q_nd), _unit_t(q_fr)]).to(torch.bfloat16)
+    qj = torch.cat([qj_nd, qj_fr]).float()
+    labels = torch.cat([src.to(device), torch.full((n_fr,), -1, dtype=torch.int64, device=device)])
+    perm = torch.randperm(Q, generator=gq, device=device)
+    out = (q[perm].contiguous(), qj[perm].contiguous(), labels[perm].contiguous())
+    if host_copy:
+        return out + (host_e, host_j)
+    return out

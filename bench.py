@@ -1,0 +1,416 @@
+#!/usr/bin/env python
+"""Benchmark of AMS action-context matching on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3|c4|c2|c3scan]
+                    [--impl ours|reference] [--ungated]
+    torchrun --nproc-per-node N ... bench.py --gpus N ...
+
+A step is one ams_match call (query prep -> tcgen05 similarity GEMM with the fused
+gate + top-k epilogue -> k-way merge [-> NCCL all-gather -> shard merge]) over the
+workload's full query batch against the whole (sharded) pool, inputs resident in HBM.
+The default workload is BASELINE.json configs[2] (C3: M=1,048,576, d=1024 bf16, J=14,
+Q=16384, k=16, theta 0.9, gamma 0.3), the north_star compute target; the pool is
+sharded by rows over N ranks (strong scaling).  Rank 0 prints ONE JSON line.
+
+Extra keys: roofline (dominant kernel, CUDA events on the launching stream), scan
+(the north_star 64-query HBM-bound scan of the same pool), e2e (host buffers through
+the C ABI, H2D + D2H inside the timed region), cpu_baseline (the oracle on the host
+cores, a bounded query sample), clocks (nvidia-smi during the timed region),
+gpu_launches (our kernels inside the timed region).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "context-match queries/sec and pool-scan HBM GB/s at 1/2/4/8 B200; % roofline"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return {"hbm_gbs": p["hbm_gbs"], "bf16_tflops": p["bf16_tflops"],
+                "bf16_tflops_sustained": p.get("bf16_tflops_sustained"), "source": "measured"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+
+
+def load_traffic(workload: str, which: str):
+    """dram read+write bytes per launch of the dominant kernel from the committed ncu
+    summary (profiles/ncu_summary.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            s = json.load(f)
+        return s[workload][which]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons, sampled every 100 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.rows = []
+        self.proc = None
+        self.th = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(self.dev)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.th = threading.Thread(target=self._read, daemon=True)
+        self.th.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        if self.th:
+            self.th.join(timeout=2)
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        reasons = set()
+        for r in self.rows:
+            for n, v in zip(self.NAMES, r[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="c3", choices=["c2", "c3", "c3scan", "c4"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ungated", action="store_true", help="gate_radius = +inf")
+    ap.add_argument("--no-scan", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=0, help="queries in the oracle sample (0 = auto)")
+    return ap.parse_args()
+
+
+def dist_setup(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if args.impl == "ours":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+    return rank, world, local
+
+
+def workload_cfg(args):
+    import ams_gen
+    return ams_gen.CONFIGS[args.workload]
+
+
+def config_block(cfg, args, world, gamma):
+    return {"workload": f"{cfg.name} (BASELINE.json configs[{ {'c1': 0, 'c2': 1, 'c3': 2, 'c3scan': 2, 'c4': 3}[cfg.name] }])",
+            "M": cfg.M, "d": cfg.d, "J": cfg.J, "Q": cfg.Q, "k": cfg.k, "theta": cfg.theta,
+            "gate_radius": gamma, "pool_dtype": cfg.dtype, "shard": f"rows contiguous over {world} rank(s)",
+            "l2": "inputs larger than L2 (pool %.2f GB > 126 MB L2)" % (cfg.M * cfg.d * 2 / 1e9),
+            "data": "synthetic (ams_gen recipe, DESIGN.md)"}
+
+
+def oracle_sample(host_e, host_j, q, qj, cfg, gamma, n_s, offset=0):
+    """Time the oracle (mode A, all host cores) on n_s queries; returns (seconds, cores)."""
+    import numpy as np
+    import oracle
+    sel = (np.arange(n_s) + offset) % q.shape[0]
+    t0 = time.perf_counter()
+    oracle.match(host_e, host_j, q[sel], qj[sel], cfg.k, cfg.theta, gamma, mode="A")
+    return time.perf_counter() - t0, oracle.max_threads()
+
+
+def auto_sample(cfg, cores):
+    # ~1e9 fp64 pair-MACs per core-second: aim for 10-30 s of CPU work in total
+    per_query = cfg.M * cfg.d / 1e9
+    n = int(max(1, min(max(cores, 4), round(20.0 / max(per_query, 1e-6)))))
+    return n
+
+
+def run_reference(args):
+    """The oracle as the reference arm (--impl reference), rank 0 only."""
+    import numpy as np
+    import torch
+    import ams_gen
+    import oracle
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    cfg = workload_cfg(args)
+    gamma = float("inf") if args.ungated else cfg.gamma
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0"))) if torch.cuda.is_available() else torch.device("cpu")
+    noop = lambda e, j, n: None  # noqa: E731
+    q, qj, labels, host_e, host_j = ams_gen.build_device_workload(cfg, dev, noop, host_copy=True)
+    q = q.view(torch.int16).cpu().numpy().view(np.uint16)
+    qj = qj.cpu().numpy()
+    cores = oracle.max_threads()
+    n_s = args.cpu_sample or max(1, cores)
+    per_query_s = cfg.M * cfg.d / 1e9 / max(cores, 1)
+    while n_s > 1 and n_s * per_query_s * (args.steps + args.warmup) > 240:
+        n_s //= 2
+    for w in range(args.warmup):
+        oracle_sample(host_e, host_j, q, qj, cfg, gamma, n_s, offset=w * n_s)
+    t = 0.0
+    for s in range(args.steps):
+        dt, cores = oracle_sample(host_e, host_j, q, qj, cfg, gamma, n_s, offset=(args.warmup + s) * n_s)
+        t += dt
+    value = args.steps * n_s / t
+    line = {"metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": config_block(cfg, args, 1, gamma),
+            "cpu_baseline": {"value": value, "unit": "queries/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{n_s} queries per step of {cfg.name} against the full pool "
+                                       f"({cfg.M} rows), oracle mode A (fp64 brute force), OpenMP over queries"},
+            "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import numpy as np
+    import torch
+    import ams_gen
+    import paper_2508_10259_b200 as ams
+    from paper_2508_10259_b200 import dist as adist
+
+    rank, world, local = dist_setup(args)
+    cfg = workload_cfg(args)
+    gamma = float("inf") if args.ungated else cfg.gamma
+    dev = torch.device("cuda", local)
+    peaks = load_peaks()
+    tdist = None
+    if world > 1:
+        import torch.distributed as tdist
+
+    def barrier():
+        if tdist is not None:
+            tdist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if tdist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ------------------------------------------------------------------ pool + queries
+    pool = adist.create_pool(cfg.d, cfg.J, cfg.M, cfg.Q, cfg.k, dtype="bf16", shard_block=0)
+    dummy = torch.zeros(1, cfg.d, dtype=torch.bfloat16, device=dev)
+    dummy_j = torch.zeros(1, cfg.J, dtype=torch.float32, device=dev)
+
+    def append_fn(e, j, n):
+        if e is None:
+            pool.append(dummy, dummy_j, n)   # this rank owns none of these rows
+        else:
+            pool.append(e, j, n)
+
+    need = lambda lo, hi: adist.owned_range_overlaps(cfg.M, world, 0, rank, lo, hi)  # noqa: E731
+    want_cpu = (not args.no_cpu_baseline) and world == 1 and rank == 0
+    built = ams_gen.build_device_workload(cfg, dev, append_fn, chunk_needed=need, host_copy=want_cpu)
+    q, qj, labels = built[:3]
+    torch.cuda.synchronize()
+    assert pool.size == cfg.M
+
+    out_i = torch.empty(cfg.Q, cfg.k, dtype=torch.int64, device=dev)
+    out_s = torch.empty(cfg.Q, cfg.k, dtype=torch.float32, device=dev)
+    out_h = torch.empty(cfg.Q, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step(qe=q, qjj=qj, nq=cfg.Q):
+        ams.ams_match(pool.handle, qe, qjj, nq, cfg.k, cfg.theta, gamma, out_i, out_s, out_h, stream)
+
+    # ------------------------------------------------------------------ main timing
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    ams.ams_pool_read_profile(pool.handle)            # drop warm-up events
+    clk = ClockSampler(torch.cuda.current_device())
+    clk.start()
+    time.sleep(0.15)
+    ams.ams_pool_set_profiling(pool.handle, True)
+    l0 = ams.ams_pool_launch_count(pool.handle)
+    barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    launches = ams.ams_pool_launch_count(pool.handle) - l0
+    ams.ams_pool_set_profiling(pool.handle, False)
+    clocks = clk.stop()
+    t_ms = max_over_ranks(ev0.elapsed_time(ev1))
+    kern_ms, kern_n = ams.ams_pool_read_profile(pool.handle)
+    kern_avg = max_over_ranks(kern_ms / max(kern_n, 1))
+    plan = ams.ams_pool_last_plan(pool.handle)
+    hit_rate = float(out_h.float().mean().item())
+    lab = labels.cpu().numpy()
+    top1 = out_i[:, 0].cpu().numpy()
+    nd = lab >= 0
+    label_top1 = float(np.mean(top1[nd] == lab[nd])) if nd.any() else None
+
+    value = cfg.Q * args.steps / (t_ms / 1e3)
+    m_shard = -(-cfg.M // world)
+    flops_launch = 2.0 * cfg.Q * m_shard * cfg.d
+    bytes_step = cfg.M * (2 * cfg.d + 4 * cfg.J + 4)
+    achieved_tf = flops_launch / (kern_avg / 1e3) / 1e12
+    roofline = {"bound": "tensor", "achieved": achieved_tf, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                "frac": achieved_tf / peaks["bf16_tflops"],
+                "traffic": load_traffic(args.workload, "match_tc"),
+                "kernel": "match_tc_kernel (tcgen05 GEMM + fused gate/top-k epilogue)",
+                "algorithmic_per_launch": {"flop": flops_launch, "bytes": bytes_step / world},
+                "kernel_ms_avg": kern_avg, "kernel_share_of_step": kern_avg / (t_ms / args.steps),
+                "peak_source": f"MEASURED_PEAKS.json bf16_tflops (burst; {peaks['source']})",
+                "frac_vs_sustained": achieved_tf / peaks["bf16_tflops_sustained"]
+                if peaks.get("bf16_tflops_sustained") else None,
+                "frac_vs_datasheet_2250": achieved_tf / 2250.0}
+
+    # ------------------------------------------------------------------ 64-query scan
+    scan = None
+    if not args.no_scan and cfg.Q >= 64:
+        nq = 64
+        qs, qjs = q[:nq].contiguous(), qj[:nq].contiguous()
+        for _ in range(5):
+            step(qs, qjs, nq)
+        torch.cuda.synchronize()
+        ams.ams_pool_read_profile(pool.handle)
+        ams.ams_pool_set_profiling(pool.handle, True)
+        reps = max(20, 5 * args.steps)
+        barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(reps):
+            step(qs, qjs, nq)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ams.ams_pool_set_profiling(pool.handle, False)
+        s_ms = max_over_ranks(ev0.elapsed_time(ev1)) / reps
+        k_ms, k_n = ams.ams_pool_read_profile(pool.handle)
+        k_avg = max_over_ranks(k_ms / max(k_n, 1))
+        gbs_kernel = (bytes_step / world) / (k_avg / 1e3) / 1e9
+        scan = {"queries": nq, "value": nq / (s_ms / 1e3), "unit": "queries/s", "ms_per_call": s_ms,
+                "pool_scan_gbps_per_gpu": (bytes_step / world) / (s_ms / 1e3) / 1e9,
+                "roofline": {"bound": "hbm", "achieved": gbs_kernel, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                             "frac": gbs_kernel / peaks["hbm_gbs"],
+                             "traffic": load_traffic(args.workload, "match_tc_scan"),
+                             "kernel_ms_avg": k_avg, "frac_vs_datasheet_8000": gbs_kernel / 8000.0,
+                             "algorithmic_bytes_per_launch": bytes_step / world}}
+
+    # ------------------------------------------------------------------ e2e (host buffers)
+    e2e = None
+    if not args.no_e2e:
+        hq = q.cpu().pin_memory()
+        hqj = qj.cpu().pin_memory()
+        ho_i = torch.empty(cfg.Q, cfg.k, dtype=torch.int64).pin_memory()
+        ho_s = torch.empty(cfg.Q, cfg.k, dtype=torch.float32).pin_memory()
+        ho_h = torch.empty(cfg.Q, dtype=torch.uint8).pin_memory()
+
+        def e2e_step():
+            ams.ams_match(pool.handle, hq, hqj, cfg.Q, cfg.k, cfg.theta, gamma, out_i, out_s, out_h, stream)
+            ho_i.copy_(out_i, non_blocking=True)
+            ho_s.copy_(out_s, non_blocking=True)
+            ho_h.copy_(out_h, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        e_ms = max_over_ranks(ev0.elapsed_time(ev1))
+        h2d = hq.numel() * hq.element_size() + hqj.numel() * hqj.element_size()
+        d2h = ho_i.numel() * 8 + ho_s.numel() * 4 + ho_h.numel()
+        e2e = {"value": cfg.Q * args.steps / (e_ms / 1e3), "unit": "queries/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "path": "ams_match(host pinned q, q_joints) + D2H of idx/score/hit"}
+
+    # ------------------------------------------------------------------ CPU oracle baseline
+    cpu = None
+    if want_cpu:
+        host_e, host_j = built[3], built[4]
+        qn = q.view(torch.int16).cpu().numpy().view(np.uint16)
+        qjn = qj.cpu().numpy()
+        import oracle
+        cores = oracle.max_threads()
+        n_s = args.cpu_sample or auto_sample(cfg, cores)
+        dt, cores = oracle_sample(host_e, host_j, qn, qjn, cfg, gamma, n_s)
+        cpu = {"value": n_s / dt, "unit": "queries/s", "cores": cores, "kind": "oracle",
+               "sample": f"first {n_s} of the {cfg.Q} {cfg.name} queries against the full {cfg.M}-row pool, "
+                         f"oracle mode A (fp64 brute force, OpenMP over queries), {dt:.1f} s wall"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+                "config": config_block(cfg, args, world, gamma),
+                "pool_scan_gbps_per_gpu": (bytes_step / world) / (t_ms / args.steps / 1e3) / 1e9,
+                "roofline": roofline, "scan": scan, "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks,
+                "gpu_launches": launches, "plan": plan, "hit_rate": hit_rate,
+                "near_dup_top1_equals_source": label_top1}
+        print(json.dumps(line), flush=True)
+    pool.close()
+    if tdist is not None:
+        tdist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

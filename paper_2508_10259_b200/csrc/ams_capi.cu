@@ -79,22 +79,26 @@ int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
 size_t esize(const Pool& p) { return p.cfg.dtype == AMS_DTYPE_BF16 ? 2 : 4; }
 
-// Plan of the tcgen05 kernel: number of row splits S (units = n_qt * S, static
-// round-robin over `grid` persistent CTAs).  Minimises the busiest CTA's tile count
-// ceil(U / grid) * ceil(n_pt / S); ties -> fewer splits (fewer partial lists).
-void plan_tc(const Pool& p, int nq, int KT, int& S, int& grid) {
-  const int n_qt = (nq + ams::kBlockM - 1) / ams::kBlockM;
+// Plan of the tcgen05 kernel.  Queries > 128 -> CTA pairs (cta_group::2, 256-query
+// tiles, 2x the operand reuse per byte from L2); otherwise one CTA per 128-query tile
+// (the HBM-bound scan).  Row splits S: units = n_qt * S are dealt round-robin to the
+// persistent clusters; minimise the busiest cluster's tile count
+// ceil(U / clusters) * ceil(n_pt / S), ties -> fewer splits (fewer partial lists).
+void plan_tc(const Pool& p, int nq, int KT, int& S, int& grid, int& cg) {
+  cg = nq > ams::kBlockM ? 2 : 1;
+  const int qtile = ams::tc_query_tile(cg);
+  const int n_qt = (nq + qtile - 1) / qtile;
   const int64_t n_pt = (p.local + ams::kBlockN - 1) / ams::kBlockN;
-  const int sms = p.num_sms;
-  const int64_t nq_pad = (int64_t)n_qt * ams::kBlockM;
+  const int clusters = p.num_sms / cg;
+  const int64_t nq_pad = (int64_t)n_qt * qtile;
   int64_t s_cap = std::max<int64_t>(1, p.part_cap / (nq_pad * ams::kEpiHalves * KT));
   s_cap = std::min<int64_t>(s_cap, std::max<int64_t>(1, n_pt));
-  s_cap = std::min<int64_t>(s_cap, std::max<int64_t>(1, (int64_t)64 * sms / n_qt + 1));
+  s_cap = std::min<int64_t>(s_cap, std::max<int64_t>(1, (int64_t)64 * clusters / n_qt + 1));
   int64_t best_cost = LLONG_MAX;
   int best = 1;
   for (int64_t s = 1; s <= s_cap; ++s) {
     const int64_t U = (int64_t)n_qt * s;
-    const int64_t waves = (U + sms - 1) / sms;
+    const int64_t waves = (U + clusters - 1) / clusters;
     const int64_t per = (n_pt + s - 1) / s;
     const int64_t cost = waves * per * 64 + s;  // + small penalty per split (merge work)
     if (cost < best_cost) {
@@ -103,7 +107,7 @@ void plan_tc(const Pool& p, int nq, int KT, int& S, int& grid) {
     }
   }
   S = best;
-  grid = (int)std::min<int64_t>((int64_t)n_qt * S, sms);
+  grid = (int)std::min<int64_t>((int64_t)n_qt * S, clusters) * cg;
 }
 
 void plan_simt(const Pool& p, int nq, int KT, int& S) {
@@ -115,7 +119,7 @@ void plan_simt(const Pool& p, int nq, int KT, int& S) {
 }
 
 void free_all(Pool& p) {
-  void* ptrs[] = {p.emb, p.inv_norm, p.joints, p.q_stage, p.q_inv, p.q_joints, p.q_joints_raw,
+  void* ptrs[] = {p.emb, p.inv_norm, p.joints, p.q_stage, p.q_inv, p.q_joints, p.q_joints_raw, p.bound,
                   p.part_s, p.part_i, p.shard_s, p.shard_i, p.gath_s, p.gath_i, p.stage_emb,
                   p.stage_joints};
   for (void* q : ptrs)
@@ -215,7 +219,7 @@ ams_status_t ams_pool_create(const ams_pool_config_t* cfg, ams_pool_t* out) {
   }
   p.cap_pad = round_up(std::max<int64_t>(p.cap_shard, 1), ams::kRowAlign);
   p.KT_max = ams::pick_KT(c.max_k);
-  p.q_pad = (int32_t)round_up(c.max_queries, ams::kBlockM);
+  p.q_pad = (int32_t)round_up(c.max_queries, 2 * ams::kBlockM);
   const size_t es = esize(p);
   const int32_t d = c.dim;
 
@@ -246,6 +250,7 @@ ams_status_t ams_pool_create(const ams_pool_config_t* cfg, ams_pool_t* out) {
             alloc(&p.q_stage, (size_t)p.q_pad * d * es) && alloc((void**)&p.q_inv, (size_t)p.q_pad * 4) &&
             alloc((void**)&p.q_joints, (size_t)p.q_pad * p.JP * 4) &&
             alloc((void**)&p.q_joints_raw, (size_t)c.max_queries * c.joint_dim * 4) &&
+            alloc((void**)&p.bound, (size_t)p.q_pad * 4) &&
             alloc((void**)&p.part_s, (size_t)part * 4) && alloc((void**)&p.part_i, (size_t)part * 4) &&
             alloc((void**)&p.shard_s, (size_t)c.max_queries * c.max_k * 4) &&
             alloc((void**)&p.shard_i, (size_t)c.max_queries * c.max_k * 8) &&
@@ -261,6 +266,7 @@ ams_status_t ams_pool_create(const ams_pool_config_t* cfg, ams_pool_t* out) {
   }
   if (c.dtype == AMS_DTYPE_BF16) {
     if (!encode_bf16_map(&p.tmap_pool, p.emb, p.cap_pad, d, ams::kBlockN) ||
+        !encode_bf16_map(&p.tmap_pool2, p.emb, p.cap_pad, d, ams::kBlockN / 2) ||
         !encode_bf16_map(&p.tmap_q, p.q_stage, p.q_pad, d, ams::kBlockM)) {
       free_all(p);
       delete pool;
@@ -392,15 +398,15 @@ ams_status_t ams_match(ams_pool_t pool, const void* q_emb, const float* q_joints
       p.last_grid = nq * S;
       p.last_kernel = 0;
     } else {
-      int S, grid;
-      plan_tc(p, nq, a.KT, S, grid);
+      int S, grid, cg;
+      plan_tc(p, nq, a.KT, S, grid, cg);
       P = S * ams::kEpiHalves;
       if (e0) AMS_CUDA_TRY(cudaEventRecord(e0, s));
-      AMS_CUDA_TRY(ams::launch_match_tc(p, a, S, grid, s));
+      AMS_CUDA_TRY(ams::launch_match_tc(p, a, S, grid, cg, s));
       if (e1) AMS_CUDA_TRY(cudaEventRecord(e1, s));
       p.last_splits = S;
       p.last_grid = grid;
-      p.last_kernel = 1;
+      p.last_kernel = cg;
     }
     p.last_partials = P;
   }

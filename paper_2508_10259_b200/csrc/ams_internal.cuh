@@ -42,6 +42,13 @@ __host__ __device__ inline int64_t shard_count(int64_t n, int32_t rank, int32_t 
   return blocks * B + ((full % world) == rank ? rem : 0);
 }
 
+// Pool joints are stored tile-transposed: the JP joints of the 256 rows of tile T form a
+// contiguous [JP][256] fp32 block, so one bulk copy stages a tile's joints and one
+// 16-byte shared load yields joint t of four consecutive rows.
+__host__ __device__ inline int64_t joint_offset(int64_t l, int t, int JP) {
+  return ((l / kRowAlign) * JP + t) * kRowAlign + (l % kRowAlign);
+}
+
 // --------------------------------------------------------------------------- pool
 struct Pool {
   ams_pool_config_t cfg{};
@@ -58,7 +65,7 @@ struct Pool {
   // shard storage
   void* emb = nullptr;        // [cap_pad, d] bf16 or fp32
   float* inv_norm = nullptr;  // [cap_pad]
-  float* joints = nullptr;    // [cap_pad, JP]
+  float* joints = nullptr;    // [cap_pad / 256][JP][256] (joint_offset)
 
   // query workspace
   int32_t q_pad = 0;          // max_queries rounded up to kBlockM
@@ -84,7 +91,10 @@ struct Pool {
   void* stage_emb = nullptr;
   float* stage_joints = nullptr;
 
-  CUtensorMap tmap_pool{};   // bf16 pool [cap_pad, d], box {64, 256}, SW128
+  uint32_t* bound = nullptr;  // [q_pad] per-query admission lower bound (tcgen05 path)
+
+  CUtensorMap tmap_pool{};   // bf16 pool [cap_pad, d], box {64, 256}, SW128 (CTA tile)
+  CUtensorMap tmap_pool2{};  // bf16 pool [cap_pad, d], box {64, 128}, SW128 (CTA-pair half tile)
   CUtensorMap tmap_q{};      // bf16 queries [q_pad, d], box {64, 128}, SW128
 
   void* nccl_comm = nullptr;  // ncclComm_t
@@ -110,7 +120,9 @@ cudaError_t launch_append(Pool& p, const void* emb_src, const float* joints_src,
                           int64_t first_global, cudaStream_t s);
 cudaError_t launch_query_prep(Pool& p, const void* q_src, const float* qj_src, int32_t nq, cudaStream_t s);
 cudaError_t launch_match_simt(Pool& p, const MatchArgs& a, int32_t splits, cudaStream_t s);
-cudaError_t launch_match_tc(Pool& p, const MatchArgs& a, int32_t splits, int32_t grid, cudaStream_t s);
+// cg = 1: one CTA per 128x256 tile; cg = 2: CTA pair (cta_group::2) per 256x256 tile
+cudaError_t launch_match_tc(Pool& p, const MatchArgs& a, int32_t splits, int32_t grid, int32_t cg, cudaStream_t s);
+int tc_query_tile(int cg);
 // merge [nq][P][KT] local lists -> [nq][k] (fp32, global int64); writes hit if out_hit != null
 cudaError_t launch_merge_partials(Pool& p, const MatchArgs& a, int32_t P, float* out_s, int64_t* out_i,
                                   uint8_t* out_hit, cudaStream_t s);
@@ -120,7 +132,5 @@ cudaError_t launch_merge_shards(Pool& p, const MatchArgs& a, int32_t G, int32_t 
                                 cudaStream_t s);
 
 int pick_KT(int k);
-int tc_stages(int JP);
-size_t tc_smem_bytes(int JP);
 
 }  // namespace ams

@@ -63,7 +63,7 @@ __global__ void append_kernel(const void* __restrict__ src, const float* __restr
       inv_norm[l] = ss > 0.0f ? __fdiv_rn(1.0f, __fsqrt_rn(ss)) : 0.0f;
     }
   }
-  if (lane < JP) joints[l * JP + lane] = lane < J ? jsrc[r * J + lane] : 0.0f;
+  if (lane < JP) joints[joint_offset(l, lane, JP)] = lane < J ? jsrc[r * J + lane] : 0.0f;
 }
 
 // ---------------------------------------------------------------------------------
@@ -136,11 +136,10 @@ __global__ void __launch_bounds__(kSimtThreads)
   for (int64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) {
     if (gated) {
       float ds = 0.0f;
-      const float* p = pj + j * JP;
 #pragma unroll
       for (int t = 0; t < 16; ++t)
         if (t < JP) {
-          const float df = __fsub_rn(r[t], p[t]);
+          const float df = __fsub_rn(r[t], pj[joint_offset(j, t, JP)]);
           ds = __fmaf_rn(df, df, ds);
         }
       if (!(ds <= g2)) continue;

@@ -7,20 +7,31 @@
 //   gate(i,j) = canonical fp32 sum_t (r_it - p_jt)^2 <= g2
 //   top-k by (s desc, j asc) per query, kept in registers of the epilogue threads.
 //
-// Tiling: a tile is 128 queries (TMEM lanes, MMA M) x 256 pool rows (TMEM columns,
-// MMA N); K advances 64 bf16 (one 128-B swizzle atom) per pipeline stage, 4 UMMAs of
-// K=16 per stage.  A work unit is (query tile, contiguous split of the pool rows); a
-// persistent CTA walks its units in split-major order so concurrent CTAs share the
-// same pool rows through L2.
+// Tiling: a tile is 128*CG queries (MMA M; TMEM lanes of each CTA) x 256 pool rows
+// (MMA N; TMEM columns); K advances 64 bf16 (one 128-B swizzle atom) per pipeline
+// stage, 4 UMMAs of K=16 per stage.  CG = 2 runs the tile on a CTA pair
+// (tcgen05.mma.cta_group::2, M = 256): each CTA stages its own 128 query rows and half
+// of the 256 pool rows, so a pair tile moves 1 MB of operands per 134 MFLOP (128 flop/B
+// from L2, vs 85 for the single-CTA 128x256 tile).  A work unit is (query tile,
+// contiguous split of the pool rows); persistent clusters walk units in split-major
+// order so concurrent CTAs stream the same pool rows through L2.
 //
-// Warp roles (320 threads, 1 CTA / SM):
+// Warp roles (320 threads per CTA, 1 CTA per SM):
 //   warp 0      TMA producer: query + pool tiles into a STAGES-deep smem ring; pool
 //               joints / inv_norm of each tile into a 2-deep aux ring (bulk copies)
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer; accumulators
-//               double-buffered in TMEM (2 x 256 columns)
-//   warps 2..9  epilogue: warp w reads TMEM lanes 32*(w%4).. (its 32 queries), column
-//               half (w-2)/4 of the tile, with tcgen05.ld; scales, gates, keeps a
-//               per-thread running top-k; one partial list per (query, split, half).
+//   warp 1      TMEM allocator + (leader CTA) single-thread tcgen05.mma issuer;
+//               accumulators double-buffered in TMEM (2 x 256 columns)
+//   warps 2..9  epilogue: warp w reads TMEM lanes 32*(w%4).. (its 32 queries) of column
+//               half (w-2)/4 with tcgen05.ld; one partial list per (query, split, half).
+//
+// Epilogue per 32-column chunk: a branch-free filter computes, with packed f32x2
+// math, either the chunk's best score (ungated) or the smallest partial joint distance
+// over the first 4 joints (gated; partial sums of squares are a lower bound of the
+// canonical sum since RN is monotone), then ONE warp vote decides whether the exact
+// per-column path runs.  Admission uses the local KT-th best AND a per-query lower bound
+// shared through global memory by every split of the same query (the KT-th best of any
+// split is <= the global k-th best, so rows below it can never enter; equal scores are
+// admitted so the index tie rule is preserved).
 #include <cuda_bf16.h>
 #include <math_constants.h>
 
@@ -34,36 +45,46 @@ namespace {
 
 constexpr int kThreadsTc = 64 + 128 * kEpiHalves;   // 320
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kABytes = kBlockM * kBlockK * 2;   // 16 KB
-constexpr uint32_t kBBytes = kBlockN * kBlockK * 2;   // 32 KB
-constexpr uint32_t kStageBytes = kABytes + kBBytes;
-constexpr uint32_t kIdesc = ptx::idesc_bf16_f32(kBlockM, kBlockN);
+constexpr uint32_t kABytes = kBlockM * kBlockK * 2;   // 16 KB: 128 query rows x 128 B
 constexpr int kColsPerHalf = kBlockN / kEpiHalves;    // 128
 constexpr int kChunk = 32;
+constexpr int kRefreshTiles = 8;                      // bound publish/refresh period
+
+template <int CG>
+struct Geo {
+  static constexpr uint32_t b_rows = kBlockN / CG;               // pool rows staged per CTA
+  static constexpr uint32_t b_bytes = b_rows * kBlockK * 2;      // 32 KB (CG 1) / 16 KB (CG 2)
+  static constexpr uint32_t stage_bytes = kABytes + b_bytes;
+  static constexpr uint32_t idesc = ptx::idesc_bf16_f32(kBlockM * CG, kBlockN);
+};
 
 struct TcParams {
   const float* inv_q;
   const float* q_joints;     // [q_pad, JP]
   const float* pool_inv;     // [cap_pad]
-  const float* pool_joints;  // [cap_pad, JP]
+  const float* pool_joints;  // [cap_pad/256][JP][256]
   float* part_s;
   int32_t* part_i;
+  uint32_t* bound;           // [nq] per-query admission lower bound (ordered-u32; 0 = none)
   int64_t L;                 // local rows
   int32_t nq, d, n_qt, n_pt, S, n_units, k, gated, P;
   float g2;
 };
 
 template <int JP>
-struct SmemLayout {
-  static constexpr uint32_t aux_j_bytes = kBlockN * JP * 4;
-  static constexpr uint32_t aux_bytes = aux_j_bytes + kBlockN * 4;
+struct Aux {
+  static constexpr uint32_t j_bytes = kBlockN * JP * 4;
+  static constexpr uint32_t bytes = j_bytes + kBlockN * 4;
 };
 
-__host__ __device__ constexpr int stages_for(int JP) { return JP >= 16 ? 3 : 4; }
+template <int JP, int CG>
+__host__ __device__ constexpr int stages_for() {
+  return CG == 1 ? (JP >= 16 ? 3 : 4) : (JP >= 16 ? 5 : 6);
+}
 
-template <int JP>
+template <int JP, int CG>
 __host__ __device__ constexpr size_t smem_for() {
-  return 1024 /*align slack*/ + (size_t)stages_for(JP) * kStageBytes + 2 * SmemLayout<JP>::aux_bytes + 256;
+  return 1024 /*align slack*/ + (size_t)stages_for<JP, CG>() * Geo<CG>::stage_bytes + 2 * Aux<JP>::bytes + 256;
 }
 
 __device__ __forceinline__ void split_tiles(int sp, int S, int n_pt, int& t_lo, int& t_hi) {
@@ -71,83 +92,108 @@ __device__ __forceinline__ void split_tiles(int sp, int S, int n_pt, int& t_lo, 
   t_hi = (int)((int64_t)(sp + 1) * n_pt / S);
 }
 
+__device__ __forceinline__ float4 lds4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+
+// One 32-column chunk of the epilogue for one thread (= one query).
+//   inv_sm: inverse norms of the chunk's 32 pool rows (smem)
+//   jsm:    joint t of chunk column c at jsm[t * 256 + c] (smem, tile-transposed)
+// Fast filter: one value per 8-column sub-chunk (best score, or smallest partial joint
+// distance); the exact path reloads only sub-chunks that some lane may admit.
 template <int KT, int JP, bool GATED>
-__device__ __forceinline__ void epi_chunk(const uint32_t (&v)[32], uint32_t taddr, int64_t jbase,
-                                          int64_t row_end, const float* __restrict__ inv_e_sm,
-                                          const float* __restrict__ joints_sm, const float (&qj)[JP], float iq,
-                                          float g2, int k, TopK<KT, int32_t>& top) {
-  uint32_t m = 0;
+__device__ __forceinline__ void epi_chunk(uint32_t taddr, int64_t jbase, int nvalid,
+                                          const float* __restrict__ inv_sm, const float* __restrict__ jsm,
+                                          const uint64_t (&QQ)[4], const float (&qj)[JP], uint64_t IQ2, float iq,
+                                          float g2, float bound, int k, TopK<KT, int32_t>& top) {
+  constexpr int JF = JP < 4 ? JP : 4;   // joints in the filter
+  uint32_t fire = 0;                    // bit sub: some column of sub-chunk sub may be admitted
+  if (GATED) {
 #pragma unroll
-  for (int c = 0; c < kChunk; c += 4) {
-    const float4 ie = *reinterpret_cast<const float4*>(inv_e_sm + c);
-    const float iev[4] = {ie.x, ie.y, ie.z, ie.w};
+    for (int sub = 0; sub < 4; ++sub) {
+      float mn = CUDART_INF_F;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int cc = c + u;
-      const float s = __fmul_rn(__fmul_rn(__uint_as_float(v[cc]), iq), iev[u]);
-      bool cand = (s > top.kth_s) && (jbase + cc < row_end);
-      if (GATED) {
-        const float4* pj = reinterpret_cast<const float4*>(joints_sm + cc * JP);
-        float4 p = pj[0];
-        float df = __fsub_rn(qj[0], p.x);
-        float ds = __fmaf_rn(df, df, 0.0f);
-        df = __fsub_rn(qj[1], p.y);
-        ds = __fmaf_rn(df, df, ds);
-        df = __fsub_rn(qj[2], p.z);
-        ds = __fmaf_rn(df, df, ds);
-        df = __fsub_rn(qj[3], p.w);
-        ds = __fmaf_rn(df, df, ds);
-        cand = cand && (ds <= g2);
-        if (JP > 4) {
-          if (__any_sync(0xffffffffu, cand)) {
+      for (int c4 = 2 * sub; c4 < 2 * sub + 2; ++c4) {
+        uint64_t da = 0ull, db = 0ull;   // +0.0f pairs
 #pragma unroll
-            for (int g = 1; g < JP / 4; ++g) {
-              p = pj[g];
-              df = __fsub_rn(qj[4 * g + 0], p.x);
-              ds = __fmaf_rn(df, df, ds);
-              df = __fsub_rn(qj[4 * g + 1], p.y);
-              ds = __fmaf_rn(df, df, ds);
-              df = __fsub_rn(qj[4 * g + 2], p.z);
-              ds = __fmaf_rn(df, df, ds);
-              df = __fsub_rn(qj[4 * g + 3], p.w);
-              ds = __fmaf_rn(df, df, ds);
-              cand = cand && (ds <= g2);
-              if (!__any_sync(0xffffffffu, cand)) break;
-            }
-          }
+        for (int t = 0; t < JF; ++t) {
+          const float4 p = lds4(jsm + t * kBlockN + 4 * c4);
+          const uint64_t a = ptx::sub2(QQ[t], ptx::pack2(p.x, p.y));
+          da = ptx::fma2(a, a, da);
+          const uint64_t b = ptx::sub2(QQ[t], ptx::pack2(p.z, p.w));
+          db = ptx::fma2(b, b, db);
         }
+        mn = fminf(mn, fminf(fminf(ptx::lo2(da), ptx::hi2(da)), fminf(ptx::lo2(db), ptx::hi2(db))));
       }
-      m |= (cand ? 1u : 0u) << cc;
+      fire |= (mn <= g2 ? 1u : 0u) << sub;
+    }
+  } else {
+    uint32_t v[32];
+    ptx::tmem_ld32(taddr, v);
+    ptx::tmem_wait_ld();
+#pragma unroll
+    for (int sub = 0; sub < 4; ++sub) {
+      float mx = -CUDART_INF_F;
+#pragma unroll
+      for (int c4 = 2 * sub; c4 < 2 * sub + 2; ++c4) {
+        const float4 ie = lds4(inv_sm + 4 * c4);
+        const uint64_t a =
+            ptx::mul2(ptx::mul2(ptx::pack2(__uint_as_float(v[4 * c4]), __uint_as_float(v[4 * c4 + 1])), IQ2),
+                      ptx::pack2(ie.x, ie.y));
+        const uint64_t b =
+            ptx::mul2(ptx::mul2(ptx::pack2(__uint_as_float(v[4 * c4 + 2]), __uint_as_float(v[4 * c4 + 3])), IQ2),
+                      ptx::pack2(ie.z, ie.w));
+        mx = fmaxf(mx, fmaxf(fmaxf(ptx::lo2(a), ptx::hi2(a)), fmaxf(ptx::lo2(b), ptx::hi2(b))));
+      }
+      fire |= (mx > top.kth_s && mx >= bound ? 1u : 0u) << sub;
     }
   }
-  // rare path: insert candidates; re-read the accumulator column (warp-uniform loop,
-  // tcgen05.ld is warp-collective) and recompute the identical score.
-  uint32_t wm = __reduce_or_sync(0xffffffffu, m);
-  while (wm != 0u) {
-    const int c = __ffs(wm) - 1;
-    wm &= wm - 1u;
-    const uint32_t raw = ptx::tmem_ld1(taddr + (uint32_t)c);
+  uint32_t wfire = __reduce_or_sync(0xffffffffu, fire);
+  // exact path (rare), sub-chunk by sub-chunk; tcgen05.ld is warp-collective and the
+  // loop is warp-uniform
+  while (wfire != 0u) {
+    const int sub = __ffs(wfire) - 1;
+    wfire &= wfire - 1u;
+    uint32_t v8[8];
+    ptx::tmem_ld8(taddr + (uint32_t)(sub * 8), v8);
     ptx::tmem_wait_ld();
-    if ((m >> c) & 1u) {
-      const float s = __fmul_rn(__fmul_rn(__uint_as_float(raw), iq), inv_e_sm[c]);
-      if (s > top.kth_s) top.insert_monotone(s, (int32_t)(jbase + c), k);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int cc = sub * 8 + c;
+      const float s = __fmul_rn(__fmul_rn(__uint_as_float(v8[c]), iq), inv_sm[cc]);
+      bool ok = (s > top.kth_s) && (s >= bound) && (cc < nvalid);
+      if (GATED) {
+        float ds = 0.0f;
+#pragma unroll
+        for (int g = 0; g < JP / 4; ++g) {
+          if (!__any_sync(0xffffffffu, ok)) break;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float df = __fsub_rn(qj[4 * g + u], jsm[(4 * g + u) * kBlockN + cc]);
+            ds = __fmaf_rn(df, df, ds);
+          }
+          ok = ok && (ds <= g2);
+        }
+      }
+      if (ok) top.insert_monotone(s, (int32_t)(jbase + cc), k);
     }
   }
 }
 
-template <int KT, int JP>
-__global__ void __launch_bounds__(kThreadsTc, 1)
+template <int KT, int JP, int CG>
+__global__ void __maxnreg__(168)
     match_tc_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_pool,
                     const TcParams prm) {
-  constexpr int STAGES = stages_for(JP);
-  constexpr uint32_t AUXJ = SmemLayout<JP>::aux_j_bytes;
-  constexpr uint32_t AUX = SmemLayout<JP>::aux_bytes;
+  constexpr int STAGES = stages_for<JP, CG>();
+  constexpr uint32_t AUXJ = Aux<JP>::j_bytes;
+  constexpr uint32_t AUX = Aux<JP>::bytes;
+  constexpr uint32_t BBYTES = Geo<CG>::b_bytes;
+  constexpr uint32_t STAGE = Geo<CG>::stage_bytes;
 
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // keep every pointer derived from smem_raw so loads stay in the shared window
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;                                   // STAGES x 16 KB
-  uint8_t* sB = smem + STAGES * kABytes;                // STAGES x 32 KB
-  uint8_t* sAux = smem + STAGES * kStageBytes;          // 2 x AUX
+  uint8_t* sB = smem + STAGES * kABytes;                // STAGES x BBYTES
+  uint8_t* sAux = smem + STAGES * STAGE;                // 2 x AUX
   uint64_t* bars = reinterpret_cast<uint64_t*>(sAux + 2 * AUX);
   uint64_t* full = bars;
   uint64_t* empty = bars + STAGES;
@@ -159,6 +205,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t crank = CG == 2 ? ptx::cluster_ctarank() : 0u;
+  const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmap_q);
@@ -169,18 +217,19 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&tfull[i], 1);
-      ptx::mbar_init(&tempty[i], 4 * kEpiHalves);
+      ptx::mbar_init(&tempty[i], 4 * kEpiHalves * CG);
       ptx::mbar_init(&afull[i], 1);
       ptx::mbar_init(&aempty[i], 4 * kEpiHalves);
     }
     ptx::fence_mbar_init();
   }
   if (warp == 1) {
-    ptx::tmem_alloc(tmem_holder, kTmemCols);
-    ptx::tmem_relinquish();
+    ptx::tmem_alloc<CG>(tmem_holder, kTmemCols);
+    ptx::tmem_relinquish<CG>();
   }
   ptx::tc_fence_before();
   __syncthreads();
+  if (CG == 2) ptx::cluster_sync();   // peer barriers initialised before any remote traffic
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
@@ -194,10 +243,11 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       int stage = 0;
       uint32_t phase = 0;
       uint32_t tile_count = 0;
-      for (int u = blockIdx.x; u < prm.n_units; u += gridDim.x) {
+      for (int u = cid; u < prm.n_units; u += ncl) {
         const int sp = u / prm.n_qt, qt = u % prm.n_qt;
         int t_lo, t_hi;
         split_tiles(sp, prm.S, prm.n_pt, t_lo, t_hi);
+        const int qrow0 = qt * kBlockM * CG + (int)crank * kBlockM;
         for (int t = t_lo; t < t_hi; ++t, ++tile_count) {
           const int buf = tile_count & 1;
           const uint32_t use = tile_count >> 1;
@@ -206,12 +256,19 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           ptx::mbar_arrive_expect_tx(&afull[buf], AUX);
           ptx::bulk_load(aux, prm.pool_joints + (int64_t)t * kBlockN * JP, AUXJ, &afull[buf]);
           ptx::bulk_load(aux + AUXJ, prm.pool_inv + (int64_t)t * kBlockN, kBlockN * 4, &afull[buf]);
+          const int prow0 = t * kBlockN + (int)crank * (int)Geo<CG>::b_rows;
           for (int kb = 0; kb < n_kb; ++kb) {
             ptx::mbar_wait(&empty[stage], phase ^ 1u);
-            ptx::mbar_arrive_expect_tx(&full[stage], kStageBytes);
-            ptx::tma_load_2d(sA + stage * kABytes, &tmap_q, &full[stage], kb * kBlockK, qt * kBlockM, pol_q);
-            ptx::tma_load_2d(sB + stage * kBBytes, &tmap_pool, &full[stage], kb * kBlockK, t * kBlockN,
-                             pol_pool);
+            if (CG == 1) {
+              ptx::mbar_arrive_expect_tx(&full[stage], STAGE);
+              ptx::tma_load_2d(sA + stage * kABytes, &tmap_q, &full[stage], kb * kBlockK, qrow0, pol_q);
+              ptx::tma_load_2d(sB + stage * BBYTES, &tmap_pool, &full[stage], kb * kBlockK, prow0, pol_pool);
+            } else {
+              if (crank == 0) ptx::mbar_arrive_expect_tx(&full[stage], CG * STAGE);
+              const uint32_t fb = ptx::mapa(ptx::smem_u32(&full[stage]), 0);
+              ptx::tma_load_2d_pair(sA + stage * kABytes, &tmap_q, fb, kb * kBlockK, qrow0, pol_q);
+              ptx::tma_load_2d_pair(sB + stage * BBYTES, &tmap_pool, fb, kb * kBlockK, prow0, pol_pool);
+            }
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1u;
@@ -221,12 +278,12 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    // ------------------------------------------------------------ MMA issuer (leader)
+    if (lane == 0 && crank == 0) {
       int stage = 0;
       uint32_t phase = 0;
       uint32_t tile_count = 0;
-      for (int u = blockIdx.x; u < prm.n_units; u += gridDim.x) {
+      for (int u = cid; u < prm.n_units; u += ncl) {
         const int sp = u / prm.n_qt;
         int t_lo, t_hi;
         split_tiles(sp, prm.S, prm.n_pt, t_lo, t_hi);
@@ -240,19 +297,19 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             ptx::mbar_wait(&full[stage], phase);
             ptx::tc_fence_after();
             const uint32_t a0 = ptx::smem_u32(sA + stage * kABytes);
-            const uint32_t b0 = ptx::smem_u32(sB + stage * kBBytes);
+            const uint32_t b0 = ptx::smem_u32(sB + stage * BBYTES);
 #pragma unroll
             for (int kk = 0; kk < kBlockK / 16; ++kk) {
-              ptx::umma_f16(d_tmem, ptx::sdesc_k_sw128(a0 + kk * 32), ptx::sdesc_k_sw128(b0 + kk * 32), kIdesc,
-                            (kb | kk) != 0 ? 1u : 0u);
+              ptx::umma_f16<CG>(d_tmem, ptx::sdesc_k_sw128(a0 + kk * 32), ptx::sdesc_k_sw128(b0 + kk * 32),
+                                Geo<CG>::idesc, (kb | kk) != 0 ? 1u : 0u);
             }
-            ptx::umma_commit(&empty[stage]);
+            ptx::umma_commit<CG>(&empty[stage]);
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1u;
             }
           }
-          ptx::umma_commit(&tfull[buf]);
+          ptx::umma_commit<CG>(&tfull[buf]);
         }
       }
     }
@@ -264,20 +321,31 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     const int h = e >> 2;              // column half
     uint32_t tile_count = 0;
     const bool gated = prm.gated != 0;
-    for (int u = blockIdx.x; u < prm.n_units; u += gridDim.x) {
+    const uint32_t tempty_leader0 = CG == 2 ? ptx::mapa(ptx::smem_u32(&tempty[0]), 0) : 0u;
+    for (int u = cid; u < prm.n_units; u += ncl) {
       const int sp = u / prm.n_qt, qt = u % prm.n_qt;
       int t_lo, t_hi;
       split_tiles(sp, prm.S, prm.n_pt, t_lo, t_hi);
       const int64_t row_end = min((int64_t)t_hi * kBlockN, prm.L);
-      const int qrow = qt * kBlockM + lg * 32 + lane;
+      const int qrow = qt * kBlockM * CG + (int)crank * kBlockM + lg * 32 + lane;
       const bool active = qrow < prm.nq;
       float qj[JP];
-      float iq = 0.0f;
 #pragma unroll
       for (int t = 0; t < JP; ++t) qj[t] = active ? prm.q_joints[(int64_t)qrow * JP + t] : 0.0f;
-      if (active) iq = prm.inv_q[qrow];
+      uint64_t QQ[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) QQ[t] = ptx::pack2(qj[t], qj[t]);   // JP >= 4
+      const float iq = active ? prm.inv_q[qrow] : 0.0f;
+      const uint64_t IQ2 = ptx::pack2(iq, iq);
+      uint32_t* bnd = prm.bound + (active ? qrow : 0);
+      float bound = -CUDART_INF_F;
+      if (active) {
+        const uint32_t b = *reinterpret_cast<volatile uint32_t*>(bnd);
+        if (b) bound = ptx::ord2f(b);
+      }
       TopK<KT, int32_t> top;
       top.init(active);
+      int since = 0;
       for (int t = t_lo; t < t_hi; ++t, ++tile_count) {
         const int buf = tile_count & 1;
         const uint32_t use = tile_count >> 1;
@@ -291,29 +359,40 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         for (int ch = 0; ch < kColsPerHalf / kChunk; ++ch) {
           const int col0 = h * kColsPerHalf + ch * kChunk;
           const uint32_t taddr = tmem_base + ((uint32_t)(lg * 32) << 16) + (uint32_t)(buf * kBlockN + col0);
-          uint32_t v[32];
-          ptx::tmem_ld32(taddr, v);
-          ptx::tmem_wait_ld();
           const int64_t jbase = (int64_t)t * kBlockN + col0;
+          const int nvalid = (int)max((int64_t)0, min((int64_t)kChunk, row_end - jbase));
           if (gated)
-            epi_chunk<KT, JP, true>(v, taddr, jbase, row_end, inv_sm + col0, joints_sm + col0 * JP, qj, iq,
-                                    prm.g2, prm.k, top);
+            epi_chunk<KT, JP, true>(taddr, jbase, nvalid, inv_sm + col0, joints_sm + col0, QQ, qj, IQ2, iq,
+                                    prm.g2, bound, prm.k, top);
           else
-            epi_chunk<KT, JP, false>(v, taddr, jbase, row_end, inv_sm + col0, joints_sm + col0 * JP, qj, iq,
-                                     prm.g2, prm.k, top);
+            epi_chunk<KT, JP, false>(taddr, jbase, nvalid, inv_sm + col0, joints_sm + col0, QQ, qj, IQ2, iq,
+                                     prm.g2, bound, prm.k, top);
         }
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          ptx::mbar_arrive(&tempty[buf]);
+          if (CG == 1)
+            ptx::mbar_arrive(&tempty[buf]);
+          else
+            ptx::mbar_arrive_cluster(tempty_leader0 + (uint32_t)(buf * sizeof(uint64_t)));
           ptx::mbar_arrive(&aempty[buf]);
+        }
+        // share the admission bound with the other splits of this query
+        if (++since == kRefreshTiles || t + 1 == t_hi) {
+          since = 0;
+          if (active) {
+            if (top.kth_s > -CUDART_INF_F) atomicMax(bnd, ptx::f2ord(top.kth_s));
+            const uint32_t b = *reinterpret_cast<volatile uint32_t*>(bnd);
+            if (b) bound = fmaxf(bound, ptx::ord2f(b));
+          }
         }
       }
       if (active) {
         const int64_t base = ((int64_t)qrow * prm.P + (int64_t)sp * kEpiHalves + h) * KT;
 #pragma unroll
         for (int r = 0; r < KT; r += 4) {
-          *reinterpret_cast<float4*>(prm.part_s + base + r) = make_float4(top.s[r], top.s[r + 1], top.s[r + 2], top.s[r + 3]);
+          *reinterpret_cast<float4*>(prm.part_s + base + r) =
+              make_float4(top.s[r], top.s[r + 1], top.s[r + 2], top.s[r + 3]);
           *reinterpret_cast<int4*>(prm.part_i + base + r) = make_int4(top.i[r], top.i[r + 1], top.i[r + 2], top.i[r + 3]);
         }
       }
@@ -322,43 +401,58 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 
   ptx::tc_fence_before();
   __syncthreads();
+  if (CG == 2) ptx::cluster_sync();   // no CTA leaves while its peer may still signal it
   if (warp == 1) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem_base, kTmemCols);
+    ptx::tmem_dealloc<CG>(tmem_base, kTmemCols);
   }
 }
 
-template <int KT, int JP>
+template <int KT, int JP, int CG>
 cudaError_t launch_tc_t(Pool& p, const TcParams& prm, int grid, cudaStream_t s) {
-  auto kern = match_tc_kernel<KT, JP>;
-  const size_t smem = smem_for<JP>();
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  kern<<<grid, kThreadsTc, smem, s>>>(p.tmap_q, p.tmap_pool, prm);
-  return cudaGetLastError();
+  auto kern = match_tc_kernel<KT, JP, CG>;
+  const size_t smem = smem_for<JP, CG>();
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kThreadsTc);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, p.tmap_q, CG == 1 ? p.tmap_pool : p.tmap_pool2, prm);
 }
 
-template <int KT>
+template <int KT, int CG>
 cudaError_t launch_tc_kt(Pool& p, const TcParams& prm, int grid, cudaStream_t s) {
   switch (p.JP) {
-    case 4: return launch_tc_t<KT, 4>(p, prm, grid, s);
-    case 8: return launch_tc_t<KT, 8>(p, prm, grid, s);
-    default: return launch_tc_t<KT, 16>(p, prm, grid, s);
+    case 4: return launch_tc_t<KT, 4, CG>(p, prm, grid, s);
+    case 8: return launch_tc_t<KT, 8, CG>(p, prm, grid, s);
+    default: return launch_tc_t<KT, 16, CG>(p, prm, grid, s);
+  }
+}
+
+template <int CG>
+cudaError_t launch_tc_cg(Pool& p, const MatchArgs& a, const TcParams& prm, int grid, cudaStream_t s) {
+  switch (a.KT) {
+    case 8: return launch_tc_kt<8, CG>(p, prm, grid, s);
+    case 16: return launch_tc_kt<16, CG>(p, prm, grid, s);
+    case 32: return launch_tc_kt<32, CG>(p, prm, grid, s);
+    default: return launch_tc_kt<64, CG>(p, prm, grid, s);
   }
 }
 
 }  // namespace
 
-int tc_stages(int JP) { return stages_for(JP); }
-size_t tc_smem_bytes(int JP) {
-  return JP <= 4 ? smem_for<4>() : JP <= 8 ? smem_for<8>() : smem_for<16>();
-}
+int tc_query_tile(int cg) { return kBlockM * cg; }
 
-cudaError_t launch_match_tc(Pool& p, const MatchArgs& a, int32_t S, int32_t grid, cudaStream_t s) {
+cudaError_t launch_match_tc(Pool& p, const MatchArgs& a, int32_t S, int32_t grid, int32_t cg, cudaStream_t s) {
   TcParams prm{};
   prm.inv_q = p.q_inv;
   prm.q_joints = p.q_joints;
@@ -366,10 +460,11 @@ cudaError_t launch_match_tc(Pool& p, const MatchArgs& a, int32_t S, int32_t grid
   prm.pool_joints = p.joints;
   prm.part_s = p.part_s;
   prm.part_i = p.part_i;
+  prm.bound = p.bound;
   prm.L = p.local;
   prm.nq = a.nq;
   prm.d = p.cfg.dim;
-  prm.n_qt = (a.nq + kBlockM - 1) / kBlockM;
+  prm.n_qt = (a.nq + kBlockM * cg - 1) / (kBlockM * cg);
   prm.n_pt = (int32_t)((p.local + kBlockN - 1) / kBlockN);
   prm.S = S;
   prm.n_units = prm.n_qt * S;
@@ -377,13 +472,9 @@ cudaError_t launch_match_tc(Pool& p, const MatchArgs& a, int32_t S, int32_t grid
   prm.gated = a.gated;
   prm.P = S * kEpiHalves;
   prm.g2 = a.g2;
-  cudaError_t e;
-  switch (a.KT) {
-    case 8: e = launch_tc_kt<8>(p, prm, grid, s); break;
-    case 16: e = launch_tc_kt<16>(p, prm, grid, s); break;
-    case 32: e = launch_tc_kt<32>(p, prm, grid, s); break;
-    default: e = launch_tc_kt<64>(p, prm, grid, s); break;
-  }
+  cudaError_t e = cudaMemsetAsync(p.bound, 0, (size_t)a.nq * sizeof(uint32_t), s);
+  if (e != cudaSuccess) return e;
+  e = cg == 2 ? launch_tc_cg<2>(p, a, prm, grid, s) : launch_tc_cg<1>(p, a, prm, grid, s);
   ++p.launches;
   return e;
 }

@@ -157,3 +157,54 @@ def test_bf16_host_vs_device_inputs_identical(ams):
     b = run_gpu(ams, w.emb, w.joints, w.q_emb, w.q_joints, cfg.k, cfg.theta, INF, "bf16", host_inputs=True)
     for x, y in zip(a, b):
         assert x.tobytes() == y.tobytes()
+
+
+@pytest.mark.parametrize("nq", [37, 300])
+@pytest.mark.parametrize("gated", [False, True])
+def test_ties_across_splits_lowest_index(ams, nq, gated):
+    """Exact ties (duplicate rows) spread over the whole pool: every merge level must
+    keep (score desc, index asc); the shared admission bound admits equal scores."""
+    rng = np.random.Generator(np.random.PCG64(77))
+    d, J, M, k = 128, 7, 20000, 16
+    base = ams_gen.f32_to_bf16_bits(rng.standard_normal((50, d)).astype(np.float32))
+    emb = base[rng.integers(0, 50, M)]
+    joints = np.zeros((M, J), np.float32)           # all rows eligible under any gate
+    q = base[rng.integers(0, 50, nq)]
+    qj = np.zeros((nq, J), np.float32)
+    gamma = 0.3 if gated else INF
+    orc = oracle.match(emb, joints, q, qj, k, 0.5, gamma)
+    g = run_gpu(ams, emb, joints, q, qj, k, 0.5, gamma, "bf16")
+    # the top-k are all exact duplicates of the query (score ~1, identical bits on GPU)
+    assert np.array_equal(g[0], orc.idx)
+    assert np.array_equal(g[2], orc.hit)
+    assert np.abs(g[1] - orc.score).max() <= 2e-3
+
+
+def test_plan_uses_cta_pairs_and_splits(ams):
+    cfg = ams_gen.small_variant("c3", 30000, 600)
+    w = ams_gen.generate_host(cfg)
+    with ams.Pool(cfg.d, cfg.J, cfg.M, 1024, 32) as pool:
+        pool.append(to_dev(w.emb), to_dev(w.joints))
+        pool.match(to_dev(w.q_emb), to_dev(w.q_joints), cfg.k, cfg.theta, INF)
+        plan = ams.ams_pool_last_plan(pool.handle)
+        assert plan["kernel_id"] == 2 and plan["grid"] % 2 == 0 and plan["splits"] >= 1
+        pool.match(to_dev(w.q_emb[:64]), to_dev(w.q_joints[:64]), cfg.k, cfg.theta, INF)
+        plan = ams.ams_pool_last_plan(pool.handle)
+        assert plan["kernel_id"] == 1 and plan["splits"] > 1
+        torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("k", [1, 9, 17, 33, 64])
+@pytest.mark.parametrize("nq", [5, 200])
+def test_every_topk_width_launches_and_matches(ams, k, nq):
+    """KT in {8, 16, 32, 64} x single-CTA / CTA-pair kernels, plus the k > M padding."""
+    cfg = ams_gen.small_variant("c2", 3000, nq)
+    w = ams_gen.generate_host(cfg)
+    for gamma in (INF, 1.5):
+        orc = oracle.match(w.emb, w.joints, w.q_emb, w.q_joints, k, cfg.theta, gamma)
+        g = run_gpu(ams, w.emb, w.joints, w.q_emb, w.q_joints, k, cfg.theta, gamma, "bf16", max_k=64)
+        check_bf16(*g, orc, cfg.theta)
+    e, j = w.emb[:40], w.joints[:40]
+    orc = oracle.match(e, j, w.q_emb, w.q_joints, k, cfg.theta, INF)
+    g = run_gpu(ams, e, j, w.q_emb, w.q_joints, k, cfg.theta, INF, "bf16", max_k=64)
+    check_bf16(*g, orc, cfg.theta)
