@@ -1,0 +1,135 @@
+"""CPU tests of the boundary and the host logic (no GPU needed).
+
+* libams.so loads and exports every symbol include/ams.h declares;
+* argument validation that needs no device;
+* the block-cyclic shard map (host functions of the C ABI) against brute force;
+* the product path has no CPU fallback and never imports the oracle.
+"""
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def ams():
+    import paper_2508_10259_b200 as m
+    return m
+
+
+def header_symbols():
+    txt = open(os.path.join(ROOT, "include", "ams.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(ams_[a-z_0-9]+)\s*\(", txt)))
+
+
+def test_library_exports_every_declared_symbol(ams):
+    declared = header_symbols()
+    assert len(declared) >= 14
+    out = subprocess.run(["nm", "-D", "--defined-only", ams.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (ams_\w+)", out))
+    missing = [s for s in declared if s not in exported]
+    assert not missing, f"missing exports: {missing}"
+    assert set(declared) == set(ams.EXPORTS)
+    for s in declared:
+        assert hasattr(ams, s), f"binding lacks {s}"
+
+
+def test_library_is_sm100a_only(ams):
+    out = subprocess.run(["cuobjdump", "--list-elf", ams.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(?!100a)\d+", out.replace("sm_100a", ""))
+
+
+def test_abi_version_and_status_strings(ams):
+    assert ams.ams_abi_version() == 1
+    for st, name in ams.STATUS.items():
+        assert ams.ams_status_string(st) == name
+
+
+def test_create_rejects_bad_config_without_device(ams):
+    bad = [dict(dim=100, joint_dim=7), dict(dim=0, joint_dim=7), dict(dim=64, joint_dim=0),
+           dict(dim=64, joint_dim=17), dict(dim=64, joint_dim=7, max_k=65), dict(dim=64, joint_dim=7, max_k=0),
+           dict(dim=64, joint_dim=7, world=2, rank=0)]   # world > 1 needs an NCCL id
+    for b in bad:
+        kw = dict(capacity=16, max_queries=8, max_k=4)
+        kw.update(b)
+        with pytest.raises(ams.AmsError) as e:
+            ams.ams_pool_create(**kw)
+        assert e.value.status == 1
+
+
+def test_null_pool_calls_are_invalid_argument(ams):
+    import ctypes
+    assert ams.lib.ams_pool_size(None, None) == 1
+    assert ams.lib.ams_match(None, None, None, 1, 1, 0.5, 0.3, None, None, None, None) == 1
+    assert ams.lib.ams_pool_append(None, None, None, 0, None, None) == 1
+    assert ams.lib.ams_pool_destroy(None) == 0
+    assert ams.lib.ams_get_nccl_unique_id(None) == 1
+
+
+@pytest.mark.parametrize("cap,world,block", [(100, 1, 0), (100, 3, 0), (1000, 8, 0), (1000, 8, 7),
+                                              (257, 2, 256), (4097, 4, 256), (5, 8, 0)])
+def test_shard_map_brute_force(ams, cap, world, block):
+    owners = np.empty(cap, np.int64)
+    locs = np.empty(cap, np.int64)
+    for o in range(cap):
+        owners[o], locs[o] = ams.ams_shard_locate(cap, world, block, o)
+    B = block if block else -(-cap // world)
+    assert np.array_equal(owners, (np.arange(cap) // B) % world)
+    for r in range(world):
+        mine = np.nonzero(owners == r)[0]
+        # local rows are 0..n-1 in increasing global order (appends stay contiguous)
+        assert np.array_equal(locs[mine], np.arange(mine.size))
+        assert ams.ams_shard_capacity(cap, world, block, r) == mine.size
+    assert sum(ams.ams_shard_capacity(cap, world, block, r) for r in range(world)) == cap
+
+
+def test_shard_locate_rejects_out_of_range(ams):
+    for args in [(10, 1, 0, 10), (10, 1, 0, -1), (10, 0, 0, 0), (10, 2, -1, 0)]:
+        with pytest.raises(ams.AmsError):
+            ams.ams_shard_locate(*args)
+
+
+def test_owned_range_overlaps_matches_map(ams):
+    from paper_2508_10259_b200.dist import owned_range_overlaps
+    for cap, world, block in [(1 << 20, 8, 0), (5000, 3, 256), (1000, 2, 7)]:
+        for lo in range(0, cap, max(1, cap // 17)):
+            hi = min(cap, lo + max(1, cap // 23))
+            for r in range(world):
+                brute = any(ams.ams_shard_locate(cap, world, block, o)[0] == r for o in range(lo, hi)) \
+                    if hi - lo < 5000 else None
+                if brute is not None:
+                    assert owned_range_overlaps(cap, world, block, r, lo, hi) == brute
+
+
+def test_product_package_has_no_oracle_or_fallback():
+    pkg = os.path.join(ROOT, "paper_2508_10259_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in src and "from oracle" not in src, f
+                assert "ams_oracle" not in src, f
+    # and the oracle does not touch the product path
+    for f in os.listdir(os.path.join(ROOT, "oracle")):
+        if f.endswith((".py", ".c", ".h")):
+            src = open(os.path.join(ROOT, "oracle", f)).read()
+            assert not re.search(r"^\s*(import|from)\s+paper_2508_10259_b200", src, re.M), f
+            assert "libams.so" not in src, f
+
+
+def test_binding_fails_loudly_without_library(tmp_path):
+    """Importing the binding with the .so absent must raise (no silent fallback)."""
+    import shutil
+    import sys
+    pkg = os.path.join(ROOT, "paper_2508_10259_b200")
+    dst = tmp_path / "paper_2508_10259_b200"
+    shutil.copytree(pkg, dst, ignore=shutil.ignore_patterns("*.so", "__pycache__"))
+    code = "import sys; sys.path.insert(0, %r); import paper_2508_10259_b200" % str(tmp_path)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True)
+    assert r.returncode != 0 and "no CPU fallback" in r.stderr
