@@ -120,6 +120,18 @@ ams_status_t ams_match(ams_pool_t pool, const void* q_emb, const float* q_joints
                        int32_t k, float threshold, float gate_radius, int64_t* out_index,
                        float* out_score, uint8_t* out_hit, void* stream);
 
+/* The final k-way merge (north_star "a final k-way merge kernel"; step a7 of
+ * DESIGN.md): merges G ranked lists per query -- in_score/in_index are DEVICE arrays
+ * [G, nq, kin] (fp32 score, int64 global index, -1 padding), each list ordered by
+ * (score desc, index asc) -- into out_index/out_score [nq, k] and out_hit [nq] (device)
+ * with the same ordering, padding and hit rule as ams_match.  ams_match uses the same
+ * kernel after its NCCL all-gather; this entry serves callers that shard themselves.
+ * Errors: AMS_ERR_INVALID_ARGUMENT (null pointers, G < 1, nq < 1, kin < 1, k < 1,
+ * k > 64, NaN threshold), AMS_ERR_CUDA. */
+ams_status_t ams_merge_topk(const float* in_score, const int64_t* in_index, int32_t G, int32_t nq,
+                            int32_t kin, int32_t k, float threshold, int64_t* out_index,
+                            float* out_score, uint8_t* out_hit, void* stream);
+
 /* Number of rows appended so far (global).  Host-side counter, no sync. */
 ams_status_t ams_pool_size(ams_pool_t pool, int64_t* n);
 

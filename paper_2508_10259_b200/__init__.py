@@ -26,7 +26,8 @@ STATUS = {0: "AMS_OK", 1: "AMS_ERR_INVALID_ARGUMENT", 2: "AMS_ERR_CAPACITY", 3: 
           4: "AMS_ERR_CUDA", 5: "AMS_ERR_NCCL", 6: "AMS_ERR_UNSUPPORTED", 7: "AMS_ERR_INTERNAL"}
 
 # Every symbol include/ams.h declares (tests check the library exports all of them).
-EXPORTS = ("ams_get_nccl_unique_id", "ams_pool_create", "ams_pool_append", "ams_match", "ams_pool_size",
+EXPORTS = ("ams_get_nccl_unique_id", "ams_pool_create", "ams_pool_append", "ams_match", "ams_merge_topk",
+           "ams_pool_size",
            "ams_pool_destroy", "ams_status_string", "ams_pool_set_profiling", "ams_pool_read_profile",
            "ams_pool_launch_count", "ams_pool_last_plan", "ams_shard_locate", "ams_shard_capacity",
            "ams_abi_version")
@@ -47,7 +48,7 @@ class ams_pool_config_t(ctypes.Structure):
 
 def _load():
     if not os.path.exists(LIB_PATH):
-        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2508_10259_b200.build` "
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python paper_2508_10259_b200/build.py` "
                           "(there is no CPU fallback)")
     L = ctypes.CDLL(LIB_PATH)
     V, I32, I64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
@@ -56,6 +57,7 @@ def _load():
         "ams_pool_create": [ctypes.POINTER(ams_pool_config_t), ctypes.POINTER(V)],
         "ams_pool_append": [V, V, V, I64, ctypes.POINTER(I64), V],
         "ams_match": [V, V, V, I32, I32, ctypes.c_float, ctypes.c_float, V, V, V, V],
+        "ams_merge_topk": [V, V, I32, I32, I32, I32, ctypes.c_float, V, V, V, V],
         "ams_pool_size": [V, ctypes.POINTER(I64)],
         "ams_pool_destroy": [V],
         "ams_pool_set_profiling": [V, I32],
@@ -155,6 +157,12 @@ def ams_match(pool: int, q_emb, q_joints, nq: int, k: int, threshold: float, gat
               out_index, out_score, out_hit, stream=None) -> None:
     _check(lib.ams_match(pool, _ptr(q_emb), _ptr(q_joints), nq, k, threshold, gate_radius, _ptr(out_index),
                          _ptr(out_score), _ptr(out_hit), _stream(stream)), "ams_match")
+
+
+def ams_merge_topk(in_score, in_index, G: int, nq: int, kin: int, k: int, threshold: float, out_index,
+                   out_score, out_hit, stream=None) -> None:
+    _check(lib.ams_merge_topk(_ptr(in_score), _ptr(in_index), G, nq, kin, k, threshold, _ptr(out_index),
+                              _ptr(out_score), _ptr(out_hit), _stream(stream)), "ams_merge_topk")
 
 
 def ams_pool_size(pool: int) -> int:

@@ -1,6 +1,6 @@
 """Build libams.so in-tree with nvcc for sm_100a (no JIT, no torch extension).
 
-    python -m paper_2508_10259_b200.build [--force]
+    python paper_2508_10259_b200/build.py [--force]     (or __graft_entry__.build())
 
 Every .cu under csrc/ is compiled with -gencode arch=compute_100a,code=sm_100a
 -lineinfo -O3 (no fast-math: the fp32 path is bit-exact), then linked into

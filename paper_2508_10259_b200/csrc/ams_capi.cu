@@ -436,6 +436,23 @@ ams_status_t ams_match(ams_pool_t pool, const void* q_emb, const float* q_joints
   return AMS_OK;
 }
 
+ams_status_t ams_merge_topk(const float* in_score, const int64_t* in_index, int32_t G, int32_t nq, int32_t kin,
+                            int32_t k, float threshold, int64_t* out_index, float* out_score, uint8_t* out_hit,
+                            void* stream) {
+  ams_pool_s* pool = nullptr;
+  if (in_score == nullptr || in_index == nullptr || out_index == nullptr || out_score == nullptr ||
+      out_hit == nullptr || G < 1 || nq < 1 || kin < 1 || k < 1 || k > 64 || std::isnan(threshold))
+    return AMS_ERR_INVALID_ARGUMENT;
+  ams::MatchArgs a{};
+  a.nq = nq;
+  a.k = k;
+  a.KT = ams::pick_KT(k);
+  a.threshold = threshold;
+  AMS_CUDA_TRY(ams::launch_merge_lists(a, G, kin, in_score, in_index, out_score, out_index, out_hit,
+                                       static_cast<cudaStream_t>(stream)));
+  return AMS_OK;
+}
+
 ams_status_t ams_pool_size(ams_pool_t pool, int64_t* n) {
   if (pool == nullptr || n == nullptr) return AMS_ERR_INVALID_ARGUMENT;
   *n = pool->p.size;

@@ -131,6 +131,8 @@ cudaError_t launch_merge_shards(Pool& p, const MatchArgs& a, int32_t G, int32_t 
                                 const int64_t* in_i, float* out_s, int64_t* out_i, uint8_t* out_hit,
                                 cudaStream_t s);
 
+cudaError_t launch_merge_lists(const MatchArgs& a, int32_t G, int32_t kin, const float* in_s, const int64_t* in_i,
+                               float* out_s, int64_t* out_i, uint8_t* out_hit, cudaStream_t s);
 int pick_KT(int k);
 
 }  // namespace ams

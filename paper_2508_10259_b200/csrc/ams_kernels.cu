@@ -319,9 +319,8 @@ cudaError_t launch_merge_partials(Pool& p, const MatchArgs& a, int32_t P, float*
   return cudaGetLastError();
 }
 
-cudaError_t launch_merge_shards(Pool& p, const MatchArgs& a, int32_t G, int32_t kin, const float* in_s,
-                                const int64_t* in_i, float* out_s, int64_t* out_i, uint8_t* out_hit,
-                                cudaStream_t s) {
+cudaError_t launch_merge_lists(const MatchArgs& a, int32_t G, int32_t kin, const float* in_s, const int64_t* in_i,
+                               float* out_s, int64_t* out_i, uint8_t* out_hit, cudaStream_t s) {
   const int wpb = 4;
   const unsigned g = blocks_for(a.nq, wpb);
 #define AMS_MS(KT_)                                                                                   \
@@ -334,8 +333,14 @@ cudaError_t launch_merge_shards(Pool& p, const MatchArgs& a, int32_t G, int32_t 
     default: AMS_MS(64); break;
   }
 #undef AMS_MS
-  ++p.launches;
   return cudaGetLastError();
+}
+
+cudaError_t launch_merge_shards(Pool& p, const MatchArgs& a, int32_t G, int32_t kin, const float* in_s,
+                                const int64_t* in_i, float* out_s, int64_t* out_i, uint8_t* out_hit,
+                                cudaStream_t s) {
+  ++p.launches;
+  return launch_merge_lists(a, G, kin, in_s, in_i, out_s, out_i, out_hit, s);
 }
 
 }  // namespace ams

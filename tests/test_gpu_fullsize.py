@@ -1,0 +1,105 @@
+"""GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py times.
+
+C2 (configs[1]): every query gated (oracle mode B) and a 256-query ungated subset
+(mode A).  C3 (configs[2]): the device-generated 1M x 1024 pool, the full 16,384-query
+call bench.py makes; sampled queries are checked against the oracle (gated: 2048
+queries, mode B; ungated: 48 queries, mode A) and every query against the
+by-construction labels (P10).  The CTA-pair kernel, 37 splits and the shared admission
+bound are all active here.
+"""
+import numpy as np
+import pytest
+
+import ams_gen
+import oracle
+from tests.parity import check_bf16
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+INF = float("inf")
+
+
+@pytest.fixture(scope="module")
+def ams():
+    import paper_2508_10259_b200 as m
+    return m
+
+
+def test_c2_full_size(ams):
+    cfg = ams_gen.CONFIGS["c2"]
+    w = ams_gen.generate_host(cfg)
+    dev = torch.device("cuda", 0)
+    with ams.Pool(cfg.d, cfg.J, cfg.M, cfg.Q, cfg.k) as pool:
+        pool.append(torch.from_numpy(w.emb).to(dev), torch.from_numpy(w.joints).to(dev))
+        q = torch.from_numpy(w.q_emb).to(dev)
+        qj = torch.from_numpy(w.q_joints).to(dev)
+        gi, gs, gh = (t.cpu().numpy() for t in pool.match(q, qj, cfg.k, cfg.theta, cfg.gamma))
+        orc = oracle.match(w.emb, w.joints, w.q_emb, w.q_joints, cfg.k, cfg.theta, cfg.gamma, mode="B")
+        check_bf16(gi, gs, gh, orc, cfg.theta, labels=w.labels)
+        nd = w.labels >= 0
+        assert np.array_equal(gh.astype(bool), nd)
+        sel = np.arange(0, cfg.Q, cfg.Q // 256)
+        ui, us, uh = (t.cpu().numpy() for t in pool.match(q, qj, cfg.k, cfg.theta, INF))
+        orc_u = oracle.match(w.emb, w.joints, w.q_emb[sel], w.q_joints[sel], cfg.k, cfg.theta, INF)
+        check_bf16(ui[sel], us[sel], uh[sel], orc_u, cfg.theta)
+
+
+@pytest.fixture(scope="module")
+def c3(ams):
+    cfg = ams_gen.CONFIGS["c3"]
+    dev = torch.device("cuda", 0)
+    pool = ams.Pool(cfg.d, cfg.J, cfg.M, cfg.Q, cfg.k)
+    q, qj, labels, host_e, host_j = ams_gen.build_device_workload(
+        cfg, dev, lambda e, j, n: pool.append(e, j, n), host_copy=True)
+    yield cfg, pool, q, qj, labels.cpu().numpy(), host_e, host_j
+    pool.close()
+
+
+def test_c3_full_size_gated_sampled(ams, c3):
+    cfg, pool, q, qj, labels, host_e, host_j = c3
+    gi, gs, gh = (t.cpu().numpy() for t in pool.match(q, qj, cfg.k, cfg.theta, cfg.gamma))
+    assert ams.ams_pool_last_plan(pool.handle)["kernel_id"] == 2
+    nd = labels >= 0
+    assert np.array_equal(gh.astype(bool), nd)                  # P10 on all 16,384 queries
+    assert np.array_equal(gi[nd, 0], labels[nd])
+    sel = np.arange(0, cfg.Q, cfg.Q // 2048)
+    qn = q.view(torch.int16).cpu().numpy().view(np.uint16)
+    qjn = qj.cpu().numpy()
+    orc = oracle.match(host_e, host_j, qn[sel], qjn[sel], cfg.k, cfg.theta, cfg.gamma, mode="B")
+    check_bf16(gi[sel], gs[sel], gh[sel], orc, cfg.theta)
+
+
+def test_c3_full_size_ungated_sampled(ams, c3):
+    cfg, pool, q, qj, labels, host_e, host_j = c3
+    gi, gs, gh = (t.cpu().numpy() for t in pool.match(q, qj, cfg.k, cfg.theta, INF))
+    sel = np.arange(7, cfg.Q, cfg.Q // 48)[:48]
+    qn = q.view(torch.int16).cpu().numpy().view(np.uint16)
+    qjn = qj.cpu().numpy()
+    orc = oracle.match(host_e, host_j, qn[sel], qjn[sel], cfg.k, cfg.theta, INF, mode="A")
+    stats = check_bf16(gi[sel], gs[sel], gh[sel], orc, cfg.theta)
+    assert stats["rank_checks"] > 0
+    nd = labels >= 0
+    assert np.array_equal(gi[nd, 0], labels[nd])
+
+
+def test_c3_scan_64_sampled(ams, c3):
+    """The north_star 64-query scan (single-CTA kernel, 148 row splits)."""
+    cfg, pool, q, qj, labels, host_e, host_j = c3
+    for gamma in (cfg.gamma, INF):
+        gi, gs, gh = (t.cpu().numpy() for t in pool.match(q[:64].contiguous(), qj[:64].contiguous(), cfg.k,
+                                                           cfg.theta, gamma))
+        plan = ams.ams_pool_last_plan(pool.handle)
+        assert plan["kernel_id"] == 1 and plan["splits"] >= 100
+        qn = q[:64].view(torch.int16).cpu().numpy().view(np.uint16)
+        sel = np.arange(0, 64, 2) if gamma == INF else np.arange(64)
+        orc = oracle.match(host_e, host_j, qn[sel], qj[:64].cpu().numpy()[sel], cfg.k, cfg.theta, gamma,
+                           mode="A" if gamma == INF else "B")
+        check_bf16(gi[sel], gs[sel], gh[sel], orc, cfg.theta)
+
+
+def test_c3_deterministic(ams, c3):
+    cfg, pool, q, qj, labels, host_e, host_j = c3
+    a = [t.cpu().numpy() for t in pool.match(q, qj, cfg.k, cfg.theta, INF)]
+    b = [t.cpu().numpy() for t in pool.match(q, qj, cfg.k, cfg.theta, INF)]
+    for x, y in zip(a, b):
+        assert x.tobytes() == y.tobytes()
