@@ -100,6 +100,7 @@ class ClockSampler:
         if self.th:
             self.th.join(timeout=2)
         sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        pw = [float(r[3]) for r in self.rows if r[3].replace(".", "").isdigit()]
         mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
         reasons = set()
         for r in self.rows:
@@ -107,7 +108,8 @@ class ClockSampler:
                 if v.lower().startswith("active"):
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.rows)}
+                "reasons": sorted(reasons), "samples": len(self.rows),
+                "power_w_median": statistics.median(pw) if pw else None}
 
 
 def parse():
@@ -115,7 +117,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="c3", choices=["c2", "c3", "c3scan", "c4"])
+    ap.add_argument("--workload", default="c3", choices=["c2", "c3", "c3scan", "c4", "c5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ungated", action="store_true", help="gate_radius = +inf")
     ap.add_argument("--no-scan", action="store_true")
@@ -150,28 +152,197 @@ def workload_cfg(args):
 
 
 def config_block(cfg, args, world, gamma):
-    return {"workload": f"{cfg.name} (BASELINE.json configs[{ {'c1': 0, 'c2': 1, 'c3': 2, 'c3scan': 2, 'c4': 3}[cfg.name] }])",
+    return {"workload": f"{cfg.name} (BASELINE.json configs[{ {'c1': 0, 'c2': 1, 'c3': 2, 'c3scan': 2, 'c4': 3, 'c5': 4}[cfg.name] }])",
             "M": cfg.M, "d": cfg.d, "J": cfg.J, "Q": cfg.Q, "k": cfg.k, "theta": cfg.theta,
             "gate_radius": gamma, "pool_dtype": cfg.dtype, "shard": f"rows contiguous over {world} rank(s)",
             "l2": "inputs larger than L2 (pool %.2f GB > 126 MB L2)" % (cfg.M * cfg.d * 2 / 1e9),
             "data": "synthetic (ams_gen recipe, DESIGN.md)"}
 
 
-def oracle_sample(host_e, host_j, q, qj, cfg, gamma, n_s, offset=0):
-    """Time the oracle (mode A, all host cores) on n_s queries; returns (seconds, cores)."""
+def oracle_sample(cfg, dev, qn, qjn, gamma, n_s, offset=0):
+    """Time the oracle (mode A, all host cores) on n_s of the workload's queries against
+    the full pool.  The pool is regenerated chunk by chunk (ams_gen, not timed) and copied
+    to the host; the oracle runs per chunk with the chunk's global ids and its
+    per-chunk lists are merged by oracle.merge -- exact by pin P8 -- so no host copy of
+    the whole pool is needed.  Returns (seconds in the oracle, cores)."""
     import numpy as np
+    import torch
+    import ams_gen
     import oracle
-    sel = (np.arange(n_s) + offset) % q.shape[0]
+    sel = (np.arange(n_s) + offset) % qn.shape[0]
+    q, qj = np.ascontiguousarray(qn[sel]), np.ascontiguousarray(qjn[sel])
+    means = ams_gen.device_means(cfg, dev)
+    keys, ids = [], []
+    t = 0.0
+    nchunks = (cfg.M + ams_gen.CHUNK_ROWS - 1) // ams_gen.CHUNK_ROWS
+    group = max(1, (1 << 20) // ams_gen.CHUNK_ROWS)   # ~1M rows per oracle call
+    for c0 in range(0, nchunks, group):
+        es, js = [], []
+        for c in range(c0, min(nchunks, c0 + group)):
+            e, j = ams_gen.device_pool_chunk(cfg, c, means, dev)
+            es.append(e.view(torch.int16).cpu().numpy().view(np.uint16))
+            js.append(j.cpu().numpy())
+        e = np.concatenate(es)
+        j = np.concatenate(js)
+        rid = np.arange(c0 * ams_gen.CHUNK_ROWS, c0 * ams_gen.CHUNK_ROWS + e.shape[0], dtype=np.int64)
+        t0 = time.perf_counter()
+        r = oracle.match(e, j, q, qj, cfg.k, cfg.theta, gamma, mode="A", row_ids=rid)
+        t += time.perf_counter() - t0
+        keys.append(r.key)
+        ids.append(r.idx)
     t0 = time.perf_counter()
-    oracle.match(host_e, host_j, q[sel], qj[sel], cfg.k, cfg.theta, gamma, mode="A")
-    return time.perf_counter() - t0, oracle.max_threads()
+    oracle.merge(np.stack(keys), np.stack(ids), cfg.k, cfg.theta)
+    t += time.perf_counter() - t0
+    return t, oracle.max_threads()
 
 
 def auto_sample(cfg, cores):
-    # ~1e9 fp64 pair-MACs per core-second: aim for 10-30 s of CPU work in total
+    # ~1e9 fp64 pair-MACs per core-second: aim for ~20 s of CPU work in total
     per_query = cfg.M * cfg.d / 1e9
-    n = int(max(1, min(max(cores, 4), round(20.0 / max(per_query, 1e-6)))))
-    return n
+    return int(max(1, min(max(cores, 4), round(20.0 / max(per_query, 1e-6)))))
+
+
+def run_stream(args):
+    """C5 (configs[4]) streaming record-and-replay.  A step = one simulated 20 ms robot
+    step: ams_pool_append of 256 new contexts, then the step's 256 queries (50 %
+    near-duplicates of rows appended <= 50 steps ago or of initial rows, 50 % mixture)
+    in seeded batches of 1..256 (log-uniform).  Every ams_match is timed with CUDA
+    events on the launching stream; value = queries/s over the timed steps."""
+    import numpy as np
+    import torch
+    import ams_gen
+    import paper_2508_10259_b200 as ams
+    from paper_2508_10259_b200 import dist as adist
+
+    rank, world, local = dist_setup(args)
+    cfg = ams_gen.CONFIGS["c5"]
+    dev = torch.device("cuda", local)
+    peaks = load_peaks()
+    T, W = args.steps, max(args.warmup, 3)
+    per_step = 256
+    cap = cfg.M + per_step * (T + W)
+    block = 256
+    pool = adist.create_pool(cfg.d, cfg.J, cap, per_step, cfg.k, dtype="bf16", shard_block=block)
+    dummy = torch.zeros(1, cfg.d, dtype=torch.bfloat16, device=dev)
+    dummy_j = torch.zeros(1, cfg.J, dtype=torch.float32, device=dev)
+
+    def append_fn(e, j, n):
+        pool.append(dummy, dummy_j, n) if e is None else pool.append(e, j, n)
+
+    need = lambda lo, hi: adist.owned_range_overlaps(cap, world, block, rank, lo, hi)  # noqa: E731
+    sup_q, sup_qj, sup_lab = ams_gen.build_device_workload(cfg, dev, append_fn, Q=8192, chunk_needed=need)
+    sup_nd = torch.nonzero(sup_lab >= 0).flatten()
+    sup_fr = torch.nonzero(sup_lab < 0).flatten()
+    # pre-generate every step's rows and queries (generation stays out of the timed region)
+    g = torch.Generator(device=dev).manual_seed(cfg.seed * 1_000_003 + 777)
+    rows, queries = [], []
+    sigma = 0.05 / math.sqrt(cfg.d)
+    for s in range(T + W):
+        e, j = ams_gen.stream_rows(cfg, s, per_step, dev)
+        rows.append((e, j))
+        n_nd = per_step // 2
+        n_recent = n_nd // 2
+        lo = max(0, s - 50)
+        src_step = torch.randint(lo, s + 1, (n_recent,), generator=g, device=dev)
+        src_row = torch.randint(0, per_step, (n_recent,), generator=g, device=dev)
+        re = torch.stack([rows[int(a)][0][int(b)] for a, b in zip(src_step.tolist(), src_row.tolist())]).float()
+        rj = torch.stack([rows[int(a)][1][int(b)] for a, b in zip(src_step.tolist(), src_row.tolist())])
+        qa = re + sigma * torch.randn(re.shape, generator=g, device=dev)
+        qa = qa / torch.linalg.vector_norm(qa, dim=1, keepdim=True)
+        qaj = rj + 0.02 * torch.randn(rj.shape, generator=g, device=dev)
+        pick_nd = sup_nd[torch.randint(0, sup_nd.numel(), (n_nd - n_recent,), generator=g, device=dev)]
+        pick_fr = sup_fr[torch.randint(0, sup_fr.numel(), (per_step - n_nd,), generator=g, device=dev)]
+        q = torch.cat([qa.to(torch.bfloat16), sup_q[pick_nd], sup_q[pick_fr]])
+        qj = torch.cat([qaj, sup_qj[pick_nd], sup_qj[pick_fr]]).float()
+        perm = torch.randperm(per_step, generator=g, device=dev)
+        queries.append((q[perm].contiguous(), qj[perm].contiguous(), ams_gen.batch_sizes(per_step, seed=s)))
+    torch.cuda.synchronize()
+    out_i = torch.empty(per_step, cfg.k, dtype=torch.int64, device=dev)
+    out_s = torch.empty(per_step, cfg.k, dtype=torch.float32, device=dev)
+    out_h = torch.empty(per_step, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    n_events = sum(len(queries[s][2]) for s in range(W, T + W))
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_events)]
+    step_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(T)]
+
+    def run_step(s, timed, ev_i):
+        e, j = rows[s]
+        pool.append(e, j, per_step, stream)
+        q, qj, sizes = queries[s]
+        off = 0
+        for b in sizes:
+            if timed:
+                evs[ev_i][0].record(stream)
+            ams.ams_match(pool.handle, q[off:off + b], qj[off:off + b], b, cfg.k, cfg.theta, cfg.gamma,
+                          out_i, out_s, out_h, stream)
+            if timed:
+                evs[ev_i][1].record(stream)
+                ev_i += 1
+            off += b
+        return ev_i
+
+    for s in range(W):
+        run_step(s, False, 0)
+    torch.cuda.synchronize()
+    clk = ClockSampler(torch.cuda.current_device())
+    clk.start()
+    time.sleep(0.15)
+    l0 = ams.ams_pool_launch_count(pool.handle)
+    if world > 1:
+        import torch.distributed as tdist
+        tdist.barrier()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    ev_i = 0
+    for i, s in enumerate(range(W, T + W)):
+        step_ev[i][0].record(stream)
+        ev_i = run_step(s, True, ev_i)
+        step_ev[i][1].record(stream)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    launches = ams.ams_pool_launch_count(pool.handle) - l0
+    clocks = clk.stop()
+    lat = np.array([a.elapsed_time(b) for a, b in evs])
+    steps_ms = np.array([a.elapsed_time(b) for a, b in step_ev])
+    total = t0.elapsed_time(t1)
+    if world > 1:
+        import torch.distributed as tdist
+        tt = torch.tensor([total, float(np.percentile(lat, 50)), float(np.percentile(lat, 99))],
+                          dtype=torch.float64, device=dev)
+        tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
+        total, p50, p99 = tt.tolist()
+        tdist.barrier()
+    else:
+        p50, p99 = float(np.percentile(lat, 50)), float(np.percentile(lat, 99))
+    m_now = pool.size
+    shard_rows = -(-m_now // world)
+    bytes_call = shard_rows * (2 * cfg.d + 4 * cfg.J + 4)
+    value = per_step * T / (total / 1e3)
+    if rank == 0:
+        gbs = bytes_call / (np.median(lat) / 1e3) / 1e9
+        line = {"metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": T, "warmup": W,
+                "ms_per_step": total / T, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "bf16", "data": "synthetic",
+                "config": {"workload": "c5 (BASELINE.json configs[4]) streaming record-and-replay",
+                           "M0": cfg.M, "d": cfg.d, "J": cfg.J, "k": cfg.k, "theta": cfg.theta,
+                           "gate_radius": cfg.gamma, "appends_per_step": per_step, "queries_per_step": per_step,
+                           "batches": "log-uniform 1..256 (seeded)", "shard": f"block-cyclic 256 over {world} rank(s)",
+                           "l2": "inputs larger than L2 (pool %.1f GB)" % (m_now * cfg.d * 2 / 1e9)},
+                "latency_ms": {"p50": p50, "p99": p99, "max": float(lat.max()), "calls": int(lat.size)},
+                "step_ms": {"p50": float(np.percentile(steps_ms, 50)), "max": float(steps_ms.max()),
+                            "fits_20ms_step": bool(steps_ms.max() < 20.0)},
+                "pool_scan_gbps_per_gpu_p50": gbs,
+                "roofline": {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                             "frac": gbs / peaks["hbm_gbs"], "traffic": None,
+                             "note": "whole ams_match call (prep + scan kernel + merge) at the median batch"},
+                "clocks": clocks, "gpu_launches": launches, "e2e": None, "cpu_baseline": None}
+        print(json.dumps(line), flush=True)
+    pool.close()
+    if world > 1:
+        import torch.distributed as tdist
+        tdist.destroy_process_group()
 
 
 def run_reference(args):
@@ -188,7 +359,7 @@ def run_reference(args):
     gamma = float("inf") if args.ungated else cfg.gamma
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0"))) if torch.cuda.is_available() else torch.device("cpu")
     noop = lambda e, j, n: None  # noqa: E731
-    q, qj, labels, host_e, host_j = ams_gen.build_device_workload(cfg, dev, noop, host_copy=True)
+    q, qj, labels = ams_gen.build_device_workload(cfg, dev, noop, chunk_needed=lambda lo, hi: False)
     q = q.view(torch.int16).cpu().numpy().view(np.uint16)
     qj = qj.cpu().numpy()
     cores = oracle.max_threads()
@@ -197,10 +368,10 @@ def run_reference(args):
     while n_s > 1 and n_s * per_query_s * (args.steps + args.warmup) > 240:
         n_s //= 2
     for w in range(args.warmup):
-        oracle_sample(host_e, host_j, q, qj, cfg, gamma, n_s, offset=w * n_s)
+        oracle_sample(cfg, dev, q, qj, gamma, n_s, offset=w * n_s)
     t = 0.0
     for s in range(args.steps):
-        dt, cores = oracle_sample(host_e, host_j, q, qj, cfg, gamma, n_s, offset=(args.warmup + s) * n_s)
+        dt, cores = oracle_sample(cfg, dev, q, qj, gamma, n_s, offset=(args.warmup + s) * n_s)
         t += dt
     value = args.steps * n_s / t
     line = {"metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
@@ -209,7 +380,8 @@ def run_reference(args):
             "config": config_block(cfg, args, 1, gamma),
             "cpu_baseline": {"value": value, "unit": "queries/s", "cores": cores, "kind": "oracle",
                              "sample": f"{n_s} queries per step of {cfg.name} against the full pool "
-                                       f"({cfg.M} rows), oracle mode A (fp64 brute force), OpenMP over queries"},
+                                       f"({cfg.M} rows), oracle mode A (fp64 brute force, OpenMP over queries) "
+                                       f"per ~1M-row chunk + oracle.merge"},
             "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -218,6 +390,9 @@ def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+        return
+    if args.workload == "c5":
+        run_stream(args)
         return
     import numpy as np
     import torch
@@ -258,8 +433,7 @@ def main():
 
     need = lambda lo, hi: adist.owned_range_overlaps(cfg.M, world, 0, rank, lo, hi)  # noqa: E731
     want_cpu = (not args.no_cpu_baseline) and world == 1 and rank == 0
-    built = ams_gen.build_device_workload(cfg, dev, append_fn, chunk_needed=need, host_copy=want_cpu)
-    q, qj, labels = built[:3]
+    q, qj, labels = ams_gen.build_device_workload(cfg, dev, append_fn, chunk_needed=need)
     torch.cuda.synchronize()
     assert pool.size == cfg.M
 
@@ -386,16 +560,16 @@ def main():
     # ------------------------------------------------------------------ CPU oracle baseline
     cpu = None
     if want_cpu:
-        host_e, host_j = built[3], built[4]
         qn = q.view(torch.int16).cpu().numpy().view(np.uint16)
         qjn = qj.cpu().numpy()
         import oracle
         cores = oracle.max_threads()
         n_s = args.cpu_sample or auto_sample(cfg, cores)
-        dt, cores = oracle_sample(host_e, host_j, qn, qjn, cfg, gamma, n_s)
+        dt, cores = oracle_sample(cfg, dev, qn, qjn, gamma, n_s)
         cpu = {"value": n_s / dt, "unit": "queries/s", "cores": cores, "kind": "oracle",
                "sample": f"first {n_s} of the {cfg.Q} {cfg.name} queries against the full {cfg.M}-row pool, "
-                         f"oracle mode A (fp64 brute force, OpenMP over queries), {dt:.1f} s wall"}
+                         f"oracle mode A (fp64 brute force, OpenMP over queries) per ~1M-row chunk + oracle.merge, "
+                         f"{dt:.1f} s in the oracle"}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,

@@ -17,7 +17,7 @@ import os
 from typing import Optional
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libams.so")
+LIB_PATH = os.environ.get("AMS_LIBRARY") or os.path.join(_HERE, "libams.so")  # override: diagnostics only
 
 AMS_OK = 0
 AMS_DTYPE_BF16 = 0

@@ -21,6 +21,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libams.so")
+# diagnostic variant (never loaded by the product path unless AMS_LIBRARY points at it)
+DIAG = os.environ.get("AMS_BUILD_DIAG")
 BUILD = os.path.join(ROOT, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -49,6 +51,10 @@ def _stale(out, deps):
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    global OUT, BUILD
+    if DIAG:
+        OUT = os.path.join(ROOT, "diag_lib", "libams_diag.so")  # travels with gpurun (build/ does not)
+        BUILD = os.path.join(ROOT, "build", "diag")
     os.makedirs(BUILD, exist_ok=True)
     inc, lib = nccl_dirs()
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
@@ -57,6 +63,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return OUT
     common = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
               "-I", os.path.join(ROOT, "include"), "-I", inc, "-Xptxas", "-v"]
+    if DIAG:
+        common += [f"-D{DIAG}"]
 
     def compile_one(src):
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")

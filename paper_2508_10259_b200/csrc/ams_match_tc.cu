@@ -361,6 +361,9 @@ __global__ void __maxnreg__(168)
           const uint32_t taddr = tmem_base + ((uint32_t)(lg * 32) << 16) + (uint32_t)(buf * kBlockN + col0);
           const int64_t jbase = (int64_t)t * kBlockN + col0;
           const int nvalid = (int)max((int64_t)0, min((int64_t)kChunk, row_end - jbase));
+#ifdef AMS_DIAG_NO_EPILOGUE  // diagnostic builds only (scripts/diag_power.py): MMA + TMA alone
+          continue;
+#endif
           if (gated)
             epi_chunk<KT, JP, true>(taddr, jbase, nvalid, inv_sm + col0, joints_sm + col0, QQ, qj, IQ2, iq,
                                     prm.g2, bound, prm.k, top);

@@ -42,17 +42,22 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-// arrive on an mbarrier of another CTA of the cluster (shared::cluster address)
+// arrive on an mbarrier of another CTA of the cluster (shared::cluster address).  Used
+// only to hand TMEM back to the leader's MMA thread: tcgen05.wait::ld +
+// tcgen05.fence::before_thread_sync order the TMEM reads, so the default (.release.cta)
+// semantics suffice -- a .release.cluster arrive costs a MEMBAR.GPU per call.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+// try_wait with a suspend-time hint: the warp sleeps until the phase completes (or the
+// hint expires) instead of re-polling -- fewer issued retries, less power while idle.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "AMS_WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra AMS_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "r"(parity), "r"(0x989680u)
       : "memory");
 }
 
