@@ -1,0 +1,90 @@
+"""GPU parity at the largest BASELINE.json sizes (C4: 16,777,216 x 1024; C5 initial pool:
+4,194,304 x 4096), in bench.py's launch configuration, on sampled outputs.
+
+The pools are 32 GB each, so the oracle is streamed: the device generator regenerates
+the pool in ~1M-row groups, each group is copied to the host and the oracle runs on it
+with the group's global row ids; the per-group lists are merged by oracle.merge (exact
+by pin P8).  Every query is also checked against the by-construction labels (P10).
+"""
+import numpy as np
+import pytest
+
+import ams_gen
+import oracle
+from tests.parity import check_bf16
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+INF = float("inf")
+
+
+@pytest.fixture(scope="module")
+def ams():
+    import paper_2508_10259_b200 as m
+    return m
+
+
+def streamed_oracle(cfg, dev, q, qj, sample_sets):
+    """sample_sets: list of (sel, gamma, mode); returns one merged oracle result per set
+    (top-k plus the exact (k+1)-th key for the gap rule: every group contributes its
+    top-(k+1))."""
+    means = ams_gen.device_means(cfg, dev)
+    nchunks = (cfg.M + ams_gen.CHUNK_ROWS - 1) // ams_gen.CHUNK_ROWS
+    group = max(1, (1 << 20) // ams_gen.CHUNK_ROWS)
+    kk = cfg.k + 1
+    parts = [([], []) for _ in sample_sets]
+    for c0 in range(0, nchunks, group):
+        es, js = [], []
+        for c in range(c0, min(nchunks, c0 + group)):
+            e, j = ams_gen.device_pool_chunk(cfg, c, means, dev)
+            es.append(e.view(torch.int16).cpu().numpy().view(np.uint16))
+            js.append(j.cpu().numpy())
+        e, j = np.concatenate(es), np.concatenate(js)
+        rid = np.arange(c0 * ams_gen.CHUNK_ROWS, c0 * ams_gen.CHUNK_ROWS + e.shape[0], dtype=np.int64)
+        for (sel, gamma, mode), (keys, ids) in zip(sample_sets, parts):
+            r = oracle.match(e, j, q[sel], qj[sel], kk, cfg.theta, gamma, mode=mode, row_ids=rid)
+            keys.append(r.key)
+            ids.append(r.idx)
+    out = []
+    for (sel, gamma, mode), (keys, ids) in zip(sample_sets, parts):
+        m = oracle.merge(np.stack(keys), np.stack(ids), kk, cfg.theta)
+        r = oracle.Result(len(sel), cfg.k)
+        r.idx, r.score, r.key = m.idx[:, :cfg.k].copy(), m.score[:, :cfg.k].copy(), m.key[:, :cfg.k].copy()
+        r.next = m.key[:, cfg.k].copy()
+        r.hit = m.hit
+        r.nelig = (m.idx >= 0).sum(1)
+        out.append(r)
+    return out
+
+
+def run_config(ams, name):
+    cfg = ams_gen.CONFIGS[name]
+    dev = torch.device("cuda", 0)
+    pool = ams.Pool(cfg.d, cfg.J, cfg.M, cfg.Q, cfg.k)
+    q, qj, labels = ams_gen.build_device_workload(cfg, dev, lambda e, j, n: pool.append(e, j, n))
+    assert pool.size == cfg.M
+    res = {}
+    for gamma in (cfg.gamma, INF):
+        res[gamma] = [t.cpu().numpy() for t in pool.match(q, qj, cfg.k, cfg.theta, gamma)]
+    plan = ams.ams_pool_last_plan(pool.handle)
+    pool.close()
+    torch.cuda.synchronize()
+    return cfg, dev, q, qj, labels.cpu().numpy(), res, plan
+
+
+@pytest.mark.parametrize("name", ["c4", "c5"])
+def test_largest_configs_sampled(ams, name):
+    cfg, dev, q, qj, labels, res, plan = run_config(ams, name)
+    nd = labels >= 0
+    gi, gs, gh = res[cfg.gamma]
+    assert np.array_equal(gh.astype(bool), nd)                 # P10 on every query
+    assert np.array_equal(gi[nd, 0], labels[nd])
+    ui, us, uh = res[INF]
+    assert np.array_equal(ui[nd, 0], labels[nd])
+    qn = q.view(torch.int16).cpu().numpy().view(np.uint16)
+    qjn = qj.cpu().numpy()
+    sel_g = np.arange(0, cfg.Q, max(1, cfg.Q // 64))[:64]
+    sel_u = np.arange(3, cfg.Q, max(1, cfg.Q // 8))[:8]
+    og, ou = streamed_oracle(cfg, dev, qn, qjn, [(sel_g, cfg.gamma, "B"), (sel_u, INF, "A")])
+    check_bf16(gi[sel_g], gs[sel_g], gh[sel_g], og, cfg.theta)
+    check_bf16(ui[sel_u], us[sel_u], uh[sel_u], ou, cfg.theta)
