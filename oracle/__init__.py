@@ -61,6 +61,12 @@ def lib():
             L.oracle_gate_g2.restype = ctypes.c_float
             L.oracle_gate_g2.argtypes = [ctypes.c_float]
             L.oracle_max_threads.restype = ctypes.c_int
+            L.oracle_hash_action.restype = ctypes.c_uint64
+            L.oracle_hash_action.argtypes = [P, ctypes.c_int64, ctypes.c_int64, ctypes.c_uint64]
+            L.oracle_hash_segment.restype = ctypes.c_uint64
+            L.oracle_hash_segment.argtypes = [P, ctypes.c_int64, ctypes.c_uint64]
+            L.oracle_hash_actions.restype = None
+            L.oracle_hash_actions.argtypes = [P, P, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, P]
             _lib = L
     return _lib
 
@@ -155,3 +161,30 @@ def gate_g2(gamma):
 
 def max_threads() -> int:
     return int(lib().oracle_max_threads())
+
+
+HASH_B = 257
+HASH_M = (1 << 61) - 1
+HASH_S = 4096
+
+
+def hash_action(data: bytes, s: int = HASH_S, B: int = HASH_B) -> int:
+    """Two-phase action hash (Alg. 1): ams_oracle.c."""
+    buf = np.frombuffer(bytes(data), dtype=np.uint8) if len(data) else np.zeros(1, np.uint8)
+    return int(lib().oracle_hash_action(_p(buf), len(data), s, B))
+
+
+def hash_segment(data: bytes, B: int = HASH_B) -> int:
+    buf = np.frombuffer(bytes(data), dtype=np.uint8) if len(data) else np.zeros(1, np.uint8)
+    return int(lib().oracle_hash_segment(_p(buf), len(data), B))
+
+
+def hash_actions(data: np.ndarray, offsets: np.ndarray, s: int = HASH_S, B: int = HASH_B) -> np.ndarray:
+    """Batch form over a CSR byte buffer: input i is data[offsets[i]:offsets[i+1]]."""
+    data = np.ascontiguousarray(data, dtype=np.uint8)
+    if data.size == 0:
+        data = np.zeros(1, np.uint8)
+    offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+    out = np.empty(len(offsets) - 1, np.uint64)
+    lib().oracle_hash_actions(_p(data), _p(offsets), len(offsets) - 1, s, B, _p(out))
+    return out

@@ -255,3 +255,47 @@ int oracle_max_threads(void) {
   return 1;
 #endif
 }
+
+/* ------------------------------------------------------------------------------------
+ * Two-phase hashing for the action index (3.2.3, Algorithm 1
+ * `lst:impl:index` at PAPER.md:545-574), concretised by SPEC.md:103-111:
+ *   Phase 1: partition the N input bytes into k = ceil(N/s) segments of s bytes (the
+ *            last may be shorter); h_i = polynomial hash of segment i:
+ *            h = 0; for each byte b: h = (h*B + b) mod M.
+ *   Phase 2: H_final = fold over i = 1..k of acc = (acc*B + h_i) mod M, from 0.
+ * B = 257, M = 2^61 - 1.  Empty input -> 0.
+ * Plain sequential definition, one byte at a time, in the paper's order.
+ * ------------------------------------------------------------------------------------ */
+#define ORC_HASH_M ((((uint64_t)1) << 61) - 1)
+
+static uint64_t mulmod61(uint64_t a, uint64_t b) {
+  unsigned __int128 p = (unsigned __int128)a * b;
+  return (uint64_t)(p % ORC_HASH_M);
+}
+
+uint64_t oracle_hash_segment(const uint8_t* data, int64_t n, uint64_t B) {
+  uint64_t h = 0;
+  for (int64_t i = 0; i < n; ++i) h = (mulmod61(h, B) + data[i]) % ORC_HASH_M;
+  return h;
+}
+
+uint64_t oracle_hash_action(const uint8_t* data, int64_t n, int64_t s, uint64_t B) {
+  if (n <= 0 || s <= 0) return 0;
+  uint64_t acc = 0;
+  for (int64_t off = 0; off < n; off += s) {
+    int64_t len = (n - off < s) ? (n - off) : s;
+    uint64_t h = oracle_hash_segment(data + off, len, B);
+    acc = (mulmod61(acc, B) + h) % ORC_HASH_M;
+  }
+  return acc;
+}
+
+/* batch form: inputs [offsets[i], offsets[i+1]) of `data` */
+void oracle_hash_actions(const uint8_t* data, const int64_t* offsets, int32_t n_inputs, int64_t s, uint64_t B,
+                         uint64_t* out) {
+#ifdef _OPENMP
+#pragma omp parallel for schedule(dynamic, 1)
+#endif
+  for (int32_t i = 0; i < n_inputs; ++i)
+    out[i] = oracle_hash_action(data + offsets[i], offsets[i + 1] - offsets[i], s, B);
+}
