@@ -132,6 +132,35 @@ ams_status_t ams_merge_topk(const float* in_score, const int64_t* in_index, int3
                             int32_t kin, int32_t k, float threshold, int64_t* out_index,
                             float* out_score, uint8_t* out_hit, void* stream);
 
+/* ---- two-phase action hash (Algorithm 1) ----
+ * Phase 1 hashes every s-byte segment of every input independently, phase 2 folds an
+ * input's segment hashes ("modular calculation").
+ * Concretisation: h_i = polynomial hash of segment i's bytes,
+ * h = (h*257 + byte) mod (2^61 - 1) from 0; H_final = fold (acc*257 + h_i) mod
+ * (2^61 - 1) from 0; an empty input hashes to 0.  Bit-exact; the result is the
+ * "unique index for action lookup and management" of PAPER.md:541. */
+typedef struct ams_hasher_s* ams_hasher_t;
+
+/* Preallocates a hasher on `device` for up to max_inputs inputs per call and max_bytes
+ * of HOST-resident input bytes per call (device-resident inputs are read in place);
+ * segment_size = s (1..2^24; SPEC default 4096).  Errors: AMS_ERR_INVALID_ARGUMENT,
+ * AMS_ERR_OUT_OF_MEMORY, AMS_ERR_CUDA. */
+ams_status_t ams_hasher_create(int32_t device, int64_t max_inputs, int64_t max_bytes, int64_t segment_size,
+                               ams_hasher_t* out);
+
+/* Hashes n_inputs byte strings: input i is data[offsets[i], offsets[i+1]) (CSR).  `data`
+ * is host or device memory; `offsets` is a HOST array of n_inputs + 1 non-decreasing
+ * int64 values (read synchronously); out_hash is a DEVICE array of n_inputs uint64.
+ * Enqueued on `stream`; a later call waits for the previous call's staging to drain.
+ * Errors: AMS_ERR_INVALID_ARGUMENT (null pointers, n_inputs out of range, decreasing
+ * offsets), AMS_ERR_CAPACITY (host bytes > max_bytes, or too many segments),
+ * AMS_ERR_CUDA. */
+ams_status_t ams_hash_actions(ams_hasher_t hasher, const uint8_t* data, const int64_t* offsets,
+                              int32_t n_inputs, uint64_t* out_hash, void* stream);
+
+/* Synchronises the device and frees the hasher.  NULL is a no-op. */
+ams_status_t ams_hasher_destroy(ams_hasher_t hasher);
+
 /* Number of rows appended so far (global).  Host-side counter, no sync. */
 ams_status_t ams_pool_size(ams_pool_t pool, int64_t* n);
 

@@ -30,7 +30,7 @@ EXPORTS = ("ams_get_nccl_unique_id", "ams_pool_create", "ams_pool_append", "ams_
            "ams_pool_size",
            "ams_pool_destroy", "ams_status_string", "ams_pool_set_profiling", "ams_pool_read_profile",
            "ams_pool_launch_count", "ams_pool_last_plan", "ams_shard_locate", "ams_shard_capacity",
-           "ams_abi_version")
+           "ams_abi_version", "ams_hasher_create", "ams_hash_actions", "ams_hasher_destroy")
 
 
 class AmsError(RuntimeError):
@@ -67,6 +67,9 @@ def _load():
                                ctypes.POINTER(I32)],
         "ams_shard_locate": [I64, I32, I64, I64, ctypes.POINTER(I32), ctypes.POINTER(I64)],
         "ams_shard_capacity": [I64, I32, I64, I32, ctypes.POINTER(I64)],
+        "ams_hasher_create": [I32, I64, I64, I64, ctypes.POINTER(V)],
+        "ams_hash_actions": [V, V, V, I32, V, V],
+        "ams_hasher_destroy": [V],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -209,6 +212,24 @@ def ams_shard_capacity(capacity: int, world: int, shard_block: int, rank: int) -
     n = ctypes.c_int64()
     _check(lib.ams_shard_capacity(capacity, world, shard_block, rank, ctypes.byref(n)), "ams_shard_capacity")
     return n.value
+
+
+def ams_hasher_create(device: int, max_inputs: int, max_bytes: int, segment_size: int = 4096) -> int:
+    out = ctypes.c_void_p()
+    _check(lib.ams_hasher_create(device, max_inputs, max_bytes, segment_size, ctypes.byref(out)), "ams_hasher_create")
+    return out.value
+
+
+def ams_hash_actions(hasher: int, data, offsets, n_inputs: int, out_hash, stream=None) -> None:
+    """offsets: host int64 array [n_inputs + 1]; data host or device; out_hash device u64."""
+    import numpy as np
+    off = np.ascontiguousarray(offsets, dtype=np.int64)
+    _check(lib.ams_hash_actions(hasher, _ptr(data), off.ctypes.data, n_inputs, _ptr(out_hash), _stream(stream)),
+           "ams_hash_actions")
+
+
+def ams_hasher_destroy(hasher: int) -> None:
+    _check(lib.ams_hasher_destroy(hasher), "ams_hasher_destroy")
 
 
 # ----------------------------------------------------------------------------- convenience

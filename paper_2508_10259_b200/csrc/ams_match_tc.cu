@@ -16,13 +16,15 @@
 // contiguous split of the pool rows); persistent clusters walk units in split-major
 // order so concurrent CTAs stream the same pool rows through L2.
 //
-// Warp roles (320 threads per CTA, 1 CTA per SM):
-//   warp 0      TMA producer: query + pool tiles into a STAGES-deep smem ring; pool
+// Warp roles (320 threads per CTA, 1 CTA per SM).  The warp scheduler issues the
+// highest warp id first, so the two latency-critical single-thread roles take the top
+// ids and are never queued behind epilogue math on their sub-partition:
+//   warps 0..7  epilogue: warp w reads TMEM lanes 32*(w%4).. (its 32 queries) of column
+//               half w/4 with tcgen05.ld; one partial list per (query, split, half).
+//   warp 8      TMA producer: query + pool tiles into a STAGES-deep smem ring; pool
 //               joints / inv_norm of each tile into a 2-deep aux ring (bulk copies)
-//   warp 1      TMEM allocator + (leader CTA) single-thread tcgen05.mma issuer;
+//   warp 9      TMEM allocator + (leader CTA) single-thread tcgen05.mma issuer;
 //               accumulators double-buffered in TMEM (2 x 256 columns)
-//   warps 2..9  epilogue: warp w reads TMEM lanes 32*(w%4).. (its 32 queries) of column
-//               half (w-2)/4 with tcgen05.ld; one partial list per (query, split, half).
 //
 // Epilogue per 32-column chunk: a branch-free filter computes, with packed f32x2
 // math, either the chunk's best score (ungated) or the smallest partial joint distance
@@ -208,7 +210,8 @@ __global__ void __maxnreg__(168)
   const uint32_t crank = CG == 2 ? ptx::cluster_ctarank() : 0u;
   const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;
 
-  if (warp == 0 && lane == 0) {
+  constexpr int kProducerWarp = 4 * kEpiHalves, kMmaWarp = 4 * kEpiHalves + 1;
+  if (warp == kProducerWarp && lane == 0) {
     ptx::prefetch_tmap(&tmap_q);
     ptx::prefetch_tmap(&tmap_pool);
     for (int i = 0; i < STAGES; ++i) {
@@ -223,7 +226,7 @@ __global__ void __maxnreg__(168)
     }
     ptx::fence_mbar_init();
   }
-  if (warp == 1) {
+  if (warp == kMmaWarp) {
     ptx::tmem_alloc<CG>(tmem_holder, kTmemCols);
     ptx::tmem_relinquish<CG>();
   }
@@ -235,7 +238,7 @@ __global__ void __maxnreg__(168)
 
   const int n_kb = prm.d / kBlockK;
 
-  if (warp == 0) {
+  if (warp == kProducerWarp) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       const uint64_t pol_q = ptx::policy_evict_last();
@@ -277,7 +280,7 @@ __global__ void __maxnreg__(168)
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer (leader)
     if (lane == 0 && crank == 0) {
       int stage = 0;
@@ -316,9 +319,8 @@ __global__ void __maxnreg__(168)
     __syncwarp();
   } else {
     // ------------------------------------------------------------ epilogue
-    const int e = warp - 2;
     const int lg = warp & 3;           // TMEM lane group accessible to this warp
-    const int h = e >> 2;              // column half
+    const int h = warp >> 2;           // column half
     uint32_t tile_count = 0;
     const bool gated = prm.gated != 0;
     const uint32_t tempty_leader0 = CG == 2 ? ptx::mapa(ptx::smem_u32(&tempty[0]), 0) : 0u;
@@ -405,7 +407,7 @@ __global__ void __maxnreg__(168)
   ptx::tc_fence_before();
   __syncthreads();
   if (CG == 2) ptx::cluster_sync();   // no CTA leaves while its peer may still signal it
-  if (warp == 1) {
+  if (warp == kMmaWarp) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<CG>(tmem_base, kTmemCols);
   }
