@@ -141,9 +141,10 @@ ams_status_t ams_merge_topk(const float* in_score, const int64_t* in_index, int3
  * "unique index for action lookup and management" of PAPER.md:541. */
 typedef struct ams_hasher_s* ams_hasher_t;
 
-/* Preallocates a hasher on `device` for up to max_inputs inputs per call and max_bytes
- * of HOST-resident input bytes per call (device-resident inputs are read in place);
- * segment_size = s (1..2^24; SPEC default 4096).  Errors: AMS_ERR_INVALID_ARGUMENT,
+/* Preallocates a hasher on `device` for up to max_inputs inputs and max_bytes input
+ * bytes per call (host-resident inputs are staged into a device buffer of that size;
+ * device-resident inputs are read in place); segment_size = s (1..2^24; SPEC default
+ * 4096).  Errors: AMS_ERR_INVALID_ARGUMENT,
  * AMS_ERR_OUT_OF_MEMORY, AMS_ERR_CUDA. */
 ams_status_t ams_hasher_create(int32_t device, int64_t max_inputs, int64_t max_bytes, int64_t segment_size,
                                ams_hasher_t* out);
@@ -153,7 +154,7 @@ ams_status_t ams_hasher_create(int32_t device, int64_t max_inputs, int64_t max_b
  * int64 values (read synchronously); out_hash is a DEVICE array of n_inputs uint64.
  * Enqueued on `stream`; a later call waits for the previous call's staging to drain.
  * Errors: AMS_ERR_INVALID_ARGUMENT (null pointers, n_inputs out of range, decreasing
- * offsets), AMS_ERR_CAPACITY (host bytes > max_bytes, or too many segments),
+ * offsets), AMS_ERR_CAPACITY (more than max_bytes input bytes),
  * AMS_ERR_CUDA. */
 ams_status_t ams_hash_actions(ams_hasher_t hasher, const uint8_t* data, const int64_t* offsets,
                               int32_t n_inputs, uint64_t* out_hash, void* stream);

@@ -243,7 +243,7 @@ ams_status_t ams_hash_actions(ams_hasher_t h, const uint8_t* data, const int64_t
   const int64_t total = offsets[n_inputs] - offsets[0];
   if (offsets[0] < 0 || total < 0 || (total > 0 && data == nullptr)) return AMS_ERR_INVALID_ARGUMENT;
   const bool device_data = total > 0 && dev_ptr(data);
-  if (!device_data && total > h->max_bytes) return AMS_ERR_CAPACITY;
+  if (total > h->max_bytes) return AMS_ERR_CAPACITY;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (cudaSetDevice(h->device) != cudaSuccess) return AMS_ERR_CUDA;
   // the pinned staging buffer is reused: wait until the previous call consumed it

@@ -117,7 +117,15 @@ __device__ __forceinline__ void epi_chunk(uint32_t taddr, int64_t jbase, int nva
         uint64_t da = 0ull, db = 0ull;   // +0.0f pairs
 #pragma unroll
         for (int t = 0; t < JF; ++t) {
+#if defined(AMS_DIAG_NO_LDS)
+          const float4 p = make_float4(qj[t] + 10.f + c4, qj[t] - 10.f - c4, qj[t] + 11.f, qj[t] - 12.f);
+#else
           const float4 p = lds4(jsm + t * kBlockN + 4 * c4);
+#endif
+#if defined(AMS_DIAG_LDS_ONLY)
+          asm volatile("" ::"f"(p.x), "f"(p.y), "f"(p.z), "f"(p.w));
+          continue;
+#endif
           const uint64_t a = ptx::sub2(QQ[t], ptx::pack2(p.x, p.y));
           da = ptx::fma2(a, a, da);
           const uint64_t b = ptx::sub2(QQ[t], ptx::pack2(p.z, p.w));
@@ -125,6 +133,9 @@ __device__ __forceinline__ void epi_chunk(uint32_t taddr, int64_t jbase, int nva
         }
         mn = fminf(mn, fminf(fminf(ptx::lo2(da), ptx::hi2(da)), fminf(ptx::lo2(db), ptx::hi2(db))));
       }
+#if defined(AMS_DIAG_LDS_ONLY)
+      mn = CUDART_INF_F;
+#endif
       fire |= (mn <= g2 ? 1u : 0u) << sub;
     }
   } else {
