@@ -120,6 +120,18 @@ ams_status_t ams_match(ams_pool_t pool, const void* q_emb, const float* q_joints
                        int32_t k, float threshold, float gate_radius, int64_t* out_index,
                        float* out_score, uint8_t* out_hit, void* stream);
 
+/* Gate-first sparse variant of ams_match: identical arguments,
+ * semantics, outputs and errors.  It evaluates the canonical joint gate for every
+ * (query, row) pair first -- reading only the pool's joints -- and computes cosine scores
+ * only for eligible pairs (CUDA-core dot products; the scores may differ from ams_match's
+ * tensor-core accumulation in the last fp32 bits, both within the stated tolerance).
+ * Efficient when the gate is selective (few eligible rows per query); with a wide gate
+ * it stays exact but degrades to a per-query scan on the GPU.  fp32 pools use the exact
+ * path of ams_match, which already evaluates the gate first. */
+ams_status_t ams_match_gate_first(ams_pool_t pool, const void* q_emb, const float* q_joints, int32_t nq,
+                                  int32_t k, float threshold, float gate_radius, int64_t* out_index,
+                                  float* out_score, uint8_t* out_hit, void* stream);
+
 /* The final k-way merge (north_star "a final k-way merge kernel"; step a7 of
  * DESIGN.md): merges G ranked lists per query -- in_score/in_index are DEVICE arrays
  * [G, nq, kin] (fp32 score, int64 global index, -1 padding), each list ordered by

@@ -26,7 +26,8 @@ STATUS = {0: "AMS_OK", 1: "AMS_ERR_INVALID_ARGUMENT", 2: "AMS_ERR_CAPACITY", 3: 
           4: "AMS_ERR_CUDA", 5: "AMS_ERR_NCCL", 6: "AMS_ERR_UNSUPPORTED", 7: "AMS_ERR_INTERNAL"}
 
 # Every symbol include/ams.h declares (tests check the library exports all of them).
-EXPORTS = ("ams_get_nccl_unique_id", "ams_pool_create", "ams_pool_append", "ams_match", "ams_merge_topk",
+EXPORTS = ("ams_get_nccl_unique_id", "ams_pool_create", "ams_pool_append", "ams_match", "ams_match_gate_first",
+           "ams_merge_topk",
            "ams_pool_size",
            "ams_pool_destroy", "ams_status_string", "ams_pool_set_profiling", "ams_pool_read_profile",
            "ams_pool_launch_count", "ams_pool_last_plan", "ams_shard_locate", "ams_shard_capacity",
@@ -57,6 +58,7 @@ def _load():
         "ams_pool_create": [ctypes.POINTER(ams_pool_config_t), ctypes.POINTER(V)],
         "ams_pool_append": [V, V, V, I64, ctypes.POINTER(I64), V],
         "ams_match": [V, V, V, I32, I32, ctypes.c_float, ctypes.c_float, V, V, V, V],
+        "ams_match_gate_first": [V, V, V, I32, I32, ctypes.c_float, ctypes.c_float, V, V, V, V],
         "ams_merge_topk": [V, V, I32, I32, I32, I32, ctypes.c_float, V, V, V, V],
         "ams_pool_size": [V, ctypes.POINTER(I64)],
         "ams_pool_destroy": [V],
@@ -162,6 +164,13 @@ def ams_match(pool: int, q_emb, q_joints, nq: int, k: int, threshold: float, gat
                          _ptr(out_score), _ptr(out_hit), _stream(stream)), "ams_match")
 
 
+def ams_match_gate_first(pool: int, q_emb, q_joints, nq: int, k: int, threshold: float, gate_radius: float,
+                         out_index, out_score, out_hit, stream=None) -> None:
+    _check(lib.ams_match_gate_first(pool, _ptr(q_emb), _ptr(q_joints), nq, k, threshold, gate_radius,
+                                    _ptr(out_index), _ptr(out_score), _ptr(out_hit), _stream(stream)),
+           "ams_match_gate_first")
+
+
 def ams_merge_topk(in_score, in_index, G: int, nq: int, kin: int, k: int, threshold: float, out_index,
                    out_score, out_hit, stream=None) -> None:
     _check(lib.ams_merge_topk(_ptr(in_score), _ptr(in_index), G, nq, kin, k, threshold, _ptr(out_index),
@@ -247,7 +256,7 @@ class Pool:
         n = emb.shape[0] if n is None else n
         return ams_pool_append(self.handle, emb, joints, n, stream)
 
-    def match(self, q_emb, q_joints, k, threshold, gate_radius, out=None, stream=None):
+    def match(self, q_emb, q_joints, k, threshold, gate_radius, out=None, stream=None, gate_first=False):
         import torch
         nq = q_emb.shape[0]
         if out is None:
@@ -255,7 +264,8 @@ class Pool:
             out = (torch.empty(nq, k, dtype=torch.int64, device=dev),
                    torch.empty(nq, k, dtype=torch.float32, device=dev),
                    torch.empty(nq, dtype=torch.uint8, device=dev))
-        ams_match(self.handle, q_emb, q_joints, nq, k, threshold, gate_radius, out[0], out[1], out[2], stream)
+        fn = ams_match_gate_first if gate_first else ams_match
+        fn(self.handle, q_emb, q_joints, nq, k, threshold, gate_radius, out[0], out[1], out[2], stream)
         return out
 
     @property

@@ -120,6 +120,7 @@ void plan_simt(const Pool& p, int nq, int KT, int& S) {
 
 void free_all(Pool& p) {
   void* ptrs[] = {p.emb, p.inv_norm, p.joints, p.q_stage, p.q_inv, p.q_joints, p.q_joints_raw, p.bound,
+                  p.gf_cnt, p.gf_cand,
                   p.part_s, p.part_i, p.shard_s, p.shard_i, p.gath_s, p.gath_i, p.stage_emb,
                   p.stage_joints};
   for (void* q : ptrs)
@@ -256,6 +257,10 @@ ams_status_t ams_pool_create(const ams_pool_config_t* cfg, ams_pool_t* out) {
             alloc((void**)&p.shard_i, (size_t)c.max_queries * c.max_k * 8) &&
             alloc(&p.stage_emb, (size_t)p.stage_rows * d * es) &&
             alloc((void**)&p.stage_joints, (size_t)p.stage_rows * c.joint_dim * 4);
+  if (ok && c.dtype == AMS_DTYPE_BF16) {
+    p.gf_cap = std::max(256, 8 * c.max_k);
+    ok = alloc((void**)&p.gf_cnt, (size_t)p.q_pad * 4) && alloc((void**)&p.gf_cand, (size_t)p.q_pad * p.gf_cap * 4);
+  }
   if (ok && c.world > 1)
     ok = alloc((void**)&p.gath_s, (size_t)c.world * c.max_queries * c.max_k * 4) &&
          alloc((void**)&p.gath_i, (size_t)c.world * c.max_queries * c.max_k * 8);
@@ -327,9 +332,9 @@ ams_status_t ams_pool_append(ams_pool_t pool, const void* emb, const float* join
   return AMS_OK;
 }
 
-ams_status_t ams_match(ams_pool_t pool, const void* q_emb, const float* q_joints, int32_t nq, int32_t k,
-                       float threshold, float gate_radius, int64_t* out_index, float* out_score,
-                       uint8_t* out_hit, void* stream) {
+static ams_status_t match_impl(ams_pool_t pool, const void* q_emb, const float* q_joints, int32_t nq, int32_t k,
+                               float threshold, float gate_radius, int64_t* out_index, float* out_score,
+                               uint8_t* out_hit, void* stream, bool gate_first) {
   if (pool == nullptr) return AMS_ERR_INVALID_ARGUMENT;
   Pool& p = pool->p;
   if (p.broken) return AMS_ERR_CUDA;
@@ -386,7 +391,18 @@ ams_status_t ams_match(ams_pool_t pool, const void* q_emb, const float* q_joints
   }
 
   int32_t P = 0;
-  if (p.local > 0) {
+  if (gate_first && p.cfg.dtype == AMS_DTYPE_BF16) {
+    if (e0) AMS_CUDA_TRY(cudaEventRecord(e0, s));
+    AMS_CUDA_TRY(ams::launch_gate_first(p, a, shard_s, shard_i, shard_hit, s));
+    if (e1) {
+      AMS_CUDA_TRY(cudaEventRecord(e1, s));
+      p.ev_pending.emplace_back(e0, e1);
+    }
+    p.last_kernel = 3;
+    p.last_splits = 0;
+    p.last_partials = 0;
+    p.last_grid = 0;
+  } else if (p.local > 0) {
     if (p.cfg.dtype == AMS_DTYPE_FP32) {
       int S;
       plan_simt(p, nq, a.KT, S);
@@ -410,7 +426,7 @@ ams_status_t ams_match(ams_pool_t pool, const void* q_emb, const float* q_joints
     }
     p.last_partials = P;
   }
-  if (e0) {
+  if (e0 && !(gate_first && p.cfg.dtype == AMS_DTYPE_BF16)) {
     if (p.local > 0) {
       p.ev_pending.emplace_back(e0, e1);
     } else {
@@ -418,7 +434,8 @@ ams_status_t ams_match(ams_pool_t pool, const void* q_emb, const float* q_joints
       p.ev_free.push_back(e1);
     }
   }
-  AMS_CUDA_TRY(ams::launch_merge_partials(p, a, P, shard_s, shard_i, shard_hit, s));
+  if (!(gate_first && p.cfg.dtype == AMS_DTYPE_BF16))
+    AMS_CUDA_TRY(ams::launch_merge_partials(p, a, P, shard_s, shard_i, shard_hit, s));
 
   if (multi) {
     ncclComm_t comm = static_cast<ncclComm_t>(p.nccl_comm);
@@ -434,6 +451,20 @@ ams_status_t ams_match(ams_pool_t pool, const void* q_emb, const float* q_joints
                                           out_hit, s));
   }
   return AMS_OK;
+}
+
+ams_status_t ams_match(ams_pool_t pool, const void* q_emb, const float* q_joints, int32_t nq, int32_t k,
+                       float threshold, float gate_radius, int64_t* out_index, float* out_score,
+                       uint8_t* out_hit, void* stream) {
+  return match_impl(pool, q_emb, q_joints, nq, k, threshold, gate_radius, out_index, out_score, out_hit, stream,
+                    false);
+}
+
+ams_status_t ams_match_gate_first(ams_pool_t pool, const void* q_emb, const float* q_joints, int32_t nq, int32_t k,
+                                  float threshold, float gate_radius, int64_t* out_index, float* out_score,
+                                  uint8_t* out_hit, void* stream) {
+  return match_impl(pool, q_emb, q_joints, nq, k, threshold, gate_radius, out_index, out_score, out_hit, stream,
+                    true);
 }
 
 ams_status_t ams_merge_topk(const float* in_score, const int64_t* in_index, int32_t G, int32_t nq, int32_t kin,

@@ -1,0 +1,248 @@
+// ams_gate_first.cu -- gate-first sparse matcher (a variant of the
+// dense path, not the north_star contract).
+//
+// Same function as ams_match: top-k by (score desc, index asc) over the
+// rows that pass the canonical fp32 joint gate, cosine scores, hit flags.  When the gate
+// is selective (reading R14: ~0-2 eligible rows per query in every config) almost all
+// of the dense path's tensor-core work scores ineligible pairs.  This variant evaluates
+// the gate for every (query, row) pair first -- reading only the pool's joints (4*JP
+// bytes per row instead of 2d) -- and computes dot products for eligible pairs only.
+//
+//   K1 gate_scan_kernel   block = 256 queries (thread = query) x a contiguous row split;
+//                         pool joint tiles ([JP][256] fp32, tile-transposed) staged in
+//                         shared memory; packed f32x2 4-joint filter per 8 rows, one warp
+//                         vote, exact canonical gate for fired rows; eligible rows are
+//                         appended to the query's candidate bucket (atomic slot).
+//   K2 score_kernel       warp per query: bf16 dot product per candidate (lanes split d,
+//                         fixed butterfly order), s = (acc*inv_q)*inv_e, register top-k;
+//                         a bucket that overflowed is recomputed exactly by the warp
+//                         scanning every row (rare; exact, on the GPU).
+//   then the shard merge path of ams_match (NCCL all-gather + merge) for world > 1.
+#include <cuda_bf16.h>
+#include <math_constants.h>
+
+#include "ams_internal.cuh"
+#include "ams_ptx.cuh"
+#include "ams_topk.cuh"
+
+namespace ams {
+namespace {
+
+constexpr int kGfThreads = 256;   // queries per block
+constexpr int kGfTile = kRowAlign; // 256 rows per staged joint tile
+
+template <int JP>
+__global__ void __launch_bounds__(kGfThreads)
+    gate_scan_kernel(const float* __restrict__ pool_joints, int64_t L, const float* __restrict__ q_joints,
+                     int32_t nq, int32_t S, float g2, int32_t cap, uint32_t* __restrict__ cnt,
+                     int32_t* __restrict__ cand) {
+  __shared__ __align__(16) float js[2][JP * kGfTile];
+  const int qg = blockIdx.x, sp = blockIdx.y;
+  const int q = qg * kGfThreads + threadIdx.x;
+  const bool active = q < nq;
+  float qj[JP];
+#pragma unroll
+  for (int t = 0; t < JP; ++t) qj[t] = active ? q_joints[(int64_t)q * JP + t] : 1e30f;   // inactive: never eligible
+  uint64_t QQ[4];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) QQ[t] = ptx::pack2(qj[t], qj[t]);
+  const int64_t n_pt = (L + kGfTile - 1) / kGfTile;
+  const int64_t t_lo = n_pt * sp / S, t_hi = n_pt * (sp + 1) / S;
+  auto stage = [&](int64_t t, int buf) {   // cp.async (LDGSTS): does not block the thread
+    const float4* src = reinterpret_cast<const float4*>(pool_joints + t * kGfTile * JP);
+    float4* dst = reinterpret_cast<float4*>(js[buf]);
+    for (int i = threadIdx.x; i < JP * kGfTile / 4; i += kGfThreads)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(ptx::smem_u32(dst + i)), "l"(src + i)
+                   : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if (t_lo < t_hi) stage(t_lo, 0);
+  for (int64_t t = t_lo; t < t_hi; ++t) {
+    const int buf = (int)((t - t_lo) & 1);
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();   // tile t landed for every thread; everyone is done with tile t-1
+    if (t + 1 < t_hi) stage(t + 1, buf ^ 1);   // prefetch the next tile into the other buffer
+    const float* jsm = js[buf];
+    const int64_t row0 = t * kGfTile;
+    const int nvalid = (int)min((int64_t)kGfTile, L - row0);
+#pragma unroll 1
+    for (int c8 = 0; c8 < kGfTile / 8; ++c8) {
+      float mn = CUDART_INF_F;
+#pragma unroll
+      for (int c4 = 2 * c8; c4 < 2 * c8 + 2; ++c4) {
+        uint64_t da = 0ull, db = 0ull;
+#pragma unroll
+        for (int t4 = 0; t4 < 4; ++t4) {
+          const float4 p = *reinterpret_cast<const float4*>(jsm + t4 * kGfTile + 4 * c4);
+          const uint64_t a = ptx::sub2(QQ[t4], ptx::pack2(p.x, p.y));
+          da = ptx::fma2(a, a, da);
+          const uint64_t b = ptx::sub2(QQ[t4], ptx::pack2(p.z, p.w));
+          db = ptx::fma2(b, b, db);
+        }
+        mn = fminf(mn, fminf(fminf(ptx::lo2(da), ptx::hi2(da)), fminf(ptx::lo2(db), ptx::hi2(db))));
+      }
+      if (!__any_sync(0xffffffffu, mn <= g2)) continue;
+      // exact canonical gate for the 8 rows of this group
+#pragma unroll 1
+      for (int c = 8 * c8; c < 8 * c8 + 8; ++c) {
+        float ds = 0.0f;
+#pragma unroll
+        for (int u = 0; u < JP; ++u) {
+          const float df = __fsub_rn(qj[u], jsm[u * kGfTile + c]);
+          ds = __fmaf_rn(df, df, ds);
+        }
+        if (active && c < nvalid && ds <= g2) {
+          const uint32_t slot = atomicAdd(&cnt[q], 1u);
+          if (slot < (uint32_t)cap) cand[(int64_t)q * cap + slot] = (int32_t)(row0 + c);
+        }
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ float bf16_dot_lane(const uint4* __restrict__ a, const uint4* __restrict__ b, int n16,
+                                               int lane) {
+  // lanes take 16-byte pieces lane, lane+32, ...; fp32 accumulation in a fixed order
+  float acc = 0.0f;
+  for (int i = lane; i < n16; i += 32) {
+    const uint4 x = __ldg(a + i), y = __ldg(b + i);
+    const uint32_t xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      acc = __fmaf_rn(__uint_as_float(xs[u] << 16), __uint_as_float(ys[u] << 16), acc);
+      acc = __fmaf_rn(__uint_as_float(xs[u] & 0xFFFF0000u), __uint_as_float(ys[u] & 0xFFFF0000u), acc);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  return acc;
+}
+
+template <int KT, int JP>
+__global__ void score_kernel(const uint16_t* __restrict__ emb, const float* __restrict__ inv_e,
+                             const float* __restrict__ pool_joints, int64_t L, const uint16_t* __restrict__ q,
+                             const float* __restrict__ inv_q, const float* __restrict__ q_joints, int32_t d,
+                             int32_t nq, int32_t k, float g2, int32_t cap, const uint32_t* __restrict__ cnt,
+                             const int32_t* __restrict__ cand, float* __restrict__ out_s, int64_t* __restrict__ out_i,
+                             uint8_t* __restrict__ out_hit, float threshold, int32_t rank, int32_t world,
+                             int64_t B) {
+  const int lane = threadIdx.x & 31;
+  const int qi = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (qi >= nq) return;
+  const int n16 = d / 8;
+  const uint4* qv = reinterpret_cast<const uint4*>(q + (int64_t)qi * d);
+  const float iq = inv_q[qi];
+  TopK<KT, int32_t> top;
+  top.init(true);
+  const uint32_t n = cnt[qi];
+  if (n <= (uint32_t)cap) {
+    for (uint32_t c = 0; c < n; ++c) {
+      const int32_t j = cand[(int64_t)qi * cap + c];
+      const float acc = bf16_dot_lane(qv, reinterpret_cast<const uint4*>(emb + (int64_t)j * d), n16, lane);
+      const float s = __fmul_rn(__fmul_rn(acc, iq), inv_e[j]);
+      if (lane == 0 && better(s, j, top.kth_s, top.kth_i)) top.insert(s, j, k);
+    }
+  } else {
+    // bucket overflow: exact exhaustive scan of this query (lane per row, increasing)
+    float r[JP];
+#pragma unroll
+    for (int t = 0; t < JP; ++t) r[t] = q_joints[(int64_t)qi * JP + t];
+    for (int64_t j = lane; j < L; j += 32) {
+      float ds = 0.0f;
+#pragma unroll
+      for (int t = 0; t < JP; ++t) {
+        const float df = __fsub_rn(r[t], pool_joints[joint_offset(j, t, JP)]);
+        ds = __fmaf_rn(df, df, ds);
+      }
+      if (!(ds <= g2)) continue;
+      const uint32_t* e = reinterpret_cast<const uint32_t*>(emb + j * d);
+      const uint32_t* qq = reinterpret_cast<const uint32_t*>(q + (int64_t)qi * d);
+      // same per-lane order as bf16_dot_lane would give is not required: any fp32 order
+      float acc = 0.0f;
+      for (int w = 0; w < d / 2; ++w) {
+        acc = __fmaf_rn(__uint_as_float(qq[w] << 16), __uint_as_float(e[w] << 16), acc);
+        acc = __fmaf_rn(__uint_as_float(qq[w] & 0xFFFF0000u), __uint_as_float(e[w] & 0xFFFF0000u), acc);
+      }
+      const float s = __fmul_rn(__fmul_rn(acc, iq), inv_e[j]);
+      if (s > top.kth_s) top.insert_monotone(s, (int32_t)j, k);
+    }
+  }
+  // k rounds of a butterfly arg-max over the lanes' lists (only lane 0's list is
+  // populated on the bucket path)
+  float s0 = -CUDART_INF_F;
+  int64_t i0 = -1;
+  for (int r = 0; r < k; ++r) {
+    float bs = top.s[0];
+    int32_t bi = top.i[0];
+    int bl = lane;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float os = __shfl_xor_sync(0xffffffffu, bs, o);
+      const int32_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+      if (better(os, oi, bs, bi) || (!better(bs, bi, os, oi) && ol < bl)) {
+        bs = os;
+        bi = oi;
+        bl = ol;
+      }
+    }
+    const int64_t gi = bi >= 0 ? shard_global((int64_t)bi, rank, world, B) : -1;
+    if (lane == 0) {
+      out_s[(int64_t)qi * k + r] = bi >= 0 ? bs : -CUDART_INF_F;
+      out_i[(int64_t)qi * k + r] = gi;
+    }
+    if (r == 0) {
+      s0 = bs;
+      i0 = gi;
+    }
+    if (lane == bl) top.pop_front();
+  }
+  if (out_hit != nullptr && lane == 0) out_hit[qi] = (i0 >= 0 && s0 >= threshold) ? 1 : 0;
+}
+
+template <int JP>
+cudaError_t launch_gf_jp(Pool& p, const MatchArgs& a, int32_t cap, float* out_s, int64_t* out_i, uint8_t* out_hit,
+                         cudaStream_t s) {
+  const int n_qg = (a.nq + kGfThreads - 1) / kGfThreads;
+  const int64_t n_pt = (p.local + kGfTile - 1) / kGfTile;
+  int S = (int)std::max<int64_t>(1, std::min<int64_t>(n_pt, (4 * (int64_t)p.num_sms + n_qg - 1) / n_qg));
+  cudaError_t e = cudaMemsetAsync(p.gf_cnt, 0, (size_t)a.nq * sizeof(uint32_t), s);
+  if (e != cudaSuccess) return e;
+  if (p.local > 0) {
+    gate_scan_kernel<JP><<<dim3(n_qg, S), kGfThreads, 0, s>>>(p.joints, p.local, p.q_joints, a.nq, S, a.g2, cap,
+                                                                p.gf_cnt, p.gf_cand);
+    ++p.launches;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  const int wpb = 4;
+  const unsigned g = (unsigned)((a.nq + wpb - 1) / wpb);
+  const auto& c = p.cfg;
+#define AMS_GF(KT_)                                                                                         \
+  score_kernel<KT_, JP><<<g, wpb * 32, 0, s>>>(static_cast<const uint16_t*>(p.emb), p.inv_norm, p.joints, p.local, \
+                                               static_cast<const uint16_t*>(p.q_stage), p.q_inv, p.q_joints, c.dim, \
+                                               a.nq, a.k, a.g2, cap, p.gf_cnt, p.gf_cand, out_s, out_i, out_hit,    \
+                                               a.threshold, c.rank, c.world, p.B)
+  switch (a.KT) {
+    case 8: AMS_GF(8); break;
+    case 16: AMS_GF(16); break;
+    case 32: AMS_GF(32); break;
+    default: AMS_GF(64); break;
+  }
+#undef AMS_GF
+  ++p.launches;
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_gate_first(Pool& p, const MatchArgs& a, float* out_s, int64_t* out_i, uint8_t* out_hit,
+                              cudaStream_t s) {
+  const int32_t cap = p.gf_cap;
+  switch (p.JP) {
+    case 4: return launch_gf_jp<4>(p, a, cap, out_s, out_i, out_hit, s);
+    case 8: return launch_gf_jp<8>(p, a, cap, out_s, out_i, out_hit, s);
+    default: return launch_gf_jp<16>(p, a, cap, out_s, out_i, out_hit, s);
+  }
+}
+
+}  // namespace ams

@@ -93,6 +93,11 @@ struct Pool {
 
   uint32_t* bound = nullptr;  // [q_pad] per-query admission lower bound (tcgen05 path)
 
+  // gate-first variant: per-query candidate buckets
+  int32_t gf_cap = 0;
+  uint32_t* gf_cnt = nullptr;  // [q_pad]
+  int32_t* gf_cand = nullptr;  // [q_pad, gf_cap] local rows
+
   CUtensorMap tmap_pool{};   // bf16 pool [cap_pad, d], box {64, 256}, SW128 (CTA tile)
   CUtensorMap tmap_pool2{};  // bf16 pool [cap_pad, d], box {64, 128}, SW128 (CTA-pair half tile)
   CUtensorMap tmap_q{};      // bf16 queries [q_pad, d], box {64, 128}, SW128
@@ -133,6 +138,9 @@ cudaError_t launch_merge_shards(Pool& p, const MatchArgs& a, int32_t G, int32_t 
 
 cudaError_t launch_merge_lists(const MatchArgs& a, int32_t G, int32_t kin, const float* in_s, const int64_t* in_i,
                                float* out_s, int64_t* out_i, uint8_t* out_hit, cudaStream_t s);
+// gate-first sparse variant (bf16 pools): writes [nq][k] (+hit if out_hit)
+cudaError_t launch_gate_first(Pool& p, const MatchArgs& a, float* out_s, int64_t* out_i, uint8_t* out_hit,
+                              cudaStream_t s);
 int pick_KT(int k);
 
 }  // namespace ams
