@@ -124,6 +124,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0, help="queries in the oracle sample (0 = auto)")
+    ap.add_argument("--gate-first", action="store_true",
+                    help="time ams_match_gate_first (SURVEY 8(f) f3 variant) instead of the dense ams_match")
+    ap.add_argument("--no-variant", action="store_true", help="skip the gate-first side measurement")
     return ap.parse_args()
 
 
@@ -273,8 +276,9 @@ def run_stream(args):
         for b in sizes:
             if timed:
                 evs[ev_i][0].record(stream)
-            ams.ams_match(pool.handle, q[off:off + b], qj[off:off + b], b, cfg.k, cfg.theta, cfg.gamma,
-                          out_i, out_s, out_h, stream)
+            (ams.ams_match_gate_first if args.gate_first else ams.ams_match)(
+                pool.handle, q[off:off + b], qj[off:off + b], b, cfg.k, cfg.theta, cfg.gamma, out_i, out_s, out_h,
+                stream)
             if timed:
                 evs[ev_i][1].record(stream)
                 ev_i += 1
@@ -319,6 +323,8 @@ def run_stream(args):
     m_now = pool.size
     shard_rows = -(-m_now // world)
     bytes_call = shard_rows * (2 * cfg.d + 4 * cfg.J + 4)
+    if args.gate_first:   # the gate-first scan reads the (padded) joints only
+        bytes_call = shard_rows * 4 * (4 if cfg.J <= 4 else 8 if cfg.J <= 8 else 16)
     value = per_step * T / (total / 1e3)
     if rank == 0:
         gbs = bytes_call / (np.median(lat) / 1e3) / 1e9
@@ -337,7 +343,8 @@ def run_stream(args):
                 "roofline": {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                              "frac": gbs / peaks["hbm_gbs"], "traffic": None,
                              "note": "whole ams_match call (prep + scan kernel + merge) at the median batch"},
-                "clocks": clocks, "gpu_launches": launches, "e2e": None, "cpu_baseline": None}
+                "clocks": clocks, "gpu_launches": launches, "e2e": None, "cpu_baseline": None,
+                "path": "ams_match_gate_first" if args.gate_first else "ams_match (dense tcgen05)"}
         print(json.dumps(line), flush=True)
     pool.close()
     if world > 1:
@@ -442,8 +449,10 @@ def main():
     out_h = torch.empty(cfg.Q, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
 
-    def step(qe=q, qjj=qj, nq=cfg.Q):
-        ams.ams_match(pool.handle, qe, qjj, nq, cfg.k, cfg.theta, gamma, out_i, out_s, out_h, stream)
+    match_fn = ams.ams_match_gate_first if args.gate_first else ams.ams_match
+
+    def step(qe=q, qjj=qj, nq=cfg.Q, fn=None):
+        (fn or match_fn)(pool.handle, qe, qjj, nq, cfg.k, cfg.theta, gamma, out_i, out_s, out_h, stream)
 
     # ------------------------------------------------------------------ main timing
     for _ in range(max(args.warmup, 3)):
@@ -494,6 +503,16 @@ def main():
                 if peaks.get("bf16_tflops_sustained") else None,
                 "frac_vs_datasheet_2250": achieved_tf / 2250.0}
 
+    if args.gate_first:   # the dominant kernels read only joints: report against HBM
+        jp = 4 if cfg.J <= 4 else 8 if cfg.J <= 8 else 16
+        jbytes = m_shard * 4 * jp
+        gbs = jbytes / (kern_avg / 1e3) / 1e9
+        roofline = {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                    "frac": gbs / peaks["hbm_gbs"], "traffic": None,
+                    "kernel": "gate_scan_kernel + score_kernel (gate-first variant)",
+                    "algorithmic_per_launch": {"bytes": jbytes}, "kernel_ms_avg": kern_avg,
+                    "note": "joint bytes per launch / kernel time; the scan is ALU-bound, so this is low by design"}
+
     # ------------------------------------------------------------------ 64-query scan
     scan = None
     if not args.no_scan and cfg.Q >= 64:
@@ -525,6 +544,28 @@ def main():
                              "traffic": load_traffic(args.workload, "match_tc_scan"),
                              "kernel_ms_avg": k_avg, "frac_vs_datasheet_8000": gbs_kernel / 8000.0,
                              "algorithmic_bytes_per_launch": bytes_step / world}}
+
+    # ------------------------------------------------------------------ gate-first variant (f3)
+    variant = None
+    if not args.no_variant and not args.gate_first and math.isfinite(gamma):
+        res = {}
+        for label, nq in (("full_batch", cfg.Q), ("scan_64", min(64, cfg.Q))):
+            qv, qjv = q[:nq].contiguous(), qj[:nq].contiguous()
+            for _ in range(3):
+                step(qv, qjv, nq, ams.ams_match_gate_first)
+            torch.cuda.synchronize()
+            reps = max(5, args.steps)
+            barrier()
+            ev0.record(stream)
+            for _ in range(reps):
+                step(qv, qjv, nq, ams.ams_match_gate_first)
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            barrier()
+            v_ms = max_over_ranks(ev0.elapsed_time(ev1)) / reps
+            res[label] = {"queries": nq, "ms_per_call": v_ms, "value": nq / (v_ms / 1e3), "unit": "queries/s",
+                          "joint_bytes_gbps_per_gpu": (cfg.M / world) * 4 * (8 if cfg.J <= 8 else 16) / (v_ms / 1e3) / 1e9}
+        variant = {"name": "ams_match_gate_first (SURVEY 8(f) f3; exact, gate evaluated first)", **res}
 
     # ------------------------------------------------------------------ e2e (host buffers)
     e2e = None
@@ -577,8 +618,10 @@ def main():
                 "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
                 "config": config_block(cfg, args, world, gamma),
                 "pool_scan_gbps_per_gpu": (bytes_step / world) / (t_ms / args.steps / 1e3) / 1e9,
-                "roofline": roofline, "scan": scan, "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks,
-                "gpu_launches": launches, "plan": plan, "hit_rate": hit_rate,
+                "roofline": roofline, "scan": scan, "gate_first_variant": variant, "e2e": e2e, "cpu_baseline": cpu,
+                "clocks": clocks,
+                "gpu_launches": launches, "plan": plan, "hit_rate": hit_rate, "path": "ams_match_gate_first"
+                if args.gate_first else "ams_match (dense tcgen05)",
                 "near_dup_top1_equals_source": label_top1}
         print(json.dumps(line), flush=True)
     pool.close()
