@@ -50,7 +50,7 @@ constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kABytes = kBlockM * kBlockK * 2;   // 16 KB: 128 query rows x 128 B
 constexpr int kColsPerHalf = kBlockN / kEpiHalves;    // 128
 constexpr int kChunk = 32;
-constexpr int kRefreshTiles = 8;                      // bound publish/refresh period
+constexpr int kRefreshTiles = 1;                      // bound publish/refresh period (tiles)
 
 template <int CG>
 struct Geo {
