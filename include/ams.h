@@ -174,6 +174,49 @@ ams_status_t ams_hash_actions(ams_hasher_t hasher, const uint8_t* data, const in
 /* Synchronises the device and frees the hasher.  NULL is a no-op. */
 ams_status_t ams_hasher_destroy(ams_hasher_t hasher);
 
+/* ---- virtual-action store ----
+ * "uniquely numbered actions with independent reference counts ... stored in a
+ * contiguous area ... Any action whose reference count drops to zero is removed."
+ * Ids are the two-phase hashes H_final (ams_hash_actions).  Device hash table + an
+ * append-only device byte arena; every operation is batched and stream-ordered. */
+typedef struct ams_vstore_s* ams_vstore_t;
+
+/* Per-action status written by ams_vstore_intern. */
+#define AMS_VSTORE_NEW 0        /* entry created, refcount 1, bytes copied to the arena */
+#define AMS_VSTORE_DEDUP 1      /* identical bytes already stored: refcount incremented */
+#define AMS_VSTORE_COLLISION 2  /* id present with DIFFERENT bytes: nothing changed (SPEC CollisionError) */
+#define AMS_VSTORE_FULL 3       /* table or arena full: nothing stored */
+
+/* max_actions live entries (table capacity 2x, power of two), arena_bytes of action
+ * bytes, batches of up to max_batch actions / max_batch_bytes bytes. */
+ams_status_t ams_vstore_create(int32_t device, int64_t max_actions, int64_t arena_bytes, int32_t max_batch,
+                               int64_t max_batch_bytes, ams_vstore_t* out);
+
+/* Interns n actions given as CSR bytes (data host or device; offsets HOST [n+1]).
+ * ids_in: DEVICE [n] precomputed ids, or NULL to hash the bytes here (two-phase hash).
+ * out_ids (DEVICE u64 [n]) receives the ids, out_status (DEVICE u8 [n]) the status. */
+ams_status_t ams_vstore_intern(ams_vstore_t store, const uint8_t* data, const int64_t* offsets, int32_t n,
+                               const uint64_t* ids_in, uint64_t* out_ids, uint8_t* out_status, void* stream);
+
+/* Decrements the reference count of n ids (DEVICE [n]); out_remaining (DEVICE i64 [n])
+ * gets the remaining count, or -1 for an unknown id (SPEC UnknownId).  At zero the
+ * entry is removed. */
+ams_status_t ams_vstore_release(ams_vstore_t store, const uint64_t* ids, int32_t n, int64_t* out_remaining,
+                                void* stream);
+
+/* Looks up n ids (DEVICE): arena offset and length (DEVICE i64 [n]; -1 if unknown) and,
+ * if out_refcount is not NULL, the reference count (0 if unknown). */
+ams_status_t ams_vstore_resolve(ams_vstore_t store, const uint64_t* ids, int32_t n, int64_t* out_offset,
+                                int64_t* out_len, int64_t* out_refcount, void* stream);
+
+/* Device pointer of the byte arena (read-only for callers). */
+ams_status_t ams_vstore_arena(ams_vstore_t store, const uint8_t** arena);
+
+/* Synchronises; live entries, their total bytes, and arena bytes used (append-only). */
+ams_status_t ams_vstore_stats(ams_vstore_t store, int64_t* n_entries, int64_t* total_bytes, int64_t* arena_used);
+
+ams_status_t ams_vstore_destroy(ams_vstore_t store);
+
 /* Number of rows appended so far (global).  Host-side counter, no sync. */
 ams_status_t ams_pool_size(ams_pool_t pool, int64_t* n);
 

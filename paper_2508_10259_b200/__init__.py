@@ -31,7 +31,9 @@ EXPORTS = ("ams_get_nccl_unique_id", "ams_pool_create", "ams_pool_append", "ams_
            "ams_pool_size",
            "ams_pool_destroy", "ams_status_string", "ams_pool_set_profiling", "ams_pool_read_profile",
            "ams_pool_launch_count", "ams_pool_last_plan", "ams_shard_locate", "ams_shard_capacity",
-           "ams_abi_version", "ams_hasher_create", "ams_hash_actions", "ams_hasher_destroy")
+           "ams_abi_version", "ams_hasher_create", "ams_hash_actions", "ams_hasher_destroy",
+           "ams_vstore_create", "ams_vstore_intern", "ams_vstore_release", "ams_vstore_resolve",
+           "ams_vstore_arena", "ams_vstore_stats", "ams_vstore_destroy")
 
 
 class AmsError(RuntimeError):
@@ -72,6 +74,13 @@ def _load():
         "ams_hasher_create": [I32, I64, I64, I64, ctypes.POINTER(V)],
         "ams_hash_actions": [V, V, V, I32, V, V],
         "ams_hasher_destroy": [V],
+        "ams_vstore_create": [I32, I64, I64, I32, I64, ctypes.POINTER(V)],
+        "ams_vstore_intern": [V, V, V, I32, V, V, V, V],
+        "ams_vstore_release": [V, V, I32, V, V],
+        "ams_vstore_resolve": [V, V, I32, V, V, V, V],
+        "ams_vstore_arena": [V, ctypes.POINTER(V)],
+        "ams_vstore_stats": [V, ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64)],
+        "ams_vstore_destroy": [V],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -239,6 +248,45 @@ def ams_hash_actions(hasher: int, data, offsets, n_inputs: int, out_hash, stream
 
 def ams_hasher_destroy(hasher: int) -> None:
     _check(lib.ams_hasher_destroy(hasher), "ams_hasher_destroy")
+
+
+def ams_vstore_create(device: int, max_actions: int, arena_bytes: int, max_batch: int, max_batch_bytes: int) -> int:
+    out = ctypes.c_void_p()
+    _check(lib.ams_vstore_create(device, max_actions, arena_bytes, max_batch, max_batch_bytes, ctypes.byref(out)),
+           "ams_vstore_create")
+    return out.value
+
+
+def ams_vstore_intern(store: int, data, offsets, n: int, ids_in, out_ids, out_status, stream=None) -> None:
+    import numpy as np
+    off = np.ascontiguousarray(offsets, dtype=np.int64)
+    _check(lib.ams_vstore_intern(store, _ptr(data), off.ctypes.data, n, _ptr(ids_in), _ptr(out_ids),
+                                 _ptr(out_status), _stream(stream)), "ams_vstore_intern")
+
+
+def ams_vstore_release(store: int, ids, n: int, out_remaining, stream=None) -> None:
+    _check(lib.ams_vstore_release(store, _ptr(ids), n, _ptr(out_remaining), _stream(stream)), "ams_vstore_release")
+
+
+def ams_vstore_resolve(store: int, ids, n: int, out_offset, out_len, out_refcount=None, stream=None) -> None:
+    _check(lib.ams_vstore_resolve(store, _ptr(ids), n, _ptr(out_offset), _ptr(out_len), _ptr(out_refcount),
+                                  _stream(stream)), "ams_vstore_resolve")
+
+
+def ams_vstore_arena(store: int) -> int:
+    p = ctypes.c_void_p()
+    _check(lib.ams_vstore_arena(store, ctypes.byref(p)), "ams_vstore_arena")
+    return p.value
+
+
+def ams_vstore_stats(store: int):
+    a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    _check(lib.ams_vstore_stats(store, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)), "ams_vstore_stats")
+    return {"entries": a.value, "total_bytes": b.value, "arena_used": c.value}
+
+
+def ams_vstore_destroy(store: int) -> None:
+    _check(lib.ams_vstore_destroy(store), "ams_vstore_destroy")
 
 
 # ----------------------------------------------------------------------------- convenience
