@@ -217,6 +217,61 @@ ams_status_t ams_vstore_stats(ams_vstore_t store, int64_t* n_entries, int64_t* t
 
 ams_status_t ams_vstore_destroy(ams_vstore_t store);
 
+/* ---- layered storage of action-context blobs ----
+ * PAPER.md:497-522 (3.2.2): "we store [frequently accessed data] in GPU memory ... for
+ * data that is infrequently accessed, we apply an on-demand recomputation strategy or move
+ * it to CPU"; PAPER.md:586-594 (3.2.3 Auto Eviction): LRU combined with priority, "first
+ * evict the KV Cache of vision models" (recomputable).  Policy as SPEC.md:200-224
+ * (evict_until): victims by ascending P = 1000*class_rank + recency_rank (VisionKV 0 <
+ * LlmKV 1 < DiffusionLatent = OutputEmbedding 2; recency rank 0 = least recently used),
+ * ties by LRU then id; VisionKV dropped, others demoted to pinned host memory.  Fast tier
+ * = HBM (stream-ordered allocations), slow tier = pinned host; copies on `stream`. */
+typedef struct ams_tier_s* ams_tier_t;
+#define AMS_BLOB_VISION_KV 0
+#define AMS_BLOB_LLM_KV 1
+#define AMS_BLOB_DIFFUSION_LATENT 2
+#define AMS_BLOB_OUTPUT_EMBEDDING 3
+#define AMS_TIER_FAST 0
+#define AMS_TIER_SLOW 1
+#define AMS_TIER_DROPPED 2
+#define AMS_EVICT_DEMOTE 1
+#define AMS_EVICT_DROP 2
+#define AMS_EVICT_PROMOTE 3
+
+/* fast_budget / slow_budget in bytes (slow_budget 0 = unbounded). */
+ams_status_t ams_tier_create(int32_t device, int64_t fast_budget, int64_t slow_budget, ams_tier_t* out);
+
+/* Admits a blob (payload host or device, copied on `stream`); placed in HBM when it fits the
+ * fast budget (evicting first), otherwise in host memory.  The eviction actions taken are
+ * written to act_ids/act_kinds (up to max_acts; *n_acts = total).  Re-admitting a DROPPED
+ * blob (after the caller recomputed it) is allowed.  Errors: AMS_ERR_INVALID_ARGUMENT
+ * (duplicate live id, bad kind/size), AMS_ERR_CAPACITY (fits no tier; nothing changed),
+ * AMS_ERR_OUT_OF_MEMORY, AMS_ERR_CUDA. */
+ams_status_t ams_tier_admit(ams_tier_t tier, int64_t blob_id, int32_t kind, const void* payload, int64_t size,
+                            int32_t* placed_tier, int64_t* act_ids, int32_t* act_kinds, int32_t max_acts,
+                            int32_t* n_acts, void* stream);
+
+/* access_count += 1, last_access = clock++ (SPEC.md:193 touch). */
+ams_status_t ams_tier_touch(ams_tier_t tier, int64_t blob_id);
+
+/* Frees >= needed bytes of HBM by the policy above (AMS_ERR_CAPACITY if impossible). */
+ams_status_t ams_tier_evict_until(ams_tier_t tier, int64_t needed, int64_t* act_ids, int32_t* act_kinds,
+                                  int32_t max_acts, int32_t* n_acts, void* stream);
+
+/* Access: counts as a touch; a host-tier blob is promoted to HBM (evicting as needed);
+ * *prev_tier = the tier before the call (AMS_TIER_DROPPED: the caller must recompute and
+ * re-admit); *device_ptr = the HBM payload (NULL if not in HBM afterwards). */
+ams_status_t ams_tier_fetch(ams_tier_t tier, int64_t blob_id, int32_t* prev_tier, const void** device_ptr,
+                            int64_t* act_ids, int32_t* act_kinds, int32_t max_acts, int32_t* n_acts,
+                            void* stream);
+
+ams_status_t ams_tier_info(ams_tier_t tier, int64_t blob_id, int32_t* tier_out, int64_t* access_count,
+                           int64_t* last_access, int64_t* size);
+ams_status_t ams_tier_usage(ams_tier_t tier, int64_t* fast_used, int64_t* slow_used);
+/* Copies the current payload (HBM or host tier) to dst (host or device) on `stream`. */
+ams_status_t ams_tier_read(ams_tier_t tier, int64_t blob_id, void* dst, void* stream);
+ams_status_t ams_tier_destroy(ams_tier_t tier);
+
 /* Number of rows appended so far (global).  Host-side counter, no sync. */
 ams_status_t ams_pool_size(ams_pool_t pool, int64_t* n);
 

@@ -33,7 +33,9 @@ EXPORTS = ("ams_get_nccl_unique_id", "ams_pool_create", "ams_pool_append", "ams_
            "ams_pool_launch_count", "ams_pool_last_plan", "ams_shard_locate", "ams_shard_capacity",
            "ams_abi_version", "ams_hasher_create", "ams_hash_actions", "ams_hasher_destroy",
            "ams_vstore_create", "ams_vstore_intern", "ams_vstore_release", "ams_vstore_resolve",
-           "ams_vstore_arena", "ams_vstore_stats", "ams_vstore_destroy")
+           "ams_vstore_arena", "ams_vstore_stats", "ams_vstore_destroy", "ams_tier_create", "ams_tier_admit",
+           "ams_tier_touch", "ams_tier_evict_until", "ams_tier_fetch", "ams_tier_info", "ams_tier_usage",
+           "ams_tier_read", "ams_tier_destroy")
 
 
 class AmsError(RuntimeError):
@@ -81,6 +83,15 @@ def _load():
         "ams_vstore_arena": [V, ctypes.POINTER(V)],
         "ams_vstore_stats": [V, ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64)],
         "ams_vstore_destroy": [V],
+        "ams_tier_create": [I32, I64, I64, ctypes.POINTER(V)],
+        "ams_tier_admit": [V, I64, I32, V, I64, ctypes.POINTER(I32), V, V, I32, ctypes.POINTER(I32), V],
+        "ams_tier_touch": [V, I64],
+        "ams_tier_evict_until": [V, I64, V, V, I32, ctypes.POINTER(I32), V],
+        "ams_tier_fetch": [V, I64, ctypes.POINTER(I32), ctypes.POINTER(V), V, V, I32, ctypes.POINTER(I32), V],
+        "ams_tier_info": [V, I64, ctypes.POINTER(I32), ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64)],
+        "ams_tier_usage": [V, ctypes.POINTER(I64), ctypes.POINTER(I64)],
+        "ams_tier_read": [V, I64, V, V],
+        "ams_tier_destroy": [V],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -287,6 +298,73 @@ def ams_vstore_stats(store: int):
 
 def ams_vstore_destroy(store: int) -> None:
     _check(lib.ams_vstore_destroy(store), "ams_vstore_destroy")
+
+
+def _acts(max_acts=64):
+    import numpy as np
+    return np.zeros(max_acts, np.int64), np.zeros(max_acts, np.int32), ctypes.c_int32(0)
+
+
+def _acts_list(ids, kinds, n):
+    m = min(n.value, len(ids))
+    return [(int(ids[i]), int(kinds[i])) for i in range(m)]
+
+
+def ams_tier_create(device: int, fast_budget: int, slow_budget: int = 0) -> int:
+    out = ctypes.c_void_p()
+    _check(lib.ams_tier_create(device, fast_budget, slow_budget, ctypes.byref(out)), "ams_tier_create")
+    return out.value
+
+
+def ams_tier_admit(tier: int, blob_id: int, kind: int, payload, size: int, stream=None):
+    """Returns (placed_tier, [(blob_id, action), ...])."""
+    ids, kinds, n = _acts()
+    placed = ctypes.c_int32(-1)
+    _check(lib.ams_tier_admit(tier, blob_id, kind, _ptr(payload), size, ctypes.byref(placed), ids.ctypes.data,
+                              kinds.ctypes.data, len(ids), ctypes.byref(n), _stream(stream)), "ams_tier_admit")
+    return placed.value, _acts_list(ids, kinds, n)
+
+
+def ams_tier_touch(tier: int, blob_id: int) -> None:
+    _check(lib.ams_tier_touch(tier, blob_id), "ams_tier_touch")
+
+
+def ams_tier_evict_until(tier: int, needed: int, stream=None):
+    ids, kinds, n = _acts()
+    _check(lib.ams_tier_evict_until(tier, needed, ids.ctypes.data, kinds.ctypes.data, len(ids), ctypes.byref(n),
+                                    _stream(stream)), "ams_tier_evict_until")
+    return _acts_list(ids, kinds, n)
+
+
+def ams_tier_fetch(tier: int, blob_id: int, stream=None):
+    """Returns (prev_tier, device_ptr or None, [(blob_id, action), ...])."""
+    ids, kinds, n = _acts()
+    prev = ctypes.c_int32(-1)
+    dp = ctypes.c_void_p()
+    _check(lib.ams_tier_fetch(tier, blob_id, ctypes.byref(prev), ctypes.byref(dp), ids.ctypes.data,
+                              kinds.ctypes.data, len(ids), ctypes.byref(n), _stream(stream)), "ams_tier_fetch")
+    return prev.value, dp.value, _acts_list(ids, kinds, n)
+
+
+def ams_tier_info(tier: int, blob_id: int):
+    t, c, l, s = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    _check(lib.ams_tier_info(tier, blob_id, ctypes.byref(t), ctypes.byref(c), ctypes.byref(l), ctypes.byref(s)),
+           "ams_tier_info")
+    return {"tier": t.value, "count": c.value, "last": l.value, "size": s.value}
+
+
+def ams_tier_usage(tier: int):
+    f, s = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib.ams_tier_usage(tier, ctypes.byref(f), ctypes.byref(s)), "ams_tier_usage")
+    return f.value, s.value
+
+
+def ams_tier_read(tier: int, blob_id: int, dst, stream=None) -> None:
+    _check(lib.ams_tier_read(tier, blob_id, _ptr(dst), _stream(stream)), "ams_tier_read")
+
+
+def ams_tier_destroy(tier: int) -> None:
+    _check(lib.ams_tier_destroy(tier), "ams_tier_destroy")
 
 
 # ----------------------------------------------------------------------------- convenience
