@@ -37,15 +37,21 @@ __global__ void __launch_bounds__(kGfThreads)
                      int32_t nq, int32_t S, float g2, int32_t cap, uint32_t* __restrict__ cnt,
                      int32_t* __restrict__ cand) {
   __shared__ __align__(16) float js[2][JP * kGfTile];
+  __shared__ __align__(16) float pn[kGfTile];       // per row: sum of squares of the first 4 joints
+  __shared__ unsigned int pmax_bits;
   const int qg = blockIdx.x, sp = blockIdx.y;
   const int q = qg * kGfThreads + threadIdx.x;
   const bool active = q < nq;
   float qj[JP];
 #pragma unroll
-  for (int t = 0; t < JP; ++t) qj[t] = active ? q_joints[(int64_t)q * JP + t] : 1e30f;   // inactive: never eligible
+  for (int t = 0; t < JP; ++t) qj[t] = active ? q_joints[(int64_t)q * JP + t] : 0.0f;
   uint64_t QQ[4];
 #pragma unroll
   for (int t = 0; t < 4; ++t) QQ[t] = ptx::pack2(qj[t], qj[t]);
+  float rq = 0.0f;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) rq = fmaf(qj[t], qj[t], rq);
+  const uint64_t M2 = ptx::pack2(-2.0f, -2.0f);
   const int64_t n_pt = (L + kGfTile - 1) / kGfTile;
   const int64_t t_lo = n_pt * sp / S, t_hi = n_pt * (sp + 1) / S;
   auto stage = [&](int64_t t, int buf) {   // cp.async (LDGSTS): does not block the thread
@@ -60,9 +66,25 @@ __global__ void __launch_bounds__(kGfThreads)
   for (int64_t t = t_lo; t < t_hi; ++t) {
     const int buf = (int)((t - t_lo) & 1);
     asm volatile("cp.async.wait_all;" ::: "memory");
+    if (threadIdx.x == 0) pmax_bits = 0u;
     __syncthreads();   // tile t landed for every thread; everyone is done with tile t-1
     if (t + 1 < t_hi) stage(t + 1, buf ^ 1);   // prefetch the next tile into the other buffer
     const float* jsm = js[buf];
+    {  // per-row partial norms (one row per thread; any fp32 order -- covered by eps)
+      float v = 0.0f;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v = fmaf(jsm[u * kGfTile + threadIdx.x], jsm[u * kGfTile + threadIdx.x], v);
+      pn[threadIdx.x] = v;
+      const unsigned int wmax = __reduce_max_sync(0xffffffffu, __float_as_uint(v));   // v >= 0: int order = float order
+      if ((threadIdx.x & 31) == 0) atomicMax(&pmax_bits, wmax);
+    }
+    __syncthreads();
+    // Superset filter in expanded form over the first 4 joints: v = P_j - 2 r.p_j <= tq,
+    // tq = g2 - R + eps.  |(v' + R') - partial canonical sum| <= ~24 u (g2 + R + Pmax),
+    // u = 2^-24; eps = 2^-18 (g2 + R + Pmax) covers it with margin.  Rows that pass get the
+    // exact canonical gate below, so the result is exact.
+    const float tq = active ? (g2 - rq) + 3.814697265625e-06f * (g2 + rq + __uint_as_float(pmax_bits))
+                            : -CUDART_INF_F;
     const int64_t row0 = t * kGfTile;
     const int nvalid = (int)min((int64_t)kGfTile, L - row0);
 #pragma unroll 1
@@ -70,18 +92,21 @@ __global__ void __launch_bounds__(kGfThreads)
       float mn = CUDART_INF_F;
 #pragma unroll
       for (int c4 = 2 * c8; c4 < 2 * c8 + 2; ++c4) {
-        uint64_t da = 0ull, db = 0ull;
+        const float4 p0 = *reinterpret_cast<const float4*>(jsm + 4 * c4);
+        const float4 pv = *reinterpret_cast<const float4*>(pn + 4 * c4);
+        uint64_t a = ptx::mul2(QQ[0], ptx::pack2(p0.x, p0.y));
+        uint64_t b = ptx::mul2(QQ[0], ptx::pack2(p0.z, p0.w));
 #pragma unroll
-        for (int t4 = 0; t4 < 4; ++t4) {
+        for (int t4 = 1; t4 < 4; ++t4) {
           const float4 p = *reinterpret_cast<const float4*>(jsm + t4 * kGfTile + 4 * c4);
-          const uint64_t a = ptx::sub2(QQ[t4], ptx::pack2(p.x, p.y));
-          da = ptx::fma2(a, a, da);
-          const uint64_t b = ptx::sub2(QQ[t4], ptx::pack2(p.z, p.w));
-          db = ptx::fma2(b, b, db);
+          a = ptx::fma2(QQ[t4], ptx::pack2(p.x, p.y), a);
+          b = ptx::fma2(QQ[t4], ptx::pack2(p.z, p.w), b);
         }
-        mn = fminf(mn, fminf(fminf(ptx::lo2(da), ptx::hi2(da)), fminf(ptx::lo2(db), ptx::hi2(db))));
+        a = ptx::fma2(a, M2, ptx::pack2(pv.x, pv.y));
+        b = ptx::fma2(b, M2, ptx::pack2(pv.z, pv.w));
+        mn = fminf(mn, fminf(fminf(ptx::lo2(a), ptx::hi2(a)), fminf(ptx::lo2(b), ptx::hi2(b))));
       }
-      if (!__any_sync(0xffffffffu, mn <= g2)) continue;
+      if (!__any_sync(0xffffffffu, mn <= tq)) continue;
       // exact canonical gate for the 8 rows of this group
 #pragma unroll 1
       for (int c = 8 * c8; c < 8 * c8 + 8; ++c) {
@@ -205,7 +230,10 @@ cudaError_t launch_gf_jp(Pool& p, const MatchArgs& a, int32_t cap, float* out_s,
                          cudaStream_t s) {
   const int n_qg = (a.nq + kGfThreads - 1) / kGfThreads;
   const int64_t n_pt = (p.local + kGfTile - 1) / kGfTile;
-  int S = (int)std::max<int64_t>(1, std::min<int64_t>(n_pt, (4 * (int64_t)p.num_sms + n_qg - 1) / n_qg));
+  // ~2 full waves of resident blocks (6 blocks/SM: 34 KB smem, 256 threads)
+  // but keep >= 8 tiles per block so per-block setup stays amortised for small batches
+  int S = (int)std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(1, n_pt / 8),
+                                                      (12 * (int64_t)p.num_sms + n_qg - 1) / n_qg));
   cudaError_t e = cudaMemsetAsync(p.gf_cnt, 0, (size_t)a.nq * sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
   if (p.local > 0) {
