@@ -144,6 +144,36 @@ ams_status_t ams_merge_topk(const float* in_score, const int64_t* in_index, int3
                             int32_t kin, int32_t k, float threshold, int64_t* out_index,
                             float* out_score, uint8_t* out_hit, void* stream);
 
+/* ---- fused NVLink shard exchange (opt-in) ----
+ * Replaces, for this pool, the NCCL all-gather + merge of ams_match / ams_match_gate_first
+ * at world > 1 (north_star "row-sharded ... with an NCCL all-gather plus a final k-way
+ * merge"; PAPER.md:486-489 define the lookup itself) by direct peer stores: each rank's
+ * intra-GPU merge kernel writes its [nq, k] list into a receive slot of EVERY rank's
+ * buffer over NVLink (CUDA IPC mappings), then raises an epoch flag with a system-scope
+ * release; the final merge kernel acquires all G flags and merges.  Outputs are identical
+ * to the NCCL path.  Collective: every rank calls it once after ams_pool_create (the
+ * three IPC handles per rank travel over the pool's NCCL communicator).  Requires all
+ * ranks on one node with peer access; the pool's matches must be issued by every rank in
+ * the same order (as with the NCCL path).  Errors: AMS_ERR_INVALID_ARGUMENT (null pool),
+ * AMS_ERR_UNSUPPORTED (world < 2, world > 8, capacity >= 2^31, IPC unavailable),
+ * AMS_ERR_OUT_OF_MEMORY, AMS_ERR_NCCL, AMS_ERR_CUDA.  Idempotent. */
+ams_status_t ams_pool_enable_peer_exchange(ams_pool_t pool);
+
+/* Single-device self-test of the exchange kernels: G (1..8) virtual ranks, each with its
+ * own receive buffer and flag array on the current device, run `rounds` exchanges
+ * (epochs 1..rounds, alternating buffer parity).  in_score/in_index: DEVICE
+ * [rounds][G][nq][k] ranked lists (score desc, index asc; -inf / -1 padding; ids < 2^31);
+ * out_score/out_index: DEVICE [rounds][G][nq][k]; out_hit [rounds][G][nq] -- virtual rank
+ * g's merged result of round r, which must equal ams_merge_topk of that round's G lists
+ * for every g.  All producer launches of a round are enqueued before its consumer
+ * launches on `stream`, so no kernel waits on a concurrently running kernel.  Allocates
+ * and frees its own buffers; synchronises `stream`.  Errors: AMS_ERR_INVALID_ARGUMENT
+ * (G, nq, k (1..64) or rounds out of range, null pointers), AMS_ERR_OUT_OF_MEMORY,
+ * AMS_ERR_CUDA. */
+ams_status_t ams_exchange_selftest(int32_t G, int32_t nq, int32_t k, int32_t rounds, float threshold,
+                                   const float* in_score, const int64_t* in_index, float* out_score,
+                                   int64_t* out_index, uint8_t* out_hit, void* stream);
+
 /* ---- two-phase action hash (Algorithm 1) ----
  * Phase 1 hashes every s-byte segment of every input independently, phase 2 folds an
  * input's segment hashes ("modular calculation").

@@ -27,7 +27,7 @@ STATUS = {0: "AMS_OK", 1: "AMS_ERR_INVALID_ARGUMENT", 2: "AMS_ERR_CAPACITY", 3: 
 
 # Every symbol include/ams.h declares (tests check the library exports all of them).
 EXPORTS = ("ams_get_nccl_unique_id", "ams_pool_create", "ams_pool_append", "ams_match", "ams_match_gate_first",
-           "ams_merge_topk",
+           "ams_merge_topk", "ams_pool_enable_peer_exchange", "ams_exchange_selftest",
            "ams_pool_size",
            "ams_pool_destroy", "ams_status_string", "ams_pool_set_profiling", "ams_pool_read_profile",
            "ams_pool_launch_count", "ams_pool_last_plan", "ams_shard_locate", "ams_shard_capacity",
@@ -64,6 +64,8 @@ def _load():
         "ams_match": [V, V, V, I32, I32, ctypes.c_float, ctypes.c_float, V, V, V, V],
         "ams_match_gate_first": [V, V, V, I32, I32, ctypes.c_float, ctypes.c_float, V, V, V, V],
         "ams_merge_topk": [V, V, I32, I32, I32, I32, ctypes.c_float, V, V, V, V],
+        "ams_pool_enable_peer_exchange": [V],
+        "ams_exchange_selftest": [I32, I32, I32, I32, ctypes.c_float, V, V, V, V, V, V],
         "ams_pool_size": [V, ctypes.POINTER(I64)],
         "ams_pool_destroy": [V],
         "ams_pool_set_profiling": [V, I32],
@@ -195,6 +197,16 @@ def ams_merge_topk(in_score, in_index, G: int, nq: int, kin: int, k: int, thresh
                    out_score, out_hit, stream=None) -> None:
     _check(lib.ams_merge_topk(_ptr(in_score), _ptr(in_index), G, nq, kin, k, threshold, _ptr(out_index),
                               _ptr(out_score), _ptr(out_hit), _stream(stream)), "ams_merge_topk")
+
+
+def ams_pool_enable_peer_exchange(pool: int) -> None:
+    _check(lib.ams_pool_enable_peer_exchange(pool), "ams_pool_enable_peer_exchange")
+
+
+def ams_exchange_selftest(G: int, nq: int, k: int, rounds: int, threshold: float, in_score, in_index, out_score,
+                          out_index, out_hit, stream=None) -> None:
+    _check(lib.ams_exchange_selftest(G, nq, k, rounds, threshold, _ptr(in_score), _ptr(in_index), _ptr(out_score),
+                                     _ptr(out_index), _ptr(out_hit), _stream(stream)), "ams_exchange_selftest")
 
 
 def ams_pool_size(pool: int) -> int:

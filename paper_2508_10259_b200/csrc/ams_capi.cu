@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstring>
 #include <new>
+#include <vector>
 
 #include "ams_internal.cuh"
 
@@ -118,7 +119,26 @@ void plan_simt(const Pool& p, int nq, int KT, int& S) {
   S = (int)std::max<int64_t>(1, std::min(want, s_cap));
 }
 
+void free_peers(Pool& p) {
+  if (p.peer_mode)
+    for (int g = 0; g < p.peers.G; ++g)
+      if (g != p.peers.rank) {
+        if (p.peers.s[g]) cudaIpcCloseMemHandle(p.peers.s[g]);
+        if (p.peers.i[g]) cudaIpcCloseMemHandle(p.peers.i[g]);
+        if (p.peers.flag[g]) cudaIpcCloseMemHandle(p.peers.flag[g]);
+      }
+  void* own[] = {p.x_s, p.x_i, p.x_flag, p.x_done};
+  for (void* q : own)
+    if (q) cudaFree(q);
+  p.peer_mode = false;
+  p.x_s = nullptr;
+  p.x_i = nullptr;
+  p.x_flag = nullptr;
+  p.x_done = nullptr;
+}
+
 void free_all(Pool& p) {
+  free_peers(p);
   void* ptrs[] = {p.emb, p.inv_norm, p.joints, p.q_stage, p.q_inv, p.q_joints, p.q_joints_raw, p.bound,
                   p.gf_cnt, p.gf_cand,
                   p.part_s, p.part_i, p.shard_s, p.shard_i, p.gath_s, p.gath_i, p.stage_emb,
@@ -434,6 +454,24 @@ static ams_status_t match_impl(ams_pool_t pool, const void* q_emb, const float* 
       p.ev_free.push_back(e1);
     }
   }
+  if (multi && p.peer_mode) {
+    // fused NVLink exchange: merge + direct peer stores + flag completion, no NCCL launch
+    ++p.epoch;
+    const float* ps = p.part_s;
+    const int32_t* pi = p.part_i;
+    int32_t Pp = P, world_ids = p.cfg.world;
+    int64_t Bids = p.B;
+    if (gate_first && p.cfg.dtype == AMS_DTYPE_BF16) {   // shard lists already hold global ids
+      AMS_CUDA_TRY(ams::launch_to_partials(shard_s, shard_i, nq, k, a.KT, p.part_s, p.part_i, s));
+      Pp = 1;
+      world_ids = 0;   // no shard map
+      Bids = 0;
+    }
+    AMS_CUDA_TRY(ams::launch_exchange_push(a.KT, ps, pi, nq, Pp, k, p.peers, p.epoch, p.x_done, world_ids, Bids, s));
+    AMS_CUDA_TRY(ams::launch_exchange_wait(a.KT, p.peers, nq, k, p.epoch, out_score, out_index, out_hit, threshold, s));
+    p.launches += 2;
+    return AMS_OK;
+  }
   if (!(gate_first && p.cfg.dtype == AMS_DTYPE_BF16))
     AMS_CUDA_TRY(ams::launch_merge_partials(p, a, P, shard_s, shard_i, shard_hit, s));
 
@@ -481,6 +519,85 @@ ams_status_t ams_merge_topk(const float* in_score, const int64_t* in_index, int3
   a.threshold = threshold;
   AMS_CUDA_TRY(ams::launch_merge_lists(a, G, kin, in_score, in_index, out_score, out_index, out_hit,
                                        static_cast<cudaStream_t>(stream)));
+  return AMS_OK;
+}
+
+ams_status_t ams_pool_enable_peer_exchange(ams_pool_t pool) {
+  if (pool == nullptr) return AMS_ERR_INVALID_ARGUMENT;
+  Pool& p = pool->p;
+  if (p.broken) return AMS_ERR_CUDA;
+  const int G = p.cfg.world, r = p.cfg.rank;
+  if (G < 2 || G > ams::kMaxPeers || p.nccl_comm == nullptr) return AMS_ERR_UNSUPPORTED;
+  if (p.peer_mode) return AMS_OK;
+  if (p.cfg.capacity >= ((int64_t)1 << 31)) return AMS_ERR_UNSUPPORTED;   // int32 ids in the partial lists
+  AMS_CUDA_TRY(cudaSetDevice(p.cfg.device));
+  const size_t slot = (size_t)2 * G * p.cfg.max_queries * p.cfg.max_k;
+  bool ok = cudaMalloc((void**)&p.x_s, slot * 4) == cudaSuccess && cudaMalloc((void**)&p.x_i, slot * 8) == cudaSuccess &&
+            cudaMalloc((void**)&p.x_flag, G * 8) == cudaSuccess && cudaMalloc((void**)&p.x_done, 16) == cudaSuccess;
+  if (!ok) {
+    cudaGetLastError();
+    free_peers(p);
+    return AMS_ERR_OUT_OF_MEMORY;
+  }
+  AMS_CUDA_TRY(cudaMemset(p.x_flag, 0, G * 8));
+  AMS_CUDA_TRY(cudaMemset(p.x_done, 0, 16));
+  AMS_CUDA_TRY(cudaDeviceSynchronize());
+  // exchange the three IPC handles of every rank over the pool's NCCL communicator
+  const size_t hb = 3 * sizeof(cudaIpcMemHandle_t);
+  std::vector<unsigned char> host((size_t)G * hb);
+  cudaIpcMemHandle_t* mine = reinterpret_cast<cudaIpcMemHandle_t*>(host.data() + (size_t)r * hb);
+  if (cudaIpcGetMemHandle(&mine[0], p.x_s) != cudaSuccess || cudaIpcGetMemHandle(&mine[1], p.x_i) != cudaSuccess ||
+      cudaIpcGetMemHandle(&mine[2], p.x_flag) != cudaSuccess) {
+    cudaGetLastError();
+    free_peers(p);
+    return AMS_ERR_UNSUPPORTED;
+  }
+  void* dbuf = nullptr;
+  AMS_CUDA_TRY(cudaMalloc(&dbuf, host.size()));
+  AMS_CUDA_TRY(cudaMemcpy(static_cast<unsigned char*>(dbuf) + (size_t)r * hb, mine, hb, cudaMemcpyHostToDevice));
+  ncclComm_t comm = static_cast<ncclComm_t>(p.nccl_comm);
+  if (ncclAllGather(static_cast<unsigned char*>(dbuf) + (size_t)r * hb, dbuf, hb, ncclChar, comm, nullptr) !=
+      ncclSuccess) {
+    cudaFree(dbuf);
+    return fail(pool, AMS_ERR_NCCL);
+  }
+  AMS_CUDA_TRY(cudaDeviceSynchronize());
+  AMS_CUDA_TRY(cudaMemcpy(host.data(), dbuf, host.size(), cudaMemcpyDeviceToHost));
+  cudaFree(dbuf);
+  ams::PeerTable pt{};
+  pt.G = G;
+  pt.rank = r;
+  pt.max_q = p.cfg.max_queries;
+  pt.max_k = p.cfg.max_k;
+  p.peer_mode = true;   // from here free_peers closes whatever was opened
+  for (int g = 0; g < G; ++g) {
+    if (g == r) {
+      pt.s[g] = p.x_s;
+      pt.i[g] = p.x_i;
+      pt.flag[g] = p.x_flag;
+      continue;
+    }
+    const cudaIpcMemHandle_t* h = reinterpret_cast<const cudaIpcMemHandle_t*>(host.data() + (size_t)g * hb);
+    void *a0 = nullptr, *a1 = nullptr, *a2 = nullptr;
+    if (cudaIpcOpenMemHandle(&a0, h[0], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
+        cudaIpcOpenMemHandle(&a1, h[1], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
+        cudaIpcOpenMemHandle(&a2, h[2], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      p.peers = pt;
+      free_peers(p);
+      return AMS_ERR_UNSUPPORTED;
+    }
+    pt.s[g] = static_cast<float*>(a0);
+    pt.i[g] = static_cast<int64_t*>(a1);
+    pt.flag[g] = static_cast<unsigned long long*>(a2);
+    p.peers = pt;
+  }
+  p.peers = pt;
+  p.epoch = 0;
+  // every rank has mapped every peer before anyone writes into a peer buffer
+  if (ncclAllGather(p.x_done + 1, p.x_done + 2, 1, ncclUint32, comm, nullptr) != ncclSuccess)
+    return fail(pool, AMS_ERR_NCCL);
+  AMS_CUDA_TRY(cudaDeviceSynchronize());
   return AMS_OK;
 }
 

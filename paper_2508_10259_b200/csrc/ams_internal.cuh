@@ -49,6 +49,18 @@ __host__ __device__ inline int64_t joint_offset(int64_t l, int t, int JP) {
   return ((l / kRowAlign) * JP + t) * kRowAlign + (l % kRowAlign);
 }
 
+// --------------------------------------------------------------------------- peer exchange
+constexpr int kMaxPeers = 8;   // one NVSwitch box
+// Receive buffers of every rank (local pointer for itself, CUDA-IPC mappings for peers):
+// s/i are [2 parities][G senders][max_q][max_k]; flag is [G senders] epochs.
+struct PeerTable {
+  float* s[kMaxPeers];
+  int64_t* i[kMaxPeers];
+  unsigned long long* flag[kMaxPeers];
+  int32_t G, rank;
+  int32_t max_q, max_k;
+};
+
 // --------------------------------------------------------------------------- pool
 struct Pool {
   ams_pool_config_t cfg{};
@@ -104,6 +116,15 @@ struct Pool {
 
   void* nccl_comm = nullptr;  // ncclComm_t
 
+  // fused NVLink exchange (opt-in, ams_pool_enable_peer_exchange)
+  bool peer_mode = false;
+  PeerTable peers{};
+  unsigned long long epoch = 0;
+  unsigned int* x_done = nullptr;
+  float* x_s = nullptr;                 // own receive buffers (also peers.s[rank])
+  int64_t* x_i = nullptr;
+  unsigned long long* x_flag = nullptr;
+
   // instrumentation
   bool profiling = false;
   std::vector<cudaEvent_t> ev_free;
@@ -141,6 +162,13 @@ cudaError_t launch_merge_lists(const MatchArgs& a, int32_t G, int32_t kin, const
 // gate-first sparse variant (bf16 pools): writes [nq][k] (+hit if out_hit)
 cudaError_t launch_gate_first(Pool& p, const MatchArgs& a, float* out_s, int64_t* out_i, uint8_t* out_hit,
                               cudaStream_t s);
+cudaError_t launch_exchange_push(int KT, const float* ps, const int32_t* pi, int32_t nq, int32_t P, int32_t k,
+                                 const PeerTable& pt, unsigned long long epoch, unsigned int* done, int32_t world_ids,
+                                 int64_t B, cudaStream_t s);
+cudaError_t launch_exchange_wait(int KT, const PeerTable& pt, int32_t nq, int32_t k, unsigned long long epoch,
+                                 float* os, int64_t* oi, uint8_t* oh, float th, cudaStream_t s);
+cudaError_t launch_to_partials(const float* s, const int64_t* i, int32_t nq, int32_t k, int32_t KT, float* ps,
+                               int32_t* pi, cudaStream_t st);
 int pick_KT(int k);
 
 }  // namespace ams
