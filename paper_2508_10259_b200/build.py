@@ -13,6 +13,7 @@ from __future__ import annotations
 import concurrent.futures as cf
 import glob
 import os
+import re
 import subprocess
 import sys
 import sysconfig
@@ -53,9 +54,11 @@ def _stale(out, deps):
 def build(force: bool = False, verbose: bool = False) -> str:
     global OUT, BUILD
     if DIAG:
-        OUT = os.path.join(ROOT, "diag_lib", "libams_diag.so")  # travels with gpurun (build/ does not)
-        BUILD = os.path.join(ROOT, "build", "diag")
+        tag = re.sub(r"[^A-Za-z0-9]+", "_", DIAG).strip("_").lower()
+        OUT = os.path.join(ROOT, "diag_lib", f"libams_diag_{tag}.so")  # travels with gpurun (build/ does not)
+        BUILD = os.path.join(ROOT, "build", "diag_" + tag)
     os.makedirs(BUILD, exist_ok=True)
+    os.makedirs(os.path.dirname(OUT), exist_ok=True)
     inc, lib = nccl_dirs()
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     hdrs = sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [os.path.join(ROOT, "include", "ams.h")]

@@ -108,6 +108,10 @@ void plan_tc(const Pool& p, int nq, int KT, int& S, int& grid, int& cg) {
     }
   }
   S = best;
+#ifdef AMS_DIAG_SPLIT_MULT   // diagnostic builds only: shorter units (L2-reuse experiments)
+  S = (int)std::min<int64_t>({(int64_t)best * AMS_DIAG_SPLIT_MULT, std::max<int64_t>(1, n_pt),
+                              std::max<int64_t>(1, p.part_cap / (nq_pad * ams::kEpiHalves * KT))});
+#endif
   grid = (int)std::min<int64_t>((int64_t)n_qt * S, clusters) * cg;
 }
 
@@ -271,7 +275,7 @@ ams_status_t ams_pool_create(const ams_pool_config_t* cfg, ams_pool_t* out) {
             alloc(&p.q_stage, (size_t)p.q_pad * d * es) && alloc((void**)&p.q_inv, (size_t)p.q_pad * 4) &&
             alloc((void**)&p.q_joints, (size_t)p.q_pad * p.JP * 4) &&
             alloc((void**)&p.q_joints_raw, (size_t)c.max_queries * c.joint_dim * 4) &&
-            alloc((void**)&p.bound, (size_t)p.q_pad * 4) &&
+            alloc((void**)&p.bound, (size_t)(p.q_pad + 32) * 4) &&
             alloc((void**)&p.part_s, (size_t)part * 4) && alloc((void**)&p.part_i, (size_t)part * 4) &&
             alloc((void**)&p.shard_s, (size_t)c.max_queries * c.max_k * 4) &&
             alloc((void**)&p.shard_i, (size_t)c.max_queries * c.max_k * 8) &&

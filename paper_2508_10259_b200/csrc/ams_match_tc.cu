@@ -42,6 +42,15 @@
 #include "ams_topk.cuh"
 
 namespace ams {
+#ifdef AMS_DIAG_TIMELINE   // diagnostic builds only: per-unit start/end globaltimer + cluster id
+constexpr int kDiagUnits = 1 << 16;
+__device__ unsigned long long g_diag_tl[kDiagUnits * 3];
+__device__ __forceinline__ unsigned int __smid() {
+  unsigned int r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+#endif
 
 namespace {
 
@@ -68,6 +77,7 @@ struct TcParams {
   float* part_s;
   int32_t* part_i;
   uint32_t* bound;           // [nq] per-query admission lower bound (ordered-u32; 0 = none)
+  uint32_t* wave_ctr;        // producers' unit-completion counter (zeroed per launch; bound[nq])
   int64_t L;                 // local rows
   int32_t nq, d, n_qt, n_pt, S, n_units, k, gated, P;
   float g2;
@@ -257,11 +267,24 @@ __global__ void __maxnreg__(168)
       int stage = 0;
       uint32_t phase = 0;
       uint32_t tile_count = 0;
-      for (int u = cid; u < prm.n_units; u += ncl) {
+      uint32_t wave = 0;
+      for (int u = cid; u < prm.n_units; u += ncl, ++wave) {
         const int sp = u / prm.n_qt, qt = u % prm.n_qt;
         int t_lo, t_hi;
         split_tiles(sp, prm.S, prm.n_pt, t_lo, t_hi);
         const int qrow0 = qt * kBlockM * CG + (int)crank * kBlockM;
+        // Wave lockstep: the units sharing a row split run in the same wave (split-major
+        // order) and re-read its rows from L2 only while they stay within ~1 ms of each
+        // other.  Static striding lets per-unit jitter accumulate across waves (measured
+        // on C4: 4 ms start spread, 13x DRAM re-reads), so no producer starts wave w
+        // before every CTA has issued all loads of wave w-1.  Best effort: the wait is
+        // bounded (~10 ms), so a grid that is not fully co-resident (MPS, concurrent
+        // kernels) still progresses -- the lockstep only ever affects speed, never results.
+        if (wave > 0) {
+          const uint32_t need = wave * gridDim.x;
+          for (int it = 0; it < (1 << 16) && *reinterpret_cast<volatile uint32_t*>(prm.wave_ctr) < need; ++it)
+            __nanosleep(128);
+        }
         for (int t = t_lo; t < t_hi; ++t, ++tile_count) {
           const int buf = tile_count & 1;
           const uint32_t use = tile_count >> 1;
@@ -289,6 +312,7 @@ __global__ void __maxnreg__(168)
             }
           }
         }
+        atomicAdd(prm.wave_ctr, 1u);
       }
     }
   } else if (warp == kMmaWarp) {
@@ -301,6 +325,10 @@ __global__ void __maxnreg__(168)
         const int sp = u / prm.n_qt;
         int t_lo, t_hi;
         split_tiles(sp, prm.S, prm.n_pt, t_lo, t_hi);
+#ifdef AMS_DIAG_TIMELINE
+        unsigned long long t0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+#endif
         for (int t = t_lo; t < t_hi; ++t, ++tile_count) {
           const int buf = tile_count & 1;
           const uint32_t use = tile_count >> 1;
@@ -325,6 +353,15 @@ __global__ void __maxnreg__(168)
           }
           ptx::umma_commit<CG>(&tfull[buf]);
         }
+#ifdef AMS_DIAG_TIMELINE
+        unsigned long long t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        if (u < kDiagUnits) {
+          g_diag_tl[3 * u] = t0;
+          g_diag_tl[3 * u + 1] = t1;
+          g_diag_tl[3 * u + 2] = (unsigned long long)cid | ((unsigned long long)__smid() << 32);
+        }
+#endif
       }
     }
     __syncwarp();
@@ -477,6 +514,7 @@ cudaError_t launch_match_tc(Pool& p, const MatchArgs& a, int32_t S, int32_t grid
   prm.part_s = p.part_s;
   prm.part_i = p.part_i;
   prm.bound = p.bound;
+  prm.wave_ctr = p.bound + a.nq;
   prm.L = p.local;
   prm.nq = a.nq;
   prm.d = p.cfg.dim;
@@ -488,7 +526,7 @@ cudaError_t launch_match_tc(Pool& p, const MatchArgs& a, int32_t S, int32_t grid
   prm.gated = a.gated;
   prm.P = S * kEpiHalves;
   prm.g2 = a.g2;
-  cudaError_t e = cudaMemsetAsync(p.bound, 0, (size_t)a.nq * sizeof(uint32_t), s);
+  cudaError_t e = cudaMemsetAsync(p.bound, 0, (size_t)(a.nq + 1) * sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
   e = cg == 2 ? launch_tc_cg<2>(p, a, prm, grid, s) : launch_tc_cg<1>(p, a, prm, grid, s);
   ++p.launches;
@@ -496,3 +534,10 @@ cudaError_t launch_match_tc(Pool& p, const MatchArgs& a, int32_t S, int32_t grid
 }
 
 }  // namespace ams
+
+#ifdef AMS_DIAG_TIMELINE
+extern "C" int ams_diag_timeline(unsigned long long* host, int n_units) {
+  if (n_units > ams::kDiagUnits) n_units = ams::kDiagUnits;
+  return (int)cudaMemcpyFromSymbol(host, ams::g_diag_tl, (size_t)n_units * 3 * 8);
+}
+#endif
