@@ -78,6 +78,10 @@ bool is_device_ptr(const void* ptr) {
 
 int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
+// Smallest gated bf16 batch staged in joint-0 order (below it one warp's queries span
+// most of the joint range and the per-lane packed filter is cheaper).
+constexpr int32_t kSortMinQueries = 129;
+
 size_t esize(const Pool& p) { return p.cfg.dtype == AMS_DTYPE_BF16 ? 2 : 4; }
 
 // Plan of the tcgen05 kernel.  Queries > 128 -> CTA pairs (cta_group::2, 256-query
@@ -143,7 +147,8 @@ void free_peers(Pool& p) {
 
 void free_all(Pool& p) {
   free_peers(p);
-  void* ptrs[] = {p.emb, p.inv_norm, p.joints, p.q_stage, p.q_inv, p.q_joints, p.q_joints_raw, p.bound,
+  void* ptrs[] = {p.emb, p.inv_norm, p.joints, p.q_stage, p.q_inv, p.q_joints, p.q_joints_raw, p.q_raw, p.q_perm,
+                  p.bound,
                   p.gf_cnt, p.gf_cand,
                   p.part_s, p.part_i, p.shard_s, p.shard_i, p.gath_s, p.gath_i, p.stage_emb,
                   p.stage_joints};
@@ -275,6 +280,7 @@ ams_status_t ams_pool_create(const ams_pool_config_t* cfg, ams_pool_t* out) {
             alloc(&p.q_stage, (size_t)p.q_pad * d * es) && alloc((void**)&p.q_inv, (size_t)p.q_pad * 4) &&
             alloc((void**)&p.q_joints, (size_t)p.q_pad * p.JP * 4) &&
             alloc((void**)&p.q_joints_raw, (size_t)c.max_queries * c.joint_dim * 4) &&
+            alloc(&p.q_raw, (size_t)c.max_queries * d * es) && alloc((void**)&p.q_perm, (size_t)p.q_pad * 4) &&
             alloc((void**)&p.bound, (size_t)(p.q_pad + 32) * 4) &&
             alloc((void**)&p.part_s, (size_t)part * 4) && alloc((void**)&p.part_i, (size_t)part * 4) &&
             alloc((void**)&p.shard_s, (size_t)c.max_queries * c.max_k * 4) &&
@@ -386,14 +392,20 @@ static ams_status_t match_impl(ams_pool_t pool, const void* q_emb, const float* 
   const void* q_src = q_emb;
   const float* qj_src = q_joints;
   if (!is_device_ptr(q_emb)) {
-    AMS_CUDA_TRY(cudaMemcpyAsync(p.q_stage, q_emb, (size_t)nq * p.cfg.dim * es, cudaMemcpyDefault, s));
-    q_src = p.q_stage;
+    AMS_CUDA_TRY(cudaMemcpyAsync(p.q_raw, q_emb, (size_t)nq * p.cfg.dim * es, cudaMemcpyDefault, s));
+    q_src = p.q_raw;
   }
   if (!is_device_ptr(q_joints)) {
     AMS_CUDA_TRY(cudaMemcpyAsync(p.q_joints_raw, q_joints, (size_t)nq * p.cfg.joint_dim * 4, cudaMemcpyDefault, s));
     qj_src = p.q_joints_raw;
   }
-  AMS_CUDA_TRY(ams::launch_query_prep(p, q_src, qj_src, nq, s));
+  // Gated tcgen05 batches are staged in joint-0 order (the epilogue's warp-level gate
+  // test then rejects most columns for all 32 queries of a warp at once).  The order is
+  // invisible to the caller: partial lists land at the caller's query index.
+  const bool sorted = p.cfg.dtype == AMS_DTYPE_BF16 && !gate_first && a.gated && p.local > 0 &&
+                      nq >= kSortMinQueries;
+  if (sorted) AMS_CUDA_TRY(ams::launch_query_order(p, qj_src, nq, s));
+  AMS_CUDA_TRY(ams::launch_query_prep(p, q_src, qj_src, nq, sorted ? p.q_perm : nullptr, s));
 
   const bool multi = p.cfg.world > 1;
   float* shard_s = multi ? p.shard_s : out_score;
@@ -442,7 +454,7 @@ static ams_status_t match_impl(ams_pool_t pool, const void* q_emb, const float* 
       plan_tc(p, nq, a.KT, S, grid, cg);
       P = S * ams::kEpiHalves;
       if (e0) AMS_CUDA_TRY(cudaEventRecord(e0, s));
-      AMS_CUDA_TRY(ams::launch_match_tc(p, a, S, grid, cg, s));
+      AMS_CUDA_TRY(ams::launch_match_tc(p, a, S, grid, cg, sorted, s));
       if (e1) AMS_CUDA_TRY(cudaEventRecord(e1, s));
       p.last_splits = S;
       p.last_grid = grid;

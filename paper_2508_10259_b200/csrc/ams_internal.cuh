@@ -85,6 +85,8 @@ struct Pool {
   float* q_inv = nullptr;     // [q_pad]
   float* q_joints = nullptr;  // [q_pad, JP]
   float* q_joints_raw = nullptr;  // [max_queries, J] host-staged joints
+  void* q_raw = nullptr;      // [max_queries, d] host-staged query rows (gathered into q_stage)
+  int32_t* q_perm = nullptr;  // [q_pad] staged position -> caller's query (joint-0 order)
 
   // partial top-k lists [nq][P][KT]
   int64_t part_cap = 0;       // entries
@@ -144,10 +146,16 @@ struct MatchArgs {
 
 cudaError_t launch_append(Pool& p, const void* emb_src, const float* joints_src, int64_t n_src,
                           int64_t first_global, cudaStream_t s);
-cudaError_t launch_query_prep(Pool& p, const void* q_src, const float* qj_src, int32_t nq, cudaStream_t s);
+// perm (device, may be null = identity): staged row q is the caller's query perm[q]
+cudaError_t launch_query_prep(Pool& p, const void* q_src, const float* qj_src, int32_t nq, const int32_t* perm,
+                              cudaStream_t s);
+// p.q_perm <- the queries ordered by joint 0 (counting sort into linear bins; one block)
+cudaError_t launch_query_order(Pool& p, const float* qj_src, int32_t nq, cudaStream_t s);
 cudaError_t launch_match_simt(Pool& p, const MatchArgs& a, int32_t splits, cudaStream_t s);
 // cg = 1: one CTA per 128x256 tile; cg = 2: CTA pair (cta_group::2) per 256x256 tile
-cudaError_t launch_match_tc(Pool& p, const MatchArgs& a, int32_t splits, int32_t grid, int32_t cg, cudaStream_t s);
+// sorted: queries were staged through p.q_perm (partials land at the caller's query index)
+cudaError_t launch_match_tc(Pool& p, const MatchArgs& a, int32_t splits, int32_t grid, int32_t cg, bool sorted,
+                            cudaStream_t s);
 int tc_query_tile(int cg);
 // merge [nq][P][KT] local lists -> [nq][k] (fp32, global int64); writes hit if out_hit != null
 cudaError_t launch_merge_partials(Pool& p, const MatchArgs& a, int32_t P, float* out_s, int64_t* out_i,

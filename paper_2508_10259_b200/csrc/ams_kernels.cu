@@ -69,15 +69,18 @@ __global__ void append_kernel(const void* __restrict__ src, const float* __restr
 // ---------------------------------------------------------------------------------
 // Query prep: stage the query rows, inv_q, zero-padded joints.  One warp per query.
 // ---------------------------------------------------------------------------------
+// Staged row q holds the caller's query perm[q] (perm == nullptr: identity).
 template <bool BF16>
 __global__ void query_prep_kernel(const void* __restrict__ src, const float* __restrict__ jsrc, int32_t nq,
-                                  int32_t d, int32_t J, int32_t JP, void* __restrict__ q_stage,
-                                  float* __restrict__ q_inv, float* __restrict__ q_joints) {
+                                  int32_t d, int32_t J, int32_t JP, const int32_t* __restrict__ perm,
+                                  void* __restrict__ q_stage, float* __restrict__ q_inv,
+                                  float* __restrict__ q_joints) {
   const int lane = threadIdx.x & 31;
   const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (q >= nq) return;
+  const int64_t o = perm != nullptr ? (int64_t)perm[q] : (int64_t)q;
   if (BF16) {
-    const uint4* s4 = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(src) + (int64_t)q * d);
+    const uint4* s4 = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(src) + o * d);
     uint4* d4 = reinterpret_cast<uint4*>(static_cast<uint16_t*>(q_stage) + (int64_t)q * d);
     double ss = 0.0;
     for (int c = lane; c < d / 8; c += 32) {
@@ -94,7 +97,7 @@ __global__ void query_prep_kernel(const void* __restrict__ src, const float* __r
     ss = warp_sum_f64(ss);
     if (lane == 0) q_inv[q] = ss > 0.0 ? __double2float_rn(1.0 / sqrt(ss)) : 0.0f;
   } else {
-    const float* s = static_cast<const float*>(src) + (int64_t)q * d;
+    const float* s = static_cast<const float*>(src) + o * d;
     float* e = static_cast<float*>(q_stage) + (int64_t)q * d;
     if (s != e)
       for (int c = lane; c < d; c += 32) e[c] = s[c];
@@ -104,7 +107,87 @@ __global__ void query_prep_kernel(const void* __restrict__ src, const float* __r
       q_inv[q] = ss > 0.0f ? __fdiv_rn(1.0f, __fsqrt_rn(ss)) : 0.0f;
     }
   }
-  if (lane < JP) q_joints[(int64_t)q * JP + lane] = lane < J ? jsrc[(int64_t)q * J + lane] : 0.0f;
+  if (lane < JP) q_joints[(int64_t)q * JP + lane] = lane < J ? jsrc[o * J + lane] : 0.0f;
+}
+
+// ---------------------------------------------------------------------------------
+// Query order for the gated tcgen05 path: a counting sort of the queries by joint 0
+// into kOrderBins linear bins between the batch's min and max (one block).  Any order
+// gives the same results (every query is scored independently); this one makes the
+// 32 queries of an epilogue warp span a narrow joint-0 interval, so most pool columns
+// fail the warp-level gate test of epi_chunk_sorted.  Order within a bin is arbitrary.
+// ---------------------------------------------------------------------------------
+constexpr int kOrderBins = 4096;
+constexpr int kOrderThreads = 1024;
+
+__global__ void __launch_bounds__(kOrderThreads)
+    query_order_kernel(const float* __restrict__ jsrc, int32_t J, int32_t nq, int32_t* __restrict__ perm) {
+  __shared__ uint32_t hist[kOrderBins];
+  __shared__ float red_lo[kOrderThreads / 32], red_hi[kOrderThreads / 32];
+  __shared__ uint32_t wsum[kOrderThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  float lo = CUDART_INF_F, hi = -CUDART_INF_F;
+  for (int q = tid; q < nq; q += kOrderThreads) {
+    const float v = jsrc[(int64_t)q * J];
+    if (v == v) {
+      lo = fminf(lo, v);
+      hi = fmaxf(hi, v);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if (lane == 0) {
+    red_lo[w] = lo;
+    red_hi[w] = hi;
+  }
+  for (int b = tid; b < kOrderBins; b += kOrderThreads) hist[b] = 0u;
+  __syncthreads();
+  lo = red_lo[0];
+  hi = red_hi[0];
+  for (int i = 1; i < kOrderThreads / 32; ++i) {
+    lo = fminf(lo, red_lo[i]);
+    hi = fmaxf(hi, red_hi[i]);
+  }
+  const float span = hi - lo;
+  const float scale = (span > 1e-30f && span < CUDART_INF_F) ? (float)kOrderBins / span : 0.0f;
+  auto bin_of = [&](float v) -> int {
+    const float f = (v - lo) * scale;
+    return (f >= 0.0f && f < (float)kOrderBins) ? (int)f : (f >= 0.0f ? kOrderBins - 1 : 0);
+  };
+  for (int q = tid; q < nq; q += kOrderThreads) atomicAdd(&hist[bin_of(jsrc[(int64_t)q * J])], 1u);
+  __syncthreads();
+  // exclusive scan: thread t owns bins [4t, 4t+4)
+  constexpr int per = kOrderBins / kOrderThreads;
+  uint32_t v[per], run = 0;
+#pragma unroll
+  for (int i = 0; i < per; ++i) {
+    v[i] = hist[tid * per + i];
+    run += v[i];
+  }
+  uint32_t incl = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[w] = incl;
+  __syncthreads();
+  uint32_t base = 0;
+  for (int i = 0; i < w; ++i) base += wsum[i];
+  base += incl - run;
+#pragma unroll
+  for (int i = 0; i < per; ++i) {
+    hist[tid * per + i] = base;
+    base += v[i];
+  }
+  __syncthreads();
+  for (int q = tid; q < nq; q += kOrderThreads) {
+    const uint32_t pos = atomicAdd(&hist[bin_of(jsrc[(int64_t)q * J])], 1u);
+    perm[pos] = q;
+  }
 }
 
 // ---------------------------------------------------------------------------------
@@ -268,15 +351,22 @@ cudaError_t launch_append(Pool& p, const void* emb_src, const float* joints_src,
   return cudaGetLastError();
 }
 
-cudaError_t launch_query_prep(Pool& p, const void* q_src, const float* qj_src, int32_t nq, cudaStream_t s) {
+cudaError_t launch_query_prep(Pool& p, const void* q_src, const float* qj_src, int32_t nq, const int32_t* perm,
+                              cudaStream_t s) {
   const int wpb = 8;
   const auto& c = p.cfg;
   if (c.dtype == AMS_DTYPE_BF16)
     query_prep_kernel<true><<<blocks_for(nq, wpb), wpb * 32, 0, s>>>(q_src, qj_src, nq, c.dim, c.joint_dim,
-                                                                     p.JP, p.q_stage, p.q_inv, p.q_joints);
+                                                                     p.JP, perm, p.q_stage, p.q_inv, p.q_joints);
   else
     query_prep_kernel<false><<<blocks_for(nq, wpb), wpb * 32, 0, s>>>(q_src, qj_src, nq, c.dim, c.joint_dim,
-                                                                      p.JP, p.q_stage, p.q_inv, p.q_joints);
+                                                                      p.JP, perm, p.q_stage, p.q_inv, p.q_joints);
+  ++p.launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_query_order(Pool& p, const float* qj_src, int32_t nq, cudaStream_t s) {
+  query_order_kernel<<<1, kOrderThreads, 0, s>>>(qj_src, p.cfg.joint_dim, nq, p.q_perm);
   ++p.launches;
   return cudaGetLastError();
 }

@@ -78,8 +78,10 @@ struct TcParams {
   int32_t* part_i;
   uint32_t* bound;           // [nq] per-query admission lower bound (ordered-u32; 0 = none)
   uint32_t* wave_ctr;        // producers' unit-completion counter (zeroed per launch; bound[nq])
+  const int32_t* perm;       // staged query position -> caller's query (nullptr: identity)
   int64_t L;                 // local rows
   int32_t nq, d, n_qt, n_pt, S, n_units, k, gated, P;
+  int32_t sorted;            // queries staged in joint-0 order: the warp-level column test pays
   float g2;
 };
 
@@ -199,6 +201,50 @@ __device__ __forceinline__ void epi_chunk(uint32_t taddr, int64_t jbase, int nva
       if (ok) top.insert_monotone(s, (int32_t)(jbase + cc), k);
     }
   }
+}
+
+// Gated chunk for a warp whose 32 queries are sorted by joint 0 (their r_0 lie in
+// [wlo, whi]).  Lane c first tests column c against the whole warp at once: the
+// canonical distance is >= RN(d0^2) (the first fmaf adds to +0, later ones only add
+// non-negative terms and RN is monotone), and the smallest |RN(r_0 - p_0)| over the
+// warp is reached at wlo or whi, so a column with RN(RN(w - p_0)^2) > g2 for the
+// nearest end w is ineligible for every lane.  The surviving columns (the ballot) are
+// then gated exactly per lane, one column at a time; TMEM is read only for a column
+// some lane passes.  Returns false (nothing done) when too many columns survive for
+// the per-column loop to beat the packed filter; the caller then runs epi_chunk.
+constexpr int kSparseMaxCols = 10;
+
+template <int KT, int JP>
+__device__ __forceinline__ bool epi_chunk_sorted(uint32_t taddr, int64_t jbase, int nvalid,
+                                                 const float* __restrict__ inv_sm, const float* __restrict__ jsm,
+                                                 const float (&qj)[JP], float iq, float g2, float bound, int k,
+                                                 float wlo, float whi, int lane, TopK<KT, int32_t>& top) {
+  const float p0 = jsm[lane];
+  const float d0 = p0 < wlo ? __fsub_rn(wlo, p0) : (p0 > whi ? __fsub_rn(whi, p0) : 0.0f);
+  uint32_t m = __ballot_sync(0xffffffffu, __fmul_rn(d0, d0) <= g2);
+  if (__popc(m) > kSparseMaxCols) return false;
+  while (m != 0u) {
+    const int c = __ffs(m) - 1;
+    m &= m - 1u;
+    float ds = 0.0f;
+    bool ok = true;
+#pragma unroll
+    for (int g = 0; g < JP / 4; ++g) {
+      if (!__any_sync(0xffffffffu, ok)) break;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float df = __fsub_rn(qj[4 * g + u], jsm[(4 * g + u) * kBlockN + c]);
+        ds = __fmaf_rn(df, df, ds);
+      }
+      ok = ok && (ds <= g2);
+    }
+    if (!__any_sync(0xffffffffu, ok)) continue;
+    const uint32_t v = ptx::tmem_ld1(taddr + (uint32_t)c);
+    ptx::tmem_wait_ld();
+    const float s = __fmul_rn(__fmul_rn(__uint_as_float(v), iq), inv_sm[c]);
+    if (ok && s > top.kth_s && s >= bound && c < nvalid) top.insert_monotone(s, (int32_t)(jbase + c), k);
+  }
+  return true;
 }
 
 template <int KT, int JP, int CG>
@@ -387,6 +433,14 @@ __global__ void __maxnreg__(168)
       for (int t = 0; t < 4; ++t) QQ[t] = ptx::pack2(qj[t], qj[t]);   // JP >= 4
       const float iq = active ? prm.inv_q[qrow] : 0.0f;
       const uint64_t IQ2 = ptx::pack2(iq, iq);
+      // joint-0 interval of the warp's active queries (empty warp: +inf/-inf, no column passes)
+      float wlo = active ? qj[0] : CUDART_INF_F, whi = active ? qj[0] : -CUDART_INF_F;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        wlo = fminf(wlo, __shfl_xor_sync(0xffffffffu, wlo, o));
+        whi = fmaxf(whi, __shfl_xor_sync(0xffffffffu, whi, o));
+      }
+      const bool sparse = gated && prm.sorted != 0;
       uint32_t* bnd = prm.bound + (active ? qrow : 0);
       float bound = -CUDART_INF_F;
       if (active) {
@@ -414,6 +468,9 @@ __global__ void __maxnreg__(168)
 #ifdef AMS_DIAG_NO_EPILOGUE  // diagnostic builds only (scripts/diag_power.py): MMA + TMA alone
           continue;
 #endif
+          if (sparse && epi_chunk_sorted<KT, JP>(taddr, jbase, nvalid, inv_sm + col0, joints_sm + col0, qj, iq,
+                                                 prm.g2, bound, prm.k, wlo, whi, lane, top))
+            continue;
           if (gated)
             epi_chunk<KT, JP, true>(taddr, jbase, nvalid, inv_sm + col0, joints_sm + col0, QQ, qj, IQ2, iq,
                                     prm.g2, bound, prm.k, top);
@@ -441,7 +498,8 @@ __global__ void __maxnreg__(168)
         }
       }
       if (active) {
-        const int64_t base = ((int64_t)qrow * prm.P + (int64_t)sp * kEpiHalves + h) * KT;
+        const int64_t qout = prm.perm != nullptr ? (int64_t)prm.perm[qrow] : (int64_t)qrow;
+        const int64_t base = (qout * prm.P + (int64_t)sp * kEpiHalves + h) * KT;
 #pragma unroll
         for (int r = 0; r < KT; r += 4) {
           *reinterpret_cast<float4*>(prm.part_s + base + r) =
@@ -505,7 +563,8 @@ cudaError_t launch_tc_cg(Pool& p, const MatchArgs& a, const TcParams& prm, int g
 
 int tc_query_tile(int cg) { return kBlockM * cg; }
 
-cudaError_t launch_match_tc(Pool& p, const MatchArgs& a, int32_t S, int32_t grid, int32_t cg, cudaStream_t s) {
+cudaError_t launch_match_tc(Pool& p, const MatchArgs& a, int32_t S, int32_t grid, int32_t cg, bool sorted,
+                            cudaStream_t s) {
   TcParams prm{};
   prm.inv_q = p.q_inv;
   prm.q_joints = p.q_joints;
@@ -515,6 +574,8 @@ cudaError_t launch_match_tc(Pool& p, const MatchArgs& a, int32_t S, int32_t grid
   prm.part_i = p.part_i;
   prm.bound = p.bound;
   prm.wave_ctr = p.bound + a.nq;
+  prm.perm = sorted ? p.q_perm : nullptr;
+  prm.sorted = sorted ? 1 : 0;
   prm.L = p.local;
   prm.nq = a.nq;
   prm.d = p.cfg.dim;

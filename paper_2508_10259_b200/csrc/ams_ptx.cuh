@@ -197,6 +197,12 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
                : "memory");
 }
 
+__device__ __forceinline__ uint32_t tmem_ld1(uint32_t taddr) {
+  uint32_t v;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(taddr) : "memory");
+  return v;
+}
+
 // Shared-memory matrix descriptor, K-major operand, 128-byte swizzle (rows of 64 bf16,
 // 8-row core-matrix groups 1024 B apart): start>>4 [0,14), LBO>>4 [16,30) (=1, unused for
 // swizzled K-major), SBO>>4 [32,46) (=1024 B), version [46,48) = 1 (sm_100),
