@@ -402,8 +402,7 @@ static ams_status_t match_impl(ams_pool_t pool, const void* q_emb, const float* 
   // Gated tcgen05 batches are staged in joint-0 order (the epilogue's warp-level gate
   // test then rejects most columns for all 32 queries of a warp at once).  The order is
   // invisible to the caller: partial lists land at the caller's query index.
-  const bool sorted = p.cfg.dtype == AMS_DTYPE_BF16 && !gate_first && a.gated && p.local > 0 &&
-                      nq >= kSortMinQueries;
+  const bool sorted = p.cfg.dtype == AMS_DTYPE_BF16 && a.gated && p.local > 0 && nq >= kSortMinQueries;
   if (sorted) AMS_CUDA_TRY(ams::launch_query_order(p, qj_src, nq, s));
   AMS_CUDA_TRY(ams::launch_query_prep(p, q_src, qj_src, nq, sorted ? p.q_perm : nullptr, s));
 
@@ -429,7 +428,7 @@ static ams_status_t match_impl(ams_pool_t pool, const void* q_emb, const float* 
   int32_t P = 0;
   if (gate_first && p.cfg.dtype == AMS_DTYPE_BF16) {
     if (e0) AMS_CUDA_TRY(cudaEventRecord(e0, s));
-    AMS_CUDA_TRY(ams::launch_gate_first(p, a, shard_s, shard_i, shard_hit, s));
+    AMS_CUDA_TRY(ams::launch_gate_first(p, a, shard_s, shard_i, shard_hit, sorted, s));
     if (e1) {
       AMS_CUDA_TRY(cudaEventRecord(e1, s));
       p.ev_pending.emplace_back(e0, e1);

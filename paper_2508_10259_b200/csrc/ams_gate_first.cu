@@ -35,7 +35,7 @@ template <int JP>
 __global__ void __launch_bounds__(kGfThreads)
     gate_scan_kernel(const float* __restrict__ pool_joints, int64_t L, const float* __restrict__ q_joints,
                      int32_t nq, int32_t S, float g2, int32_t cap, uint32_t* __restrict__ cnt,
-                     int32_t* __restrict__ cand) {
+                     int32_t* __restrict__ cand, int32_t sorted) {
   __shared__ __align__(16) float js[2][JP * kGfTile];
   __shared__ __align__(16) float pn[kGfTile];       // per row: sum of squares of the first 4 joints
   __shared__ unsigned int pmax_bits;
@@ -52,6 +52,14 @@ __global__ void __launch_bounds__(kGfThreads)
 #pragma unroll
   for (int t = 0; t < 4; ++t) rq = fmaf(qj[t], qj[t], rq);
   const uint64_t M2 = ptx::pack2(-2.0f, -2.0f);
+  // joint-0 interval of the warp's active queries (see ams_match_tc.cu epi_chunk_sorted)
+  float wlo = active ? qj[0] : CUDART_INF_F, whi = active ? qj[0] : -CUDART_INF_F;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    wlo = fminf(wlo, __shfl_xor_sync(0xffffffffu, wlo, o));
+    whi = fmaxf(whi, __shfl_xor_sync(0xffffffffu, whi, o));
+  }
+  const int lane = threadIdx.x & 31;
   const int64_t n_pt = (L + kGfTile - 1) / kGfTile;
   const int64_t t_lo = n_pt * sp / S, t_hi = n_pt * (sp + 1) / S;
   auto stage = [&](int64_t t, int buf) {   // cp.async (LDGSTS): does not block the thread
@@ -87,8 +95,36 @@ __global__ void __launch_bounds__(kGfThreads)
                             : -CUDART_INF_F;
     const int64_t row0 = t * kGfTile;
     const int nvalid = (int)min((int64_t)kGfTile, L - row0);
+    auto exact = [&](int c) {   // canonical gate of row c for this lane's query
+      float ds = 0.0f;
+#pragma unroll
+      for (int u = 0; u < JP; ++u) {
+        const float df = __fsub_rn(qj[u], jsm[u * kGfTile + c]);
+        ds = __fmaf_rn(df, df, ds);
+      }
+      if (active && c < nvalid && ds <= g2) {
+        const uint32_t slot = atomicAdd(&cnt[q], 1u);
+        if (slot < (uint32_t)cap) cand[(int64_t)q * cap + slot] = (int32_t)(row0 + c);
+      }
+    };
 #pragma unroll 1
     for (int c8 = 0; c8 < kGfTile / 8; ++c8) {
+      if (sorted && (c8 & 3) == 0) {
+        // warp-level joint-0 test of the next 32 rows: a row whose joint 0 is farther
+        // than gamma from the warp's whole interval is ineligible for every lane
+        const float p0 = jsm[8 * c8 + lane];
+        const float d0 = p0 < wlo ? __fsub_rn(wlo, p0) : (p0 > whi ? __fsub_rn(whi, p0) : 0.0f);
+        uint32_t m = __ballot_sync(0xffffffffu, __fmul_rn(d0, d0) <= g2);
+        if (__popc(m) <= 10) {
+          while (m != 0u) {
+            const int c = 8 * c8 + __ffs(m) - 1;
+            m &= m - 1u;
+            exact(c);
+          }
+          c8 += 3;
+          continue;
+        }
+      }
       float mn = CUDART_INF_F;
 #pragma unroll
       for (int c4 = 2 * c8; c4 < 2 * c8 + 2; ++c4) {
@@ -109,18 +145,7 @@ __global__ void __launch_bounds__(kGfThreads)
       if (!__any_sync(0xffffffffu, mn <= tq)) continue;
       // exact canonical gate for the 8 rows of this group
 #pragma unroll 1
-      for (int c = 8 * c8; c < 8 * c8 + 8; ++c) {
-        float ds = 0.0f;
-#pragma unroll
-        for (int u = 0; u < JP; ++u) {
-          const float df = __fsub_rn(qj[u], jsm[u * kGfTile + c]);
-          ds = __fmaf_rn(df, df, ds);
-        }
-        if (active && c < nvalid && ds <= g2) {
-          const uint32_t slot = atomicAdd(&cnt[q], 1u);
-          if (slot < (uint32_t)cap) cand[(int64_t)q * cap + slot] = (int32_t)(row0 + c);
-        }
-      }
+      for (int c = 8 * c8; c < 8 * c8 + 8; ++c) exact(c);
     }
   }
 }
@@ -150,10 +175,11 @@ __global__ void score_kernel(const uint16_t* __restrict__ emb, const float* __re
                              int32_t nq, int32_t k, float g2, int32_t cap, const uint32_t* __restrict__ cnt,
                              const int32_t* __restrict__ cand, float* __restrict__ out_s, int64_t* __restrict__ out_i,
                              uint8_t* __restrict__ out_hit, float threshold, int32_t rank, int32_t world,
-                             int64_t B) {
+                             int64_t B, const int32_t* __restrict__ perm) {
   const int lane = threadIdx.x & 31;
   const int qi = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (qi >= nq) return;
+  const int64_t qo = perm != nullptr ? (int64_t)perm[qi] : (int64_t)qi;   // caller's query index
   const int n16 = d / 8;
   const uint4* qv = reinterpret_cast<const uint4*>(q + (int64_t)qi * d);
   const float iq = inv_q[qi];
@@ -213,8 +239,8 @@ __global__ void score_kernel(const uint16_t* __restrict__ emb, const float* __re
     }
     const int64_t gi = bi >= 0 ? shard_global((int64_t)bi, rank, world, B) : -1;
     if (lane == 0) {
-      out_s[(int64_t)qi * k + r] = bi >= 0 ? bs : -CUDART_INF_F;
-      out_i[(int64_t)qi * k + r] = gi;
+      out_s[qo * k + r] = bi >= 0 ? bs : -CUDART_INF_F;
+      out_i[qo * k + r] = gi;
     }
     if (r == 0) {
       s0 = bs;
@@ -222,12 +248,12 @@ __global__ void score_kernel(const uint16_t* __restrict__ emb, const float* __re
     }
     if (lane == bl) top.pop_front();
   }
-  if (out_hit != nullptr && lane == 0) out_hit[qi] = (i0 >= 0 && s0 >= threshold) ? 1 : 0;
+  if (out_hit != nullptr && lane == 0) out_hit[qo] = (i0 >= 0 && s0 >= threshold) ? 1 : 0;
 }
 
 template <int JP>
 cudaError_t launch_gf_jp(Pool& p, const MatchArgs& a, int32_t cap, float* out_s, int64_t* out_i, uint8_t* out_hit,
-                         cudaStream_t s) {
+                         bool sorted, cudaStream_t s) {
   const int n_qg = (a.nq + kGfThreads - 1) / kGfThreads;
   const int64_t n_pt = (p.local + kGfTile - 1) / kGfTile;
   // ~2 full waves of resident blocks (6 blocks/SM: 34 KB smem, 256 threads)
@@ -238,7 +264,7 @@ cudaError_t launch_gf_jp(Pool& p, const MatchArgs& a, int32_t cap, float* out_s,
   if (e != cudaSuccess) return e;
   if (p.local > 0) {
     gate_scan_kernel<JP><<<dim3(n_qg, S), kGfThreads, 0, s>>>(p.joints, p.local, p.q_joints, a.nq, S, a.g2, cap,
-                                                                p.gf_cnt, p.gf_cand);
+                                                                p.gf_cnt, p.gf_cand, sorted ? 1 : 0);
     ++p.launches;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
@@ -249,7 +275,7 @@ cudaError_t launch_gf_jp(Pool& p, const MatchArgs& a, int32_t cap, float* out_s,
   score_kernel<KT_, JP><<<g, wpb * 32, 0, s>>>(static_cast<const uint16_t*>(p.emb), p.inv_norm, p.joints, p.local, \
                                                static_cast<const uint16_t*>(p.q_stage), p.q_inv, p.q_joints, c.dim, \
                                                a.nq, a.k, a.g2, cap, p.gf_cnt, p.gf_cand, out_s, out_i, out_hit,    \
-                                               a.threshold, c.rank, c.world, p.B)
+                                               a.threshold, c.rank, c.world, p.B, sorted ? p.q_perm : nullptr)
   switch (a.KT) {
     case 8: AMS_GF(8); break;
     case 16: AMS_GF(16); break;
@@ -264,12 +290,12 @@ cudaError_t launch_gf_jp(Pool& p, const MatchArgs& a, int32_t cap, float* out_s,
 }  // namespace
 
 cudaError_t launch_gate_first(Pool& p, const MatchArgs& a, float* out_s, int64_t* out_i, uint8_t* out_hit,
-                              cudaStream_t s) {
+                              bool sorted, cudaStream_t s) {
   const int32_t cap = p.gf_cap;
   switch (p.JP) {
-    case 4: return launch_gf_jp<4>(p, a, cap, out_s, out_i, out_hit, s);
-    case 8: return launch_gf_jp<8>(p, a, cap, out_s, out_i, out_hit, s);
-    default: return launch_gf_jp<16>(p, a, cap, out_s, out_i, out_hit, s);
+    case 4: return launch_gf_jp<4>(p, a, cap, out_s, out_i, out_hit, sorted, s);
+    case 8: return launch_gf_jp<8>(p, a, cap, out_s, out_i, out_hit, sorted, s);
+    default: return launch_gf_jp<16>(p, a, cap, out_s, out_i, out_hit, sorted, s);
   }
 }
 

@@ -168,8 +168,9 @@ cudaError_t launch_merge_shards(Pool& p, const MatchArgs& a, int32_t G, int32_t 
 cudaError_t launch_merge_lists(const MatchArgs& a, int32_t G, int32_t kin, const float* in_s, const int64_t* in_i,
                                float* out_s, int64_t* out_i, uint8_t* out_hit, cudaStream_t s);
 // gate-first sparse variant (bf16 pools): writes [nq][k] (+hit if out_hit)
+// sorted: queries were staged through p.q_perm (outputs land at the caller's query index)
 cudaError_t launch_gate_first(Pool& p, const MatchArgs& a, float* out_s, int64_t* out_i, uint8_t* out_hit,
-                              cudaStream_t s);
+                              bool sorted, cudaStream_t s);
 cudaError_t launch_exchange_push(int KT, const float* ps, const int32_t* pi, int32_t nq, int32_t P, int32_t k,
                                  const PeerTable& pt, unsigned long long epoch, unsigned int* done, int32_t world_ids,
                                  int64_t B, cudaStream_t s);

@@ -118,3 +118,28 @@ def test_sorted_matches_unsorted_batches(ams):
     check_bf16(*whole, orc, 0.95)
     for i in range(3):
         np.testing.assert_array_equal(whole[i], np.concatenate([p[i] for p in parts]))
+
+
+@pytest.mark.parametrize("J,M,nq,spread,gamma", [
+    (1, 3001, 129, 1.0, 0.05),
+    (7, 4097, 777, 0.4, 0.3),
+    (14, 2600, 2048, 0.15, 0.35),
+    (7, 20000, 4100, 3.14159, 0.3),
+])
+def test_sorted_gate_first(ams, J, M, nq, spread, gamma):
+    """The gate-first variant takes the same joint-0 order (warp-level row test in
+    gate_scan_kernel, outputs scattered back by score_kernel)."""
+    rng = np.random.default_rng(2000 + J + nq)
+    d = 128
+    pe = emb_bits(rng, M, d)
+    pj = rng.uniform(-spread, spread, (M, J)).astype(np.float32)
+    src = rng.integers(0, M, nq // 2)
+    q = np.concatenate([near_dups(rng, pe[src], 0.05 / np.sqrt(d)), emb_bits(rng, nq - nq // 2, d)])
+    qj = np.concatenate([pj[src] + rng.normal(0, 0.02, (src.size, J)).astype(np.float32),
+                         rng.uniform(-spread, spread, (nq - nq // 2, J)).astype(np.float32)])
+    orc = oracle.match(pe, pj, q, qj, 10, 0.9, gamma)
+    with ams.Pool(d, J, M, nq, 10) as pool:
+        pool.append(torch.from_numpy(pe).cuda(), torch.from_numpy(pj).cuda())
+        g = [t.cpu().numpy() for t in pool.match(torch.from_numpy(q).cuda(), torch.from_numpy(qj).cuda(), 10, 0.9,
+                                                 gamma, gate_first=True)]
+    check_bf16(*g, orc, 0.9)
