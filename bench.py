@@ -499,7 +499,8 @@ def main():
                 "kernel": "match_tc_kernel (tcgen05 GEMM + fused gate/top-k epilogue)",
                 "algorithmic_per_launch": {"flop": flops_launch, "bytes": bytes_step / world},
                 "kernel_ms_avg": kern_avg, "kernel_share_of_step": kern_avg / (t_ms / args.steps),
-                "peak_source": f"MEASURED_PEAKS.json bf16_tflops (burst; {peaks['source']})",
+                "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)" if peaks["source"] == "measured"
+                else "fallback 1590 TF burst (B200_PROFILING.md; MEASURED_PEAKS.json absent)",
                 "frac_vs_sustained": achieved_tf / peaks["bf16_tflops_sustained"]
                 if peaks.get("bf16_tflops_sustained") else None,
                 "frac_vs_datasheet_2250": achieved_tf / 2250.0}
@@ -542,6 +543,8 @@ def main():
                 "pool_scan_gbps_per_gpu": (bytes_step / world) / (s_ms / 1e3) / 1e9,
                 "roofline": {"bound": "hbm", "achieved": gbs_kernel, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                              "frac": gbs_kernel / peaks["hbm_gbs"],
+                             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks["source"] == "measured"
+                             else "fallback 6650 GB/s (B200_PROFILING.md; MEASURED_PEAKS.json absent)",
                              "traffic": load_traffic(args.workload, "match_tc_scan"),
                              "kernel_ms_avg": k_avg, "frac_vs_datasheet_8000": gbs_kernel / 8000.0,
                              "algorithmic_bytes_per_launch": bytes_step / world}}
