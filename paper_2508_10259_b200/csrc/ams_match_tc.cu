@@ -116,8 +116,8 @@ __device__ __forceinline__ float4 lds4(const float* p) { return *reinterpret_cas
 template <int KT, int JP, bool GATED>
 __device__ __forceinline__ void epi_chunk(uint32_t taddr, int64_t jbase, int nvalid,
                                           const float* __restrict__ inv_sm, const float* __restrict__ jsm,
-                                          const uint64_t (&QQ)[4], const float (&qj)[JP], uint64_t IQ2, float iq,
-                                          float g2, float bound, int k, TopK<KT, int32_t>& top) {
+                                          const uint64_t (&QQ)[4], const float (&qj)[JP], float iq, float ie_min,
+                                          float ie_max, float g2, float bound, int k, TopK<KT, int32_t>& top) {
   constexpr int JF = JP < 4 ? JP : 4;   // joints in the filter
   uint32_t fire = 0;                    // bit sub: some column of sub-chunk sub may be admitted
   if (GATED) {
@@ -151,24 +151,24 @@ __device__ __forceinline__ void epi_chunk(uint32_t taddr, int64_t jbase, int nva
       fire |= (mn <= g2 ? 1u : 0u) << sub;
     }
   } else {
+    // Upper bound of the 8 scores of a sub-chunk from the raw maximum: with
+    // m = RN(max_c acc_c * iq), every s_c = RN(RN(acc_c * iq) * ie_c) is <= RN(m * ie_max)
+    // when m >= 0 and <= RN(m * ie_min) when m < 0 (iq, ie >= 0; RN is monotone), where
+    // ie_min/ie_max bound the tile's inverse norms.  0.5 FMNMX3 per column instead of
+    // scaling every score.
     uint32_t v[32];
     ptx::tmem_ld32(taddr, v);
     ptx::tmem_wait_ld();
 #pragma unroll
     for (int sub = 0; sub < 4; ++sub) {
-      float mx = -CUDART_INF_F;
-#pragma unroll
-      for (int c4 = 2 * sub; c4 < 2 * sub + 2; ++c4) {
-        const float4 ie = lds4(inv_sm + 4 * c4);
-        const uint64_t a =
-            ptx::mul2(ptx::mul2(ptx::pack2(__uint_as_float(v[4 * c4]), __uint_as_float(v[4 * c4 + 1])), IQ2),
-                      ptx::pack2(ie.x, ie.y));
-        const uint64_t b =
-            ptx::mul2(ptx::mul2(ptx::pack2(__uint_as_float(v[4 * c4 + 2]), __uint_as_float(v[4 * c4 + 3])), IQ2),
-                      ptx::pack2(ie.z, ie.w));
-        mx = fmaxf(mx, fmaxf(fmaxf(ptx::lo2(a), ptx::hi2(a)), fmaxf(ptx::lo2(b), ptx::hi2(b))));
-      }
-      fire |= (mx > top.kth_s && mx >= bound ? 1u : 0u) << sub;
+#define AMS_V(c) __uint_as_float(v[8 * sub + (c)])
+      const float mv = fmaxf(ptx::fmax3(ptx::fmax3(AMS_V(0), AMS_V(1), AMS_V(2)), ptx::fmax3(AMS_V(3), AMS_V(4), AMS_V(5)),
+                                        AMS_V(6)),
+                             AMS_V(7));
+#undef AMS_V
+      const float m = __fmul_rn(mv, iq);
+      const float ub = __fmul_rn(m, m >= 0.0f ? ie_max : ie_min);
+      fire |= (ub > top.kth_s && ub >= bound ? 1u : 0u) << sub;
     }
   }
   uint32_t wfire = __reduce_or_sync(0xffffffffu, fire);
@@ -432,7 +432,6 @@ __global__ void __maxnreg__(168)
 #pragma unroll
       for (int t = 0; t < 4; ++t) QQ[t] = ptx::pack2(qj[t], qj[t]);   // JP >= 4
       const float iq = active ? prm.inv_q[qrow] : 0.0f;
-      const uint64_t IQ2 = ptx::pack2(iq, iq);
       // joint-0 interval of the warp's active queries (empty warp: +inf/-inf, no column passes)
       float wlo = active ? qj[0] : CUDART_INF_F, whi = active ? qj[0] : -CUDART_INF_F;
 #pragma unroll
@@ -459,6 +458,17 @@ __global__ void __maxnreg__(168)
         const uint8_t* aux = sAux + buf * AUX;
         const float* joints_sm = reinterpret_cast<const float*>(aux);
         const float* inv_sm = reinterpret_cast<const float*>(aux + AUXJ);
+        float ie_min = 0.0f, ie_max = 0.0f;   // inverse-norm range of this warp's column half
+        if (!gated) {
+          const float4 a = lds4(inv_sm + h * kColsPerHalf + 4 * lane);
+          ie_min = fminf(fminf(a.x, a.y), fminf(a.z, a.w));
+          ie_max = ptx::fmax3(a.x, a.y, fmaxf(a.z, a.w));
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            ie_min = fminf(ie_min, __shfl_xor_sync(0xffffffffu, ie_min, o));
+            ie_max = fmaxf(ie_max, __shfl_xor_sync(0xffffffffu, ie_max, o));
+          }
+        }
 #pragma unroll 1
         for (int ch = 0; ch < kColsPerHalf / kChunk; ++ch) {
           const int col0 = h * kColsPerHalf + ch * kChunk;
@@ -472,10 +482,10 @@ __global__ void __maxnreg__(168)
                                                  prm.g2, bound, prm.k, wlo, whi, lane, top))
             continue;
           if (gated)
-            epi_chunk<KT, JP, true>(taddr, jbase, nvalid, inv_sm + col0, joints_sm + col0, QQ, qj, IQ2, iq,
+            epi_chunk<KT, JP, true>(taddr, jbase, nvalid, inv_sm + col0, joints_sm + col0, QQ, qj, iq, ie_min, ie_max,
                                     prm.g2, bound, prm.k, top);
           else
-            epi_chunk<KT, JP, false>(taddr, jbase, nvalid, inv_sm + col0, joints_sm + col0, QQ, qj, IQ2, iq,
+            epi_chunk<KT, JP, false>(taddr, jbase, nvalid, inv_sm + col0, joints_sm + col0, QQ, qj, iq, ie_min, ie_max,
                                      prm.g2, bound, prm.k, top);
         }
         ptx::tc_fence_before();
