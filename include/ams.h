@@ -113,6 +113,10 @@ ams_status_t ams_pool_append(ams_pool_t pool, const void* emb, const float* join
  *   out_hit[i]          1 iff out_index[i,0] >= 0 and out_score[i,0] >= threshold
  * Outputs are DEVICE buffers: out_index int64 [nq, k], out_score fp32 [nq, k],
  * out_hit uint8 [nq].  With world > 1 every rank receives identical outputs.
+ * Host-resident q_emb / q_joints are copied on a pool-internal copy stream into one of
+ * two staging buffers and `stream` waits for that copy only, so the H2D of one call
+ * overlaps the kernels still running from the previous call on `stream`; the host
+ * buffers must stay valid (and unmodified) until `stream` reaches this call.
  * Errors: AMS_ERR_INVALID_ARGUMENT (null pool/pointers, nq < 1 or > max_queries,
  * k < 1 or > max_k, NaN threshold, NaN or negative gate_radius), AMS_ERR_CUDA,
  * AMS_ERR_NCCL.  k larger than the pool is legal (padded). */

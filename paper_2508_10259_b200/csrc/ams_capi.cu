@@ -147,8 +147,15 @@ void free_peers(Pool& p) {
 
 void free_all(Pool& p) {
   free_peers(p);
-  void* ptrs[] = {p.emb, p.inv_norm, p.joints, p.q_stage, p.q_inv, p.q_joints, p.q_joints_raw, p.q_raw, p.q_perm,
-                  p.bound,
+  for (int b = 0; b < 2; ++b) {
+    if (p.staged[b]) cudaEventDestroy(p.staged[b]);
+    if (p.consumed[b]) cudaEventDestroy(p.consumed[b]);
+    p.staged[b] = p.consumed[b] = nullptr;
+  }
+  if (p.copy_stream) cudaStreamDestroy(p.copy_stream);
+  p.copy_stream = nullptr;
+  void* ptrs[] = {p.emb, p.inv_norm, p.joints, p.q_stage, p.q_inv, p.q_joints, p.q_joints_raw[0], p.q_joints_raw[1],
+                  p.q_raw[0], p.q_raw[1], p.q_perm, p.bound,
                   p.gf_cnt, p.gf_cand,
                   p.part_s, p.part_i, p.shard_s, p.shard_i, p.gath_s, p.gath_i, p.stage_emb,
                   p.stage_joints};
@@ -279,8 +286,10 @@ ams_status_t ams_pool_create(const ams_pool_config_t* cfg, ams_pool_t* out) {
             alloc((void**)&p.joints, (size_t)p.cap_pad * p.JP * 4) &&
             alloc(&p.q_stage, (size_t)p.q_pad * d * es) && alloc((void**)&p.q_inv, (size_t)p.q_pad * 4) &&
             alloc((void**)&p.q_joints, (size_t)p.q_pad * p.JP * 4) &&
-            alloc((void**)&p.q_joints_raw, (size_t)c.max_queries * c.joint_dim * 4) &&
-            alloc(&p.q_raw, (size_t)c.max_queries * d * es) && alloc((void**)&p.q_perm, (size_t)p.q_pad * 4) &&
+            alloc((void**)&p.q_joints_raw[0], (size_t)c.max_queries * c.joint_dim * 4) &&
+            alloc((void**)&p.q_joints_raw[1], (size_t)c.max_queries * c.joint_dim * 4) &&
+            alloc(&p.q_raw[0], (size_t)c.max_queries * d * es) && alloc(&p.q_raw[1], (size_t)c.max_queries * d * es) &&
+            alloc((void**)&p.q_perm, (size_t)p.q_pad * 4) &&
             alloc((void**)&p.bound, (size_t)(p.q_pad + 32) * 4) &&
             alloc((void**)&p.part_s, (size_t)part * 4) && alloc((void**)&p.part_i, (size_t)part * 4) &&
             alloc((void**)&p.shard_s, (size_t)c.max_queries * c.max_k * 4) &&
@@ -308,7 +317,12 @@ ams_status_t ams_pool_create(const ams_pool_config_t* cfg, ams_pool_t* out) {
       return AMS_ERR_CUDA;
     }
   }
-  if (cudaDeviceSynchronize() != cudaSuccess) {
+  bool sok = cudaStreamCreateWithFlags(&p.copy_stream, cudaStreamNonBlocking) == cudaSuccess;
+  for (int b = 0; b < 2 && sok; ++b)
+    sok = cudaEventCreateWithFlags(&p.staged[b], cudaEventDisableTiming) == cudaSuccess &&
+          cudaEventCreateWithFlags(&p.consumed[b], cudaEventDisableTiming) == cudaSuccess;
+  if (!sok || cudaDeviceSynchronize() != cudaSuccess) {
+    cudaGetLastError();
     free_all(p);
     delete pool;
     return AMS_ERR_CUDA;
@@ -387,17 +401,30 @@ static ams_status_t match_impl(ams_pool_t pool, const void* q_emb, const float* 
   a.gated = std::isinf(a.g2) ? 0 : 1;
   a.threshold = threshold;
 
-  // stage queries (host sources are copied first; device sources are read in place)
+  // stage queries: device sources are read in place; host sources are copied on the
+  // pool's copy stream into staging buffer b (free once the prep of two calls ago has
+  // read it), and s waits only for that copy -- the H2D of this call overlaps whatever
+  // s is still running from the previous one.
   const size_t es = esize(p);
   const void* q_src = q_emb;
   const float* qj_src = q_joints;
-  if (!is_device_ptr(q_emb)) {
-    AMS_CUDA_TRY(cudaMemcpyAsync(p.q_raw, q_emb, (size_t)nq * p.cfg.dim * es, cudaMemcpyDefault, s));
-    q_src = p.q_raw;
-  }
-  if (!is_device_ptr(q_joints)) {
-    AMS_CUDA_TRY(cudaMemcpyAsync(p.q_joints_raw, q_joints, (size_t)nq * p.cfg.joint_dim * 4, cudaMemcpyDefault, s));
-    qj_src = p.q_joints_raw;
+  const bool host_q = !is_device_ptr(q_emb), host_j = !is_device_ptr(q_joints);
+  int b = -1;
+  if (host_q || host_j) {
+    b = p.stage_buf;
+    p.stage_buf ^= 1;
+    AMS_CUDA_TRY(cudaStreamWaitEvent(p.copy_stream, p.consumed[b], 0));
+    if (host_q) {
+      AMS_CUDA_TRY(cudaMemcpyAsync(p.q_raw[b], q_emb, (size_t)nq * p.cfg.dim * es, cudaMemcpyDefault, p.copy_stream));
+      q_src = p.q_raw[b];
+    }
+    if (host_j) {
+      AMS_CUDA_TRY(cudaMemcpyAsync(p.q_joints_raw[b], q_joints, (size_t)nq * p.cfg.joint_dim * 4, cudaMemcpyDefault,
+                                   p.copy_stream));
+      qj_src = p.q_joints_raw[b];
+    }
+    AMS_CUDA_TRY(cudaEventRecord(p.staged[b], p.copy_stream));
+    AMS_CUDA_TRY(cudaStreamWaitEvent(s, p.staged[b], 0));
   }
   // Gated tcgen05 batches are staged in joint-0 order (the epilogue's warp-level gate
   // test then rejects most columns for all 32 queries of a warp at once).  The order is
@@ -405,6 +432,7 @@ static ams_status_t match_impl(ams_pool_t pool, const void* q_emb, const float* 
   const bool sorted = p.cfg.dtype == AMS_DTYPE_BF16 && a.gated && p.local > 0 && nq >= kSortMinQueries;
   if (sorted) AMS_CUDA_TRY(ams::launch_query_order(p, qj_src, nq, s));
   AMS_CUDA_TRY(ams::launch_query_prep(p, q_src, qj_src, nq, sorted ? p.q_perm : nullptr, s));
+  if (b >= 0) AMS_CUDA_TRY(cudaEventRecord(p.consumed[b], s));   // staging b read (order + prep)
 
   const bool multi = p.cfg.world > 1;
   float* shard_s = multi ? p.shard_s : out_score;

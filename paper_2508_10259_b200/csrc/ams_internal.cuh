@@ -84,8 +84,14 @@ struct Pool {
   void* q_stage = nullptr;    // [q_pad, d]
   float* q_inv = nullptr;     // [q_pad]
   float* q_joints = nullptr;  // [q_pad, JP]
-  float* q_joints_raw = nullptr;  // [max_queries, J] host-staged joints
-  void* q_raw = nullptr;      // [max_queries, d] host-staged query rows (gathered into q_stage)
+  // host-sourced queries: double-buffered staging filled on copy_stream, so the H2D of
+  // call i+1 overlaps the kernels of call i (staged[b] / consumed[b] order the reuse)
+  float* q_joints_raw[2] = {nullptr, nullptr};  // [max_queries, J]
+  void* q_raw[2] = {nullptr, nullptr};          // [max_queries, d], gathered into q_stage
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t staged[2] = {nullptr, nullptr};
+  cudaEvent_t consumed[2] = {nullptr, nullptr};
+  int32_t stage_buf = 0;
   int32_t* q_perm = nullptr;  // [q_pad] staged position -> caller's query (joint-0 order)
 
   // partial top-k lists [nq][P][KT]

@@ -143,3 +143,26 @@ def test_sorted_gate_first(ams, J, M, nq, spread, gamma):
         g = [t.cpu().numpy() for t in pool.match(torch.from_numpy(q).cuda(), torch.from_numpy(qj).cuda(), 10, 0.9,
                                                  gamma, gate_first=True)]
     check_bf16(*g, orc, 0.9)
+
+
+def test_host_staging_pipeline(ams):
+    """Back-to-back calls with host inputs and no synchronisation in between: the
+    double-buffered staging (copy stream + events) must hand every call its own
+    queries.  Mixed sizes exercise both the sorted (>= 129) and plain staging."""
+    rng = np.random.default_rng(21)
+    M, d, J = 3000, 128, 7
+    pe = emb_bits(rng, M, d)
+    pj = rng.uniform(-0.5, 0.5, (M, J)).astype(np.float32)
+    sizes = [300, 64, 1000, 129, 5, 777]
+    qs = [emb_bits(rng, n, d) for n in sizes]
+    qjs = [rng.uniform(-0.5, 0.5, (n, J)).astype(np.float32) for n in sizes]
+    with ams.Pool(d, J, M, max(sizes), 10) as pool:
+        pool.append(torch.from_numpy(pe).cuda(), torch.from_numpy(pj).cuda())
+        torch.cuda.synchronize()
+        hq = [torch.from_numpy(q).pin_memory() for q in qs]
+        hj = [torch.from_numpy(j).pin_memory() for j in qjs]
+        outs = [pool.match(a, b, 10, 0.9, 0.3) for a, b in zip(hq, hj)]
+        torch.cuda.synchronize()
+    for q, qj, o in zip(qs, qjs, outs):
+        orc = oracle.match(pe, pj, q, qj, 10, 0.9, 0.3)
+        check_bf16(*[t.cpu().numpy() for t in o], orc, 0.9)
