@@ -155,7 +155,7 @@ void free_all(Pool& p) {
   if (p.copy_stream) cudaStreamDestroy(p.copy_stream);
   p.copy_stream = nullptr;
   void* ptrs[] = {p.emb, p.inv_norm, p.joints, p.q_stage, p.q_inv, p.q_joints, p.q_joints_raw[0], p.q_joints_raw[1],
-                  p.q_raw[0], p.q_raw[1], p.q_perm, p.bound,
+                  p.q_raw[0], p.q_raw[1], p.q_perm, p.bound, p.slots,
                   p.gf_cnt, p.gf_cand,
                   p.part_s, p.part_i, p.shard_s, p.shard_i, p.gath_s, p.gath_i, p.stage_emb,
                   p.stage_joints};
@@ -291,6 +291,7 @@ ams_status_t ams_pool_create(const ams_pool_config_t* cfg, ams_pool_t* out) {
             alloc(&p.q_raw[0], (size_t)c.max_queries * d * es) && alloc(&p.q_raw[1], (size_t)c.max_queries * d * es) &&
             alloc((void**)&p.q_perm, (size_t)p.q_pad * 4) &&
             alloc((void**)&p.bound, (size_t)(p.q_pad + 32) * 4) &&
+            alloc((void**)&p.slots, (size_t)p.q_pad * p.KT_max * 4) &&
             alloc((void**)&p.part_s, (size_t)part * 4) && alloc((void**)&p.part_i, (size_t)part * 4) &&
             alloc((void**)&p.shard_s, (size_t)c.max_queries * c.max_k * 4) &&
             alloc((void**)&p.shard_i, (size_t)c.max_queries * c.max_k * 8) &&

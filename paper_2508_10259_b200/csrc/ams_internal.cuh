@@ -112,6 +112,7 @@ struct Pool {
   float* stage_joints = nullptr;
 
   uint32_t* bound = nullptr;  // [q_pad] per-query admission lower bound (tcgen05 path)
+  uint32_t* slots = nullptr;  // [q_pad][KT_max] union-bound slots (tcgen05 path, ungated)
 
   // gate-first variant: per-query candidate buckets
   int32_t gf_cap = 0;

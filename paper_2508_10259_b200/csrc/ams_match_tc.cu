@@ -52,6 +52,20 @@ __device__ __forceinline__ unsigned int __smid() {
 }
 #endif
 
+#ifdef AMS_DIAG_COUNT   // diagnostic builds only: [0] chunks, [1] firing sub-chunks, [2] inserts
+__device__ unsigned long long g_diag_cnt[4];
+#define AMS_COUNT(i, v)                                                                 \
+  do {                                                                                  \
+    const unsigned long long v_ = (unsigned long long)(v);                              \
+    if ((threadIdx.x & 31) == 0) atomicAdd(&g_diag_cnt[i], v_);                         \
+    __syncwarp();                                                                       \
+  } while (0)
+#else
+#define AMS_COUNT(i, v) \
+  do {                   \
+  } while (0)
+#endif
+
 namespace {
 
 constexpr int kThreadsTc = 64 + 128 * kEpiHalves;   // 320
@@ -79,6 +93,7 @@ struct TcParams {
   uint32_t* bound;           // [nq] per-query admission lower bound (ordered-u32; 0 = none)
   uint32_t* wave_ctr;        // producers' unit-completion counter (zeroed per launch; bound[nq])
   const int32_t* perm;       // staged query position -> caller's query (nullptr: identity)
+  uint32_t* slots;           // [q_pad][KT] union-bound slots (ordered-u32; ungated only, else null)
   int64_t L;                 // local rows
   int32_t nq, d, n_qt, n_pt, S, n_units, k, gated, P;
   int32_t sorted;            // queries staged in joint-0 order: the warp-level column test pays
@@ -172,6 +187,8 @@ __device__ __forceinline__ void epi_chunk(uint32_t taddr, int64_t jbase, int nva
     }
   }
   uint32_t wfire = __reduce_or_sync(0xffffffffu, fire);
+  AMS_COUNT(0, 1);
+  AMS_COUNT(1, __popc(wfire));
   // exact path (rare), sub-chunk by sub-chunk; tcgen05.ld is warp-collective and the
   // loop is warp-uniform
   while (wfire != 0u) {
@@ -198,6 +215,7 @@ __device__ __forceinline__ void epi_chunk(uint32_t taddr, int64_t jbase, int nva
           ok = ok && (ds <= g2);
         }
       }
+      AMS_COUNT(2, __popc(__ballot_sync(0xffffffffu, ok)));
       if (ok) top.insert_monotone(s, (int32_t)(jbase + cc), k);
     }
   }
@@ -504,6 +522,21 @@ __global__ void __maxnreg__(168)
             if (top.kth_s > -CUDART_INF_F) atomicMax(bnd, ptx::f2ord(top.kth_s));
             const uint32_t b = *reinterpret_cast<volatile uint32_t*>(bnd);
             if (b) bound = fmaxf(bound, ptx::ord2f(b));
+            if (prm.slots != nullptr) {
+              // union bound: list l keeps its best score in slot l mod k; slots hold
+              // rows of disjoint list groups, so with all k slots filled their minimum
+              // is the score of one of k distinct rows, <= the k-th best of the pool
+              uint32_t* sl = prm.slots + (int64_t)qrow * KT;
+              if (top.s[0] > -CUDART_INF_F) atomicMax(sl + (sp * kEpiHalves + h) % prm.k, ptx::f2ord(top.s[0]));
+              uint32_t mn = 0xFFFFFFFFu;
+#pragma unroll
+              for (int r = 0; r < KT; r += 4) {
+                const uint4 v = __ldcg(reinterpret_cast<const uint4*>(sl + r));
+                mn = min(mn, min(min(r < prm.k ? v.x : ~0u, r + 1 < prm.k ? v.y : ~0u),
+                                 min(r + 2 < prm.k ? v.z : ~0u, r + 3 < prm.k ? v.w : ~0u)));
+              }
+              if (mn != 0u) bound = fmaxf(bound, ptx::ord2f(mn));
+            }
           }
         }
       }
@@ -599,12 +632,29 @@ cudaError_t launch_match_tc(Pool& p, const MatchArgs& a, int32_t S, int32_t grid
   prm.g2 = a.g2;
   cudaError_t e = cudaMemsetAsync(p.bound, 0, (size_t)(a.nq + 1) * sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
+  // ungated: the union bound needs >= k lists per query (each list fills one slot)
+  prm.slots = (!a.gated && prm.P >= a.k) ? p.slots : nullptr;
+  if (prm.slots != nullptr) {
+    e = cudaMemsetAsync(p.slots, 0, (size_t)prm.n_qt * kBlockM * cg * a.KT * sizeof(uint32_t), s);
+    if (e != cudaSuccess) return e;
+  }
   e = cg == 2 ? launch_tc_cg<2>(p, a, prm, grid, s) : launch_tc_cg<1>(p, a, prm, grid, s);
   ++p.launches;
   return e;
 }
 
 }  // namespace ams
+
+#ifdef AMS_DIAG_COUNT
+extern "C" int ams_diag_counts(unsigned long long* host, int reset) {
+  int e = (int)cudaMemcpyFromSymbol(host, ams::g_diag_cnt, 4 * 8);
+  if (reset) {
+    unsigned long long z[4] = {0, 0, 0, 0};
+    cudaMemcpyToSymbol(ams::g_diag_cnt, z, sizeof z);
+  }
+  return e;
+}
+#endif
 
 #ifdef AMS_DIAG_TIMELINE
 extern "C" int ams_diag_timeline(unsigned long long* host, int n_units) {
