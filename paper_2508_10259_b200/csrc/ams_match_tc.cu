@@ -194,6 +194,7 @@ __device__ __forceinline__ void epi_chunk(uint32_t taddr, int64_t jbase, int nva
   while (wfire != 0u) {
     const int sub = __ffs(wfire) - 1;
     wfire &= wfire - 1u;
+    __syncwarp();   // tcgen05.ld is .sync.aligned: reconverge after the previous inserts
     uint32_t v8[8];
     ptx::tmem_ld8(taddr + (uint32_t)(sub * 8), v8);
     ptx::tmem_wait_ld();
