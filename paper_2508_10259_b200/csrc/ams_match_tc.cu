@@ -172,6 +172,7 @@ __device__ __forceinline__ void epi_chunk(uint32_t taddr, int64_t jbase, int nva
     // ie_min/ie_max bound the tile's inverse norms.  0.5 FMNMX3 per column instead of
     // scaling every score.
     uint32_t v[32];
+    __syncwarp();
     ptx::tmem_ld32(taddr, v);
     ptx::tmem_wait_ld();
 #pragma unroll
