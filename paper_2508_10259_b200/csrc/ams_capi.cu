@@ -517,7 +517,8 @@ static ams_status_t match_impl(ams_pool_t pool, const void* q_emb, const float* 
     return AMS_OK;
   }
   if (!(gate_first && p.cfg.dtype == AMS_DTYPE_BF16))
-    AMS_CUDA_TRY(ams::launch_merge_partials(p, a, P, shard_s, shard_i, shard_hit, s));
+    AMS_CUDA_TRY(ams::launch_merge_partials(p, a, P, shard_s, shard_i, shard_hit,
+                                            p.cfg.dtype == AMS_DTYPE_BF16 && p.local > 0, s));
 
   if (multi) {
     ncclComm_t comm = static_cast<ncclComm_t>(p.nccl_comm);

@@ -165,8 +165,10 @@ cudaError_t launch_match_tc(Pool& p, const MatchArgs& a, int32_t splits, int32_t
                             cudaStream_t s);
 int tc_query_tile(int cg);
 // merge [nq][P][KT] local lists -> [nq][k] (fp32, global int64); writes hit if out_hit != null
+// tc_bounds: the lists come from launch_match_tc, whose per-query lower bounds (p.bound,
+// p.slots) prune entries that cannot reach the top k
 cudaError_t launch_merge_partials(Pool& p, const MatchArgs& a, int32_t P, float* out_s, int64_t* out_i,
-                                  uint8_t* out_hit, cudaStream_t s);
+                                  uint8_t* out_hit, bool tc_bounds, cudaStream_t s);
 // merge [G][nq][kin] global lists -> [nq][k] + hit
 cudaError_t launch_merge_shards(Pool& p, const MatchArgs& a, int32_t G, int32_t kin, const float* in_s,
                                 const int64_t* in_i, float* out_s, int64_t* out_i, uint8_t* out_hit,

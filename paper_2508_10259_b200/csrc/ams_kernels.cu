@@ -4,6 +4,7 @@
 #include <math_constants.h>
 
 #include "ams_internal.cuh"
+#include "ams_ptx.cuh"
 #include "ams_topk.cuh"
 
 namespace ams {
@@ -253,6 +254,13 @@ __device__ __forceinline__ void warp_emit(TopK<KT, I>& t, int k, int lane, float
   float s0 = -CUDART_INF_F;
   int64_t i0 = -1;
   for (int r = 0; r < k; ++r) {
+    if (!__any_sync(0xffffffffu, t.i[0] >= 0)) {   // every list exhausted: pad the rest
+      for (int rr = r + lane; rr < k; rr += 32) {
+        out_s[rr] = -CUDART_INF_F;
+        out_i[rr] = -1;
+      }
+      break;
+    }
     float bs = t.s[0];
     I bi = t.i[0];
     int bl = lane;
@@ -282,23 +290,67 @@ __device__ __forceinline__ void warp_emit(TopK<KT, I>& t, int k, int lane, float
   if (out_hit != nullptr && lane == 0) *out_hit = (i0 >= 0 && s0 >= threshold) ? 1 : 0;
 }
 
+// Lower bound of query q's k-th best score left by the tcgen05 kernel (ordered-u32, 0 =
+// none): the max over lists of their KT-th best, and -- when every one of the k union
+// slots is filled -- the minimum slot (k distinct rows score at least that much).  Rows
+// scoring below it cannot be among the k best; equal scores are kept for the tie rule.
+__device__ __forceinline__ float tc_lower_bound(const uint32_t* __restrict__ bound, const uint32_t* __restrict__ slots,
+                                                int32_t slot_stride, int32_t k, int q) {
+  float b = -CUDART_INF_F;
+  if (bound != nullptr) {
+    const uint32_t u = bound[q];
+    if (u != 0u) b = ptx::ord2f(u);
+  }
+  if (slots != nullptr) {
+    uint32_t mn = 0xFFFFFFFFu;
+    for (int r = 0; r < k; ++r) mn = min(mn, slots[(int64_t)q * slot_stride + r]);
+    if (mn != 0u) b = fmaxf(b, ptx::ord2f(mn));
+  }
+  return b;
+}
+
 template <int KT>
 __global__ void merge_partials_kernel(const float* __restrict__ part_s, const int32_t* __restrict__ part_i,
                                       int32_t nq, int32_t P, int32_t k, float* __restrict__ out_s,
                                       int64_t* __restrict__ out_i, uint8_t* __restrict__ out_hit,
-                                      float threshold, int32_t rank, int32_t world, int64_t B) {
+                                      float threshold, int32_t rank, int32_t world, int64_t B,
+                                      const uint32_t* __restrict__ bound, const uint32_t* __restrict__ slots,
+                                      int32_t slot_stride) {
   const int lane = threadIdx.x & 31;
   const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (q >= nq) return;
+  const float lb = tc_lower_bound(bound, slots, slot_stride, k, q);
   TopK<KT, int32_t> t;
   t.init(true);
-  for (int p = lane; p < P; p += 32) {
-    const int64_t base = ((int64_t)q * P + p) * KT;
-    for (int r = 0; r < k; ++r) {
-      const int32_t j = part_i[base + r];
-      const float v = part_s[base + r];
-      if (j < 0 || !better(v, j, t.kth_s, t.kth_i)) break;
-      t.insert(v, j, k);
+  // lists are sorted: walk each from its head while entries can still enter.  Heads are
+  // loaded kHeads lists at a time per lane so their loads are in flight together (most
+  // lists of a gated batch are empty).
+  constexpr int kHeads = 8;
+  for (int p0 = 0; p0 < P; p0 += 32 * kHeads) {
+    float hs[kHeads];
+    int32_t hj[kHeads];
+#pragma unroll
+    for (int u = 0; u < kHeads; ++u) {
+      const int p = p0 + u * 32 + lane;
+      hj[u] = -1;
+      hs[u] = -CUDART_INF_F;
+      if (p < P) {
+        const int64_t base = ((int64_t)q * P + p) * KT;
+        hj[u] = part_i[base];
+        hs[u] = part_s[base];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kHeads; ++u) {
+      if (hj[u] < 0 || hs[u] < lb || !better(hs[u], hj[u], t.kth_s, t.kth_i)) continue;
+      t.insert(hs[u], hj[u], k);
+      const int64_t base = ((int64_t)q * P + p0 + u * 32 + lane) * KT;
+      for (int r = 1; r < k; ++r) {
+        const int32_t j = part_i[base + r];
+        const float v = part_s[base + r];
+        if (j < 0 || v < lb || !better(v, j, t.kth_s, t.kth_i)) break;
+        t.insert(v, j, k);
+      }
     }
   }
   warp_emit(t, k, lane, out_s + (int64_t)q * k, out_i + (int64_t)q * k,
@@ -391,13 +443,15 @@ cudaError_t launch_match_simt(Pool& p, const MatchArgs& a, int32_t S, cudaStream
 }
 
 cudaError_t launch_merge_partials(Pool& p, const MatchArgs& a, int32_t P, float* out_s, int64_t* out_i,
-                                  uint8_t* out_hit, cudaStream_t s) {
+                                  uint8_t* out_hit, bool tc_bounds, cudaStream_t s) {
   const int wpb = 4;
   const auto& c = p.cfg;
   const unsigned g = blocks_for(a.nq, wpb);
+  const uint32_t* bnd = tc_bounds ? p.bound : nullptr;
+  const uint32_t* sl = (tc_bounds && !a.gated && P >= a.k) ? p.slots : nullptr;   // as launch_match_tc
 #define AMS_MERGE(KT_)                                                                                 \
   merge_partials_kernel<KT_><<<g, wpb * 32, 0, s>>>(p.part_s, p.part_i, a.nq, P, a.k, out_s, out_i, out_hit, \
-                                                     a.threshold, c.rank, c.world, p.B)
+                                                     a.threshold, c.rank, c.world, p.B, bnd, sl, a.KT)
   switch (a.KT) {
     case 8: AMS_MERGE(8); break;
     case 16: AMS_MERGE(16); break;

@@ -460,7 +460,9 @@ __global__ void __maxnreg__(168)
         whi = fmaxf(whi, __shfl_xor_sync(0xffffffffu, whi, o));
       }
       const bool sparse = gated && prm.sorted != 0;
-      uint32_t* bnd = prm.bound + (active ? qrow : 0);
+      // the caller's query index: partial lists, the bound and its slots are indexed by it
+      const int64_t qout = (active && prm.perm != nullptr) ? (int64_t)prm.perm[qrow] : (int64_t)qrow;
+      uint32_t* bnd = prm.bound + (active ? qout : 0);
       float bound = -CUDART_INF_F;
       if (active) {
         const uint32_t b = *reinterpret_cast<volatile uint32_t*>(bnd);
@@ -528,7 +530,7 @@ __global__ void __maxnreg__(168)
               // union bound: list l keeps its best score in slot l mod k; slots hold
               // rows of disjoint list groups, so with all k slots filled their minimum
               // is the score of one of k distinct rows, <= the k-th best of the pool
-              uint32_t* sl = prm.slots + (int64_t)qrow * KT;
+              uint32_t* sl = prm.slots + qout * KT;
               if (top.s[0] > -CUDART_INF_F) atomicMax(sl + (sp * kEpiHalves + h) % prm.k, ptx::f2ord(top.s[0]));
               uint32_t mn = 0xFFFFFFFFu;
 #pragma unroll
@@ -543,7 +545,6 @@ __global__ void __maxnreg__(168)
         }
       }
       if (active) {
-        const int64_t qout = prm.perm != nullptr ? (int64_t)prm.perm[qrow] : (int64_t)qrow;
         const int64_t base = (qout * prm.P + (int64_t)sp * kEpiHalves + h) * KT;
 #pragma unroll
         for (int r = 0; r < KT; r += 4) {
