@@ -78,7 +78,7 @@ bool is_device_ptr(const void* ptr) {
 
 int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
-// Smallest gated bf16 batch staged in joint-0 order (below it one warp's queries span
+// Smallest gated bf16 batch staged in (joint 0, joint 1) order (below it one warp's queries span
 // most of the joint range and the per-lane packed filter is cheaper).
 constexpr int32_t kSortMinQueries = 129;
 
@@ -427,7 +427,7 @@ static ams_status_t match_impl(ams_pool_t pool, const void* q_emb, const float* 
     AMS_CUDA_TRY(cudaEventRecord(p.staged[b], p.copy_stream));
     AMS_CUDA_TRY(cudaStreamWaitEvent(s, p.staged[b], 0));
   }
-  // Gated tcgen05 batches are staged in joint-0 order (the epilogue's warp-level gate
+  // Gated batches are staged in (joint 0, joint 1) order (the epilogue's warp-level gate
   // test then rejects most columns for all 32 queries of a warp at once).  The order is
   // invisible to the caller: partial lists land at the caller's query index.
   const bool sorted = p.cfg.dtype == AMS_DTYPE_BF16 && a.gated && p.local > 0 && nq >= kSortMinQueries;

@@ -52,12 +52,15 @@ __global__ void __launch_bounds__(kGfThreads)
 #pragma unroll
   for (int t = 0; t < 4; ++t) rq = fmaf(qj[t], qj[t], rq);
   const uint64_t M2 = ptx::pack2(-2.0f, -2.0f);
-  // joint-0 interval of the warp's active queries (see ams_match_tc.cu epi_chunk_sorted)
+  // joint-0 / joint-1 intervals of the warp's active queries (see ams_match_tc.cu epi_chunk_sorted)
   float wlo = active ? qj[0] : CUDART_INF_F, whi = active ? qj[0] : -CUDART_INF_F;
+  float wlo1 = active ? qj[1] : CUDART_INF_F, whi1 = active ? qj[1] : -CUDART_INF_F;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     wlo = fminf(wlo, __shfl_xor_sync(0xffffffffu, wlo, o));
     whi = fmaxf(whi, __shfl_xor_sync(0xffffffffu, whi, o));
+    wlo1 = fminf(wlo1, __shfl_xor_sync(0xffffffffu, wlo1, o));
+    whi1 = fmaxf(whi1, __shfl_xor_sync(0xffffffffu, whi1, o));
   }
   const int lane = threadIdx.x & 31;
   const int64_t n_pt = (L + kGfTile - 1) / kGfTile;
@@ -110,16 +113,34 @@ __global__ void __launch_bounds__(kGfThreads)
 #pragma unroll 1
     for (int c8 = 0; c8 < kGfTile / 8; ++c8) {
       if (sorted && (c8 & 3) == 0) {
-        // warp-level joint-0 test of the next 32 rows: a row whose joint 0 is farther
-        // than gamma from the warp's whole interval is ineligible for every lane
-        const float p0 = jsm[8 * c8 + lane];
+        // warp-level two-joint test of the next 32 rows (ams_match_tc.cu
+        // epi_chunk_sorted): ineligible for every lane when it fails
+        const float p0 = jsm[8 * c8 + lane], p1 = jsm[kGfTile + 8 * c8 + lane];
         const float d0 = p0 < wlo ? __fsub_rn(wlo, p0) : (p0 > whi ? __fsub_rn(whi, p0) : 0.0f);
-        uint32_t m = __ballot_sync(0xffffffffu, __fmul_rn(d0, d0) <= g2);
+        const float d1 = p1 < wlo1 ? __fsub_rn(wlo1, p1) : (p1 > whi1 ? __fsub_rn(whi1, p1) : 0.0f);
+        uint32_t m = __ballot_sync(0xffffffffu, __fmaf_rn(d1, d1, __fmul_rn(d0, d0)) <= g2);
         if (__popc(m) <= 10) {
           while (m != 0u) {
             const int c = 8 * c8 + __ffs(m) - 1;
             m &= m - 1u;
-            exact(c);
+            // canonical gate with a warp-uniform early exit every 4 joints (partial sums
+            // of squares only grow)
+            float ds = 0.0f;
+            bool ok = active && c < nvalid;
+#pragma unroll
+            for (int g4 = 0; g4 < JP / 4; ++g4) {
+              if (!__any_sync(0xffffffffu, ok)) break;
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const float df = __fsub_rn(qj[4 * g4 + u], jsm[(4 * g4 + u) * kGfTile + c]);
+                ds = __fmaf_rn(df, df, ds);
+              }
+              ok = ok && (ds <= g2);
+            }
+            if (ok) {
+              const uint32_t slot = atomicAdd(&cnt[q], 1u);
+              if (slot < (uint32_t)cap) cand[(int64_t)q * cap + slot] = (int32_t)(row0 + c);
+            }
           }
           c8 += 3;
           continue;

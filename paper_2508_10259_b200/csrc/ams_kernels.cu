@@ -112,39 +112,31 @@ __global__ void query_prep_kernel(const void* __restrict__ src, const float* __r
 }
 
 // ---------------------------------------------------------------------------------
-// Query order for the gated tcgen05 path: a counting sort of the queries by joint 0
-// into kOrderBins linear bins between the batch's min and max (one block).  Any order
-// gives the same results (every query is scored independently); this one makes the
-// 32 queries of an epilogue warp span a narrow joint-0 interval, so most pool columns
-// fail the warp-level gate test of epi_chunk_sorted.  Order within a bin is arbitrary.
+// Query order for gated batches: a counting sort of the queries by a two-joint key
+// (one block).  Any order gives the same results (every query is scored
+// independently); this one makes the 32 queries of a warp span a small box in
+// (joint 0, joint 1), so most pool rows fail the warp-level gate test of the epilogue
+// (ams_match_tc.cu epi_chunk_sorted) and of gate_scan_kernel.  Key = b0 * B1 + b1 with
+// b0 a linear bin of joint 0 among B0 = clamp(nq / 256, 1, 64) bins (~256 queries, i.e.
+// 8 warps, per b0 bin) and b1 a linear bin of joint 1 among B1 = 4096 / B0 bins, each
+// between the batch's min and max (J = 1: joint 0 alone, 4096 bins).  Order within a
+// bin is arbitrary.
 // ---------------------------------------------------------------------------------
 constexpr int kOrderBins = 4096;
 constexpr int kOrderThreads = 1024;
 
-__global__ void __launch_bounds__(kOrderThreads)
-    query_order_kernel(const float* __restrict__ jsrc, int32_t J, int32_t nq, int32_t* __restrict__ perm) {
-  __shared__ uint32_t hist[kOrderBins];
-  __shared__ float red_lo[kOrderThreads / 32], red_hi[kOrderThreads / 32];
-  __shared__ uint32_t wsum[kOrderThreads / 32];
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  float lo = CUDART_INF_F, hi = -CUDART_INF_F;
-  for (int q = tid; q < nq; q += kOrderThreads) {
-    const float v = jsrc[(int64_t)q * J];
-    if (v == v) {
-      lo = fminf(lo, v);
-      hi = fmaxf(hi, v);
-    }
-  }
+__device__ __forceinline__ void block_minmax(float& lo, float& hi, float* red_lo, float* red_hi) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
     hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
   }
+  __syncthreads();
   if (lane == 0) {
     red_lo[w] = lo;
     red_hi[w] = hi;
   }
-  for (int b = tid; b < kOrderBins; b += kOrderThreads) hist[b] = 0u;
   __syncthreads();
   lo = red_lo[0];
   hi = red_hi[0];
@@ -152,13 +144,45 @@ __global__ void __launch_bounds__(kOrderThreads)
     lo = fminf(lo, red_lo[i]);
     hi = fmaxf(hi, red_hi[i]);
   }
-  const float span = hi - lo;
-  const float scale = (span > 1e-30f && span < CUDART_INF_F) ? (float)kOrderBins / span : 0.0f;
-  auto bin_of = [&](float v) -> int {
-    const float f = (v - lo) * scale;
-    return (f >= 0.0f && f < (float)kOrderBins) ? (int)f : (f >= 0.0f ? kOrderBins - 1 : 0);
+}
+
+// linear bin of v among n bins of [lo, hi] (NaN and out-of-range values clamp)
+__device__ __forceinline__ int lin_bin(float v, float lo, float scale, int n) {
+  const float f = (v - lo) * scale;
+  return (f >= 0.0f && f < (float)n) ? (int)f : (f >= 0.0f ? n - 1 : 0);
+}
+
+__global__ void __launch_bounds__(kOrderThreads)
+    query_order_kernel(const float* __restrict__ jsrc, int32_t J, int32_t nq, int32_t* __restrict__ perm) {
+  __shared__ uint32_t hist[kOrderBins];
+  __shared__ float red_lo[kOrderThreads / 32], red_hi[kOrderThreads / 32];
+  __shared__ uint32_t wsum[kOrderThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int nj = J >= 2 ? 2 : 1;
+  const int B0 = nj == 1 ? kOrderBins : max(1, min(64, nq / 256));
+  const int B1 = kOrderBins / B0;
+  float lo[2], sc[2];
+  for (int t = 0; t < nj; ++t) {
+    float l = CUDART_INF_F, h = -CUDART_INF_F;
+    for (int q = tid; q < nq; q += kOrderThreads) {
+      const float v = jsrc[(int64_t)q * J + t];
+      if (v == v) {
+        l = fminf(l, v);
+        h = fmaxf(h, v);
+      }
+    }
+    block_minmax(l, h, red_lo, red_hi);
+    const float span = h - l;
+    lo[t] = l;
+    sc[t] = (span > 1e-30f && span < CUDART_INF_F) ? (float)(t == 0 ? B0 : B1) / span : 0.0f;
+  }
+  auto key_of = [&](int q) -> int {
+    const int b0 = lin_bin(jsrc[(int64_t)q * J], lo[0], sc[0], B0);
+    return nj == 1 ? b0 : b0 * B1 + lin_bin(jsrc[(int64_t)q * J + 1], lo[1], sc[1], B1);
   };
-  for (int q = tid; q < nq; q += kOrderThreads) atomicAdd(&hist[bin_of(jsrc[(int64_t)q * J])], 1u);
+  for (int b = tid; b < kOrderBins; b += kOrderThreads) hist[b] = 0u;
+  __syncthreads();
+  for (int q = tid; q < nq; q += kOrderThreads) atomicAdd(&hist[key_of(q)], 1u);
   __syncthreads();
   // exclusive scan: thread t owns bins [4t, 4t+4)
   constexpr int per = kOrderBins / kOrderThreads;
@@ -186,7 +210,7 @@ __global__ void __launch_bounds__(kOrderThreads)
   }
   __syncthreads();
   for (int q = tid; q < nq; q += kOrderThreads) {
-    const uint32_t pos = atomicAdd(&hist[bin_of(jsrc[(int64_t)q * J])], 1u);
+    const uint32_t pos = atomicAdd(&hist[key_of(q)], 1u);
     perm[pos] = q;
   }
 }

@@ -96,7 +96,7 @@ struct TcParams {
   uint32_t* slots;           // [q_pad][KT] union-bound slots (ordered-u32; ungated only, else null)
   int64_t L;                 // local rows
   int32_t nq, d, n_qt, n_pt, S, n_units, k, gated, P;
-  int32_t sorted;            // queries staged in joint-0 order: the warp-level column test pays
+  int32_t sorted;            // queries staged in (joint 0, joint 1) order: the warp-level column test pays
   float g2;
 };
 
@@ -223,12 +223,12 @@ __device__ __forceinline__ void epi_chunk(uint32_t taddr, int64_t jbase, int nva
   }
 }
 
-// Gated chunk for a warp whose 32 queries are sorted by joint 0 (their r_0 lie in
-// [wlo, whi]).  Lane c first tests column c against the whole warp at once: the
-// canonical distance is >= RN(d0^2) (the first fmaf adds to +0, later ones only add
-// non-negative terms and RN is monotone), and the smallest |RN(r_0 - p_0)| over the
-// warp is reached at wlo or whi, so a column with RN(RN(w - p_0)^2) > g2 for the
-// nearest end w is ineligible for every lane.  The surviving columns (the ballot) are
+// Gated chunk for a warp whose 32 queries are ordered by (joint 0, joint 1) (their r_0
+// lie in [wlo, whi], r_1 in [wlo1, whi1]).  Lane c first tests column c against the
+// whole warp at once: the canonical distance after two joints is
+// fmaf(d1, d1, RN(d0^2)) and later terms only add (RN is monotone); |RN(r_t - p_t)| is
+// smallest at the interval end nearer to p_t, so with D_t = RN(w_t - p_t) for that end
+// (0 inside), a column with fmaf(D1, D1, RN(D0^2)) > g2 is ineligible for every lane.  The surviving columns (the ballot) are
 // then gated exactly per lane, one column at a time; TMEM is read only for a column
 // some lane passes.  Returns false (nothing done) when too many columns survive for
 // the per-column loop to beat the packed filter; the caller then runs epi_chunk.
@@ -238,10 +238,12 @@ template <int KT, int JP>
 __device__ __forceinline__ bool epi_chunk_sorted(uint32_t taddr, int64_t jbase, int nvalid,
                                                  const float* __restrict__ inv_sm, const float* __restrict__ jsm,
                                                  const float (&qj)[JP], float iq, float g2, float bound, int k,
-                                                 float wlo, float whi, int lane, TopK<KT, int32_t>& top) {
-  const float p0 = jsm[lane];
+                                                 float wlo, float whi, float wlo1, float whi1, int lane,
+                                                 TopK<KT, int32_t>& top) {
+  const float p0 = jsm[lane], p1 = jsm[kBlockN + lane];
   const float d0 = p0 < wlo ? __fsub_rn(wlo, p0) : (p0 > whi ? __fsub_rn(whi, p0) : 0.0f);
-  uint32_t m = __ballot_sync(0xffffffffu, __fmul_rn(d0, d0) <= g2);
+  const float d1 = p1 < wlo1 ? __fsub_rn(wlo1, p1) : (p1 > whi1 ? __fsub_rn(whi1, p1) : 0.0f);
+  uint32_t m = __ballot_sync(0xffffffffu, __fmaf_rn(d1, d1, __fmul_rn(d0, d0)) <= g2);
   if (__popc(m) > kSparseMaxCols) return false;
   while (m != 0u) {
     const int c = __ffs(m) - 1;
@@ -452,12 +454,15 @@ __global__ void __maxnreg__(168)
 #pragma unroll
       for (int t = 0; t < 4; ++t) QQ[t] = ptx::pack2(qj[t], qj[t]);   // JP >= 4
       const float iq = active ? prm.inv_q[qrow] : 0.0f;
-      // joint-0 interval of the warp's active queries (empty warp: +inf/-inf, no column passes)
+      // joint-0 / joint-1 intervals of the warp's active queries (empty warp: no column passes)
       float wlo = active ? qj[0] : CUDART_INF_F, whi = active ? qj[0] : -CUDART_INF_F;
+      float wlo1 = active ? qj[1] : CUDART_INF_F, whi1 = active ? qj[1] : -CUDART_INF_F;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         wlo = fminf(wlo, __shfl_xor_sync(0xffffffffu, wlo, o));
         whi = fmaxf(whi, __shfl_xor_sync(0xffffffffu, whi, o));
+        wlo1 = fminf(wlo1, __shfl_xor_sync(0xffffffffu, wlo1, o));
+        whi1 = fmaxf(whi1, __shfl_xor_sync(0xffffffffu, whi1, o));
       }
       const bool sparse = gated && prm.sorted != 0;
       // the caller's query index: partial lists, the bound and its slots are indexed by it
@@ -501,7 +506,7 @@ __global__ void __maxnreg__(168)
           continue;
 #endif
           if (sparse && epi_chunk_sorted<KT, JP>(taddr, jbase, nvalid, inv_sm + col0, joints_sm + col0, qj, iq,
-                                                 prm.g2, bound, prm.k, wlo, whi, lane, top))
+                                                 prm.g2, bound, prm.k, wlo, whi, wlo1, whi1, lane, top))
             continue;
           if (gated)
             epi_chunk<KT, JP, true>(taddr, jbase, nvalid, inv_sm + col0, joints_sm + col0, QQ, qj, iq, ie_min, ie_max,
