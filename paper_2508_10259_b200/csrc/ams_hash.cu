@@ -73,6 +73,14 @@ __device__ __forceinline__ uint64_t warp_sum_mod(uint64_t v) {
   return v;
 }
 
+// Fast path weights (full, 16-B aligned segments of 512*J bytes, J <= 8): the lane's
+// value is sum_j sum_u G2(j,u) * E[J-1-j][u] with G2 = b0*B + b1 the 2-byte groups of its
+// j-th 16-byte piece and E[jj][u] = B^(2(7-u)) * B^(512 jj) mod M (= the Horner weights
+// of the slow path, expanded).  Split into 32-bit halves so every product is a single
+// 32x32->64 multiply-add with no reduction until the end.
+__constant__ uint32_t kE_lo[8][8];
+__constant__ uint32_t kE_hi[8][8];
+
 struct Tables {
   const uint64_t* pow16;   // B^(16 e) mod M, e = 0..s/16
   uint64_t B4, B512, B32;
@@ -84,13 +92,22 @@ __global__ void phase1_kernel(const uint8_t* __restrict__ data, const int64_t* _
                               Tables tb, uint64_t* __restrict__ seg_hash) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g < n_segs; g += warps) {
-    // input owning segment g: last i with seg_base[i] <= g
-    int lo = 0, hi = n_inputs - 1;
+  // each warp takes a contiguous run of segments: one binary search for the owning
+  // input of its first segment, then a forward walk (no dependent search per segment)
+  const int64_t wid = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t per = (n_segs + warps - 1) / warps;
+  const int64_t g_begin = wid * per, g_end = min(n_segs, g_begin + per);
+  int lo = 0;
+  if (g_begin < g_end) {   // input owning segment g_begin: last i with seg_base[i] <= g
+    int hi = n_inputs - 1;
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
-      if (seg_base[mid] <= g) lo = mid; else hi = mid - 1;
+      if (seg_base[mid] <= g_begin) lo = mid; else hi = mid - 1;
     }
+  }
+  int64_t next_base = g_begin < g_end ? seg_base[lo + 1] : 0;
+  for (int64_t g = g_begin; g < g_end; ++g) {
+    while (g >= next_base) next_base = seg_base[++lo + 1];   // skips empty inputs
     const int64_t j = g - seg_base[lo];
     const int64_t start = offsets[lo] + j * s;
     const int64_t len = min(s, offsets[lo + 1] - start);
@@ -101,6 +118,33 @@ __global__ void phase1_kernel(const uint8_t* __restrict__ data, const int64_t* _
     const uint4* body = reinterpret_cast<const uint4*>(p + head);
     uint64_t acc = 0;
     int64_t last = -1;
+    if (head == 0 && tail == 0 && (P & 31) == 0 && P > 0 && P <= 256) {
+      // lazy accumulation: sum < 64 * 2^49 (lo) and 64 * 2^46 (hi), reduced once
+      const int J = (int)(P >> 5);
+      uint64_t lo = 0, hi = 0;
+      auto piece = [&](const uint4 w, int jj) {
+        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int wi = 0; wi < 4; ++wi) {
+          const uint32_t ga = (ws[wi] & 0xFFu) * 257u + ((ws[wi] >> 8) & 0xFFu);
+          const uint32_t gb = ((ws[wi] >> 16) & 0xFFu) * 257u + (ws[wi] >> 24);
+          lo += (uint64_t)ga * kE_lo[jj][2 * wi] + (uint64_t)gb * kE_lo[jj][2 * wi + 1];
+          hi += (uint64_t)ga * kE_hi[jj][2 * wi] + (uint64_t)gb * kE_hi[jj][2 * wi + 1];
+        }
+      };
+      if (J == 8) {   // the default 4 KB segment: all eight 16-B loads in flight at once
+        uint4 w[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) w[j] = __ldg(body + lane + 32 * j);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) piece(w[j], 7 - j);
+      } else {
+        for (int j = 0; j < J; ++j) piece(__ldg(body + lane + 32 * j), J - 1 - j);
+      }
+      // hi * 2^32 = (hi >> 29) * 2^61 + (hi mod 2^29) * 2^32, and 2^61 = 1 (mod M)
+      acc = red(red(lo) + (hi >> 29) + ((hi & 0x1FFFFFFFull) << 32));
+      last = lane + 32 * (J - 1);
+    } else
     for (int64_t q = lane; q < P; q += 32) {
       const uint4 w = __ldg(body + q);
       uint64_t h = g4(w.x);
@@ -231,6 +275,24 @@ ams_status_t ams_hasher_create(int32_t device, int64_t max_inputs, int64_t max_b
     return AMS_ERR_CUDA;
   }
   h->tb.pow16 = h->d_pow16;
+  {  // fast-path weights E[jj][u] = B^(2(7-u)) * B^(512 jj) mod M
+    uint32_t elo[8][8], ehi[8][8];
+    uint64_t bj = 1;   // B^(512 jj)
+    for (int jj = 0; jj < 8; ++jj) {
+      for (int u = 0; u < 8; ++u) {
+        uint64_t w = bj;
+        for (int e = 0; e < 2 * (7 - u); ++e) w = mulmod_host(w, kB);
+        elo[jj][u] = (uint32_t)(w & 0xFFFFFFFFull);
+        ehi[jj][u] = (uint32_t)(w >> 32);
+      }
+      bj = mulmod_host(bj, b512);
+    }
+    if (cudaMemcpyToSymbol(kE_lo, elo, sizeof elo) != cudaSuccess ||
+        cudaMemcpyToSymbol(kE_hi, ehi, sizeof ehi) != cudaSuccess) {
+      hasher_free(h);
+      return AMS_ERR_CUDA;
+    }
+  }
   *out = h;
   return AMS_OK;
 }
