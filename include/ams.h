@@ -73,7 +73,11 @@ typedef struct {
   int32_t max_k;          /* >= every k passed to ams_match; 1 <= max_k <= 64 */
   int32_t device;         /* CUDA ordinal used by this rank */
   int32_t rank, world;    /* world == 1: single GPU, no NCCL; world <= 64 */
-  const void* nccl_id;    /* 128-byte ncclUniqueId, identical on all ranks (NULL if world == 1) */
+  const void* nccl_id;    /* 128-byte ncclUniqueId, identical on all ranks; NULL if world == 1.
+                             world == 1 with a non-NULL id builds a 1-rank communicator and
+                             runs the world > 1 path (shard merge, NCCL all-gather, final
+                             merge; peer exchange if enabled) on one GPU -- results are
+                             identical; used by the tests to exercise that path */
   int64_t shard_block;    /* rows per block of the block-cyclic row map (global append
                              ordinal o lives on rank (o / B) % world);
                              0 -> contiguous: B = ceil(capacity / world) */
@@ -159,7 +163,8 @@ ams_status_t ams_merge_topk(const float* in_score, const int64_t* in_index, int3
  * three IPC handles per rank travel over the pool's NCCL communicator).  Requires all
  * ranks on one node with peer access; the pool's matches must be issued by every rank in
  * the same order (as with the NCCL path).  Errors: AMS_ERR_INVALID_ARGUMENT (null pool),
- * AMS_ERR_UNSUPPORTED (world < 2, world > 8, capacity >= 2^31, IPC unavailable),
+ * AMS_ERR_UNSUPPORTED (pool without a communicator -- world == 1 and no nccl_id --,
+ * world > 8, capacity >= 2^31, IPC unavailable),
  * AMS_ERR_OUT_OF_MEMORY, AMS_ERR_NCCL, AMS_ERR_CUDA.  Idempotent. */
 ams_status_t ams_pool_enable_peer_exchange(ams_pool_t pool);
 

@@ -301,7 +301,8 @@ ams_status_t ams_pool_create(const ams_pool_config_t* cfg, ams_pool_t* out) {
     p.gf_cap = std::max(256, 8 * c.max_k);
     ok = alloc((void**)&p.gf_cnt, (size_t)p.q_pad * 4) && alloc((void**)&p.gf_cand, (size_t)p.q_pad * p.gf_cap * 4);
   }
-  if (ok && c.world > 1)
+  p.collective = c.world > 1 || c.nccl_id != nullptr;
+  if (ok && p.collective)
     ok = alloc((void**)&p.gath_s, (size_t)c.world * c.max_queries * c.max_k * 4) &&
          alloc((void**)&p.gath_i, (size_t)c.world * c.max_queries * c.max_k * 8);
   if (!ok) {
@@ -328,7 +329,7 @@ ams_status_t ams_pool_create(const ams_pool_config_t* cfg, ams_pool_t* out) {
     delete pool;
     return AMS_ERR_CUDA;
   }
-  if (c.world > 1) {
+  if (p.collective) {
     ncclUniqueId id;
     memcpy(&id, c.nccl_id, sizeof id);
     ncclComm_t comm;
@@ -435,7 +436,7 @@ static ams_status_t match_impl(ams_pool_t pool, const void* q_emb, const float* 
   AMS_CUDA_TRY(ams::launch_query_prep(p, q_src, qj_src, nq, sorted ? p.q_perm : nullptr, s));
   if (b >= 0) AMS_CUDA_TRY(cudaEventRecord(p.consumed[b], s));   // staging b read (order + prep)
 
-  const bool multi = p.cfg.world > 1;
+  const bool multi = p.collective;
   float* shard_s = multi ? p.shard_s : out_score;
   int64_t* shard_i = multi ? p.shard_i : out_index;
   uint8_t* shard_hit = multi ? nullptr : out_hit;
@@ -572,7 +573,7 @@ ams_status_t ams_pool_enable_peer_exchange(ams_pool_t pool) {
   Pool& p = pool->p;
   if (p.broken) return AMS_ERR_CUDA;
   const int G = p.cfg.world, r = p.cfg.rank;
-  if (G < 2 || G > ams::kMaxPeers || p.nccl_comm == nullptr) return AMS_ERR_UNSUPPORTED;
+  if (G < 1 || G > ams::kMaxPeers || p.nccl_comm == nullptr) return AMS_ERR_UNSUPPORTED;
   if (p.peer_mode) return AMS_OK;
   if (p.cfg.capacity >= ((int64_t)1 << 31)) return AMS_ERR_UNSUPPORTED;   // int32 ids in the partial lists
   AMS_CUDA_TRY(cudaSetDevice(p.cfg.device));

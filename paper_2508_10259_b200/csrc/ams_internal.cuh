@@ -73,6 +73,8 @@ struct Pool {
   int32_t num_sms = 148;
   int32_t KT_max = 8;
   bool broken = false;
+  bool collective = false;    // world > 1, or world == 1 with an nccl_id: shard lists go
+                              // through the NCCL all-gather + shard merge (or peer exchange)
 
   // shard storage
   void* emb = nullptr;        // [cap_pad, d] bf16 or fp32
