@@ -348,7 +348,11 @@ __global__ void __maxnreg__(168)
         // before every CTA has issued all loads of wave w-1.  Best effort: the wait is
         // bounded (~10 ms), so a grid that is not fully co-resident (MPS, concurrent
         // kernels) still progresses -- the lockstep only ever affects speed, never results.
+#ifndef AMS_DIAG_NO_LOCKSTEP   // diagnostic builds only: measure the lockstep's cost
         if (wave > 0) {
+#else
+        if (false) {
+#endif
           const uint32_t need = wave * gridDim.x;
           for (int it = 0; it < (1 << 16) && *reinterpret_cast<volatile uint32_t*>(prm.wave_ctr) < need; ++it)
             __nanosleep(128);

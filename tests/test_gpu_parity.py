@@ -208,3 +208,21 @@ def test_every_topk_width_launches_and_matches(ams, k, nq):
     orc = oracle.match(e, j, w.q_emb, w.q_joints, k, cfg.theta, INF)
     g = run_gpu(ams, e, j, w.q_emb, w.q_joints, k, cfg.theta, INF, "bf16", max_k=64)
     check_bf16(*g, orc, cfg.theta)
+
+
+@pytest.mark.parametrize("nq", [64, 512])
+def test_self_match_score_and_norms(ams, nq):
+    """Pin P5 on the GPU: a query equal to a stored row with the same joints finds that
+    row (or a lower-index duplicate) first with |s - 1| <= 1e-5 -- tight enough to catch
+    an inverse norm that is off by more than a few ulps (fp32 sums over d = 1024 would
+    not be) or a query/pool scale mix-up; the north_star tolerance is 2e-3."""
+    cfg = ams_gen.small_variant("c3", 5000, nq)
+    w = ams_gen.generate_host(cfg)
+    rng = np.random.default_rng(nq)
+    src = rng.choice(cfg.M, nq, replace=False)
+    q, qj = w.emb[src], w.joints[src]
+    for gamma in (0.3, INF):
+        idx, score, hit = run_gpu(ams, w.emb, w.joints, q, qj, 4, 0.99, gamma, "bf16")
+        assert np.all(idx[:, 0] <= src)
+        assert np.all(np.abs(score[:, 0].astype(np.float64) - 1.0) <= 1e-5), np.abs(score[:, 0] - 1).max()
+        assert np.all(hit == 1)
