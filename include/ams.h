@@ -30,7 +30,9 @@
  *     valid until the stream reaches that point.  An append is visible to every later
  *     match on the same stream.
  *   - A pool is NOT thread-safe; callers serialise calls on one pool ("a
- *     single pool serializes writers").
+ *     single pool serializes writers").  Calls on one pool share its device workspace
+ *     (staging, partial lists), so they must also be ordered on the device: issue them on
+ *     one stream, or order the streams (events) between calls.
  *   - Argument errors are detected synchronously and nothing is enqueued.
  *   - After AMS_ERR_CUDA / AMS_ERR_NCCL the pool is unusable and must be destroyed.
  *   - Multi-GPU (world > 1): one process per GPU; create / append / match / destroy are
