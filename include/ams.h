@@ -137,7 +137,12 @@ ams_status_t ams_match(ams_pool_t pool, const void* q_emb, const float* q_joints
  * tensor-core accumulation in the last fp32 bits, both within the stated tolerance).
  * Efficient when the gate is selective (few eligible rows per query); with a wide gate
  * it stays exact but degrades to a per-query scan on the GPU.  fp32 pools use the exact
- * path of ams_match, which already evaluates the gate first. */
+ * path of ams_match, which already evaluates the gate first.
+ * On pools of >= 64 K local rows, batches of >= 129 queries use a joint-0 index of the
+ * pool (rows bucket-sorted by joint 0; built on first use -- allocating cap * (4 * JP + 4)
+ * bytes, JP = J rounded up to 4/8/16 -- and rebuilt once more than max(64 K, L/32) rows
+ * were appended since): each block of queries scans only the rows whose joint 0 lies
+ * within gamma of its queries' joint 0.  Results are unchanged. */
 ams_status_t ams_match_gate_first(ams_pool_t pool, const void* q_emb, const float* q_joints, int32_t nq,
                                   int32_t k, float threshold, float gate_radius, int64_t* out_index,
                                   float* out_score, uint8_t* out_hit, void* stream);

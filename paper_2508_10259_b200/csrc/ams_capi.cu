@@ -156,7 +156,7 @@ void free_all(Pool& p) {
   p.copy_stream = nullptr;
   void* ptrs[] = {p.emb, p.inv_norm, p.joints, p.q_stage, p.q_inv, p.q_joints, p.q_joints_raw[0], p.q_joints_raw[1],
                   p.q_raw[0], p.q_raw[1], p.q_perm, p.bound, p.slots,
-                  p.gf_cnt, p.gf_cand,
+                  p.gf_cnt, p.gf_cand, p.snap_j, p.snap_id, p.snap_off, p.snap_aux,
                   p.part_s, p.part_i, p.shard_s, p.shard_i, p.gath_s, p.gath_i, p.stage_emb,
                   p.stage_joints};
   for (void* q : ptrs)

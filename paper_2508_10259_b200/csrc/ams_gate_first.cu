@@ -31,14 +31,34 @@ namespace {
 constexpr int kGfThreads = 256;   // queries per block
 constexpr int kGfTile = kRowAlign; // 256 rows per staged joint tile
 
+// The rows a scan visits: a contiguous range of a tile-transposed joint array, either
+// the pool itself (ids == nullptr, plain mode: rows [begin, end)) or the joint-0 index
+// snapshot (ids = snapshot position -> local row; bin_off != nullptr: each block derives
+// its range from its queries' joint-0 interval).
+struct GfRows {
+  const float* jt;         // [tiles][JP][256]
+  const int32_t* ids;      // nullptr: row = local row
+  int64_t begin, end;      // plain mode range
+  const int32_t* bin_off;  // snapshot mode: [kSnapBins + 1]
+  const float* meta;       // snapshot mode: {lo, scale} of the bins
+};
+
+// linear bin of v among kSnapBins bins (lo, scale); NaN and out-of-range values clamp.
+// Monotone in v, identical in the build and in the lookup.
+__device__ __forceinline__ int snap_bin(float v, float lo, float scale) {
+  const float f = (v - lo) * scale;
+  return (f >= 0.0f && f < (float)kSnapBins) ? (int)f : (f >= 0.0f ? kSnapBins - 1 : 0);
+}
+
 template <int JP>
 __global__ void __launch_bounds__(kGfThreads)
-    gate_scan_kernel(const float* __restrict__ pool_joints, int64_t L, const float* __restrict__ q_joints,
-                     int32_t nq, int32_t S, float g2, int32_t cap, uint32_t* __restrict__ cnt,
-                     int32_t* __restrict__ cand, int32_t sorted) {
+    gate_scan_kernel(const GfRows rows, const float* __restrict__ q_joints, int32_t nq, int32_t S, float g2,
+                     int32_t cap, uint32_t* __restrict__ cnt, int32_t* __restrict__ cand, int32_t sorted) {
   __shared__ __align__(16) float js[2][JP * kGfTile];
   __shared__ __align__(16) float pn[kGfTile];       // per row: sum of squares of the first 4 joints
   __shared__ unsigned int pmax_bits;
+  __shared__ float blk_lo[kGfThreads / 32], blk_hi[kGfThreads / 32];
+  const float* __restrict__ pool_joints = rows.jt;
   const int qg = blockIdx.x, sp = blockIdx.y;
   const int q = qg * kGfThreads + threadIdx.x;
   const bool active = q < nq;
@@ -63,8 +83,35 @@ __global__ void __launch_bounds__(kGfThreads)
     whi1 = fmaxf(whi1, __shfl_xor_sync(0xffffffffu, whi1, o));
   }
   const int lane = threadIdx.x & 31;
-  const int64_t n_pt = (L + kGfTile - 1) / kGfTile;
-  const int64_t t_lo = n_pt * sp / S, t_hi = n_pt * (sp + 1) / S;
+  int64_t R0 = rows.begin, R1 = rows.end;
+  if (rows.bin_off != nullptr) {
+    // snapshot: rows whose joint 0 lies within gamma of the block's joint-0 interval.  A
+    // row can pass only if RN(RN(r0 - p0)^2) <= g2, i.e. |r0 - p0| <= sqrt(g2)(1 + 2^-23);
+    // gp rounds that up, and one extra bin on each side absorbs the rounding of the bin
+    // arithmetic, so every eligible row is inside [R0, R1).
+    if (lane == 0) {
+      blk_lo[threadIdx.x >> 5] = wlo;
+      blk_hi[threadIdx.x >> 5] = whi;
+    }
+    __syncthreads();
+    float blo = blk_lo[0], bhi = blk_hi[0];
+    for (int w = 1; w < kGfThreads / 32; ++w) {
+      blo = fminf(blo, blk_lo[w]);
+      bhi = fmaxf(bhi, blk_hi[w]);
+    }
+    if (!(blo <= bhi)) {
+      R0 = R1 = 0;   // no active query in this block
+    } else {
+      const float lo = rows.meta[0], scale = rows.meta[1];
+      const float gp = __fmul_ru(__fsqrt_ru(g2), 1.00000095367431640625f);   // (1 + 2^-20)
+      const int ba = max(0, snap_bin(__fsub_rd(blo, gp), lo, scale) - 1);
+      const int bb = min(kSnapBins - 1, snap_bin(__fadd_ru(bhi, gp), lo, scale) + 1);
+      R0 = rows.bin_off[ba];
+      R1 = rows.bin_off[bb + 1];
+    }
+  }
+  const int64_t T0 = R0 / kGfTile, n_pt = R1 > R0 ? (R1 + kGfTile - 1) / kGfTile - T0 : 0;
+  const int64_t t_lo = T0 + n_pt * sp / S, t_hi = T0 + n_pt * (sp + 1) / S;
   auto stage = [&](int64_t t, int buf) {   // cp.async (LDGSTS): does not block the thread
     const float4* src = reinterpret_cast<const float4*>(pool_joints + t * kGfTile * JP);
     float4* dst = reinterpret_cast<float4*>(js[buf]);
@@ -97,7 +144,13 @@ __global__ void __launch_bounds__(kGfThreads)
     const float tq = active ? (g2 - rq) + 3.814697265625e-06f * (g2 + rq + __uint_as_float(pmax_bits))
                             : -CUDART_INF_F;
     const int64_t row0 = t * kGfTile;
-    const int nvalid = (int)min((int64_t)kGfTile, L - row0);
+    const int cmin = (int)max((int64_t)0, R0 - row0);                 // rows [cmin, nvalid) of the tile
+    const int nvalid = (int)min((int64_t)kGfTile, R1 - row0);
+    auto emit = [&](int c) {   // eligible row c of the tile for this lane's query
+      const uint32_t slot = atomicAdd(&cnt[q], 1u);
+      if (slot < (uint32_t)cap)
+        cand[(int64_t)q * cap + slot] = rows.ids != nullptr ? rows.ids[row0 + c] : (int32_t)(row0 + c);
+    };
     auto exact = [&](int c) {   // canonical gate of row c for this lane's query
       float ds = 0.0f;
 #pragma unroll
@@ -105,10 +158,7 @@ __global__ void __launch_bounds__(kGfThreads)
         const float df = __fsub_rn(qj[u], jsm[u * kGfTile + c]);
         ds = __fmaf_rn(df, df, ds);
       }
-      if (active && c < nvalid && ds <= g2) {
-        const uint32_t slot = atomicAdd(&cnt[q], 1u);
-        if (slot < (uint32_t)cap) cand[(int64_t)q * cap + slot] = (int32_t)(row0 + c);
-      }
+      if (active && c >= cmin && c < nvalid && ds <= g2) emit(c);
     };
 #pragma unroll 1
     for (int c8 = 0; c8 < kGfTile / 8; ++c8) {
@@ -126,7 +176,7 @@ __global__ void __launch_bounds__(kGfThreads)
             // canonical gate with a warp-uniform early exit every 4 joints (partial sums
             // of squares only grow)
             float ds = 0.0f;
-            bool ok = active && c < nvalid;
+            bool ok = active && c >= cmin && c < nvalid;
 #pragma unroll
             for (int g4 = 0; g4 < JP / 4; ++g4) {
               if (!__any_sync(0xffffffffu, ok)) break;
@@ -137,10 +187,7 @@ __global__ void __launch_bounds__(kGfThreads)
               }
               ok = ok && (ds <= g2);
             }
-            if (ok) {
-              const uint32_t slot = atomicAdd(&cnt[q], 1u);
-              if (slot < (uint32_t)cap) cand[(int64_t)q * cap + slot] = (int32_t)(row0 + c);
-            }
+            if (ok) emit(c);
           }
           c8 += 3;
           continue;
@@ -272,6 +319,117 @@ __global__ void score_kernel(const uint16_t* __restrict__ emb, const float* __re
   if (out_hit != nullptr && lane == 0) out_hit[qo] = (i0 >= 0 && s0 >= threshold) ? 1 : 0;
 }
 
+// ------------------------------------------------------------------ joint-0 index build
+// A bucket sort of the local rows [0, L) by joint 0 (any order within a bin is fine: a
+// scan covers whole bins).  aux layout: [0, kSnapBins) histogram then cursor,
+// [kSnapBins, kSnapBins + 2) {min, max} of joint 0 as ordered u32, then {lo, scale} as
+// floats at [kSnapBins + 2, kSnapBins + 4).
+constexpr int kSnapMinRows = 65536;   // smaller pools: the plain scan is cheap enough
+
+__global__ void snap_minmax_kernel(const float* __restrict__ joints, int64_t L, int32_t JP, uint32_t* __restrict__ mm) {
+  uint32_t lo = 0xFFFFFFFFu, hi = 0u;
+  for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < L; l += (int64_t)gridDim.x * blockDim.x) {
+    const float v = joints[joint_offset(l, 0, JP)];
+    if (v == v) {
+      lo = min(lo, ptx::f2ord(v));
+      hi = max(hi, ptx::f2ord(v));
+    }
+  }
+  lo = __reduce_min_sync(0xffffffffu, lo);
+  hi = __reduce_max_sync(0xffffffffu, hi);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&mm[0], lo);
+    atomicMax(&mm[1], hi);
+  }
+}
+
+__device__ __forceinline__ void snap_params(const uint32_t* mm, float& lo, float& scale) {
+  lo = mm[0] == 0xFFFFFFFFu ? 0.0f : ptx::ord2f(mm[0]);
+  const float hi = mm[1] == 0u ? 0.0f : ptx::ord2f(mm[1]);
+  const float span = hi - lo;
+  scale = (span > 1e-30f && span < CUDART_INF_F) ? (float)kSnapBins / span : 0.0f;
+}
+
+__global__ void snap_hist_kernel(const float* __restrict__ joints, int64_t L, int32_t JP, uint32_t* __restrict__ aux) {
+  float lo, scale;
+  snap_params(aux + kSnapBins, lo, scale);
+  for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < L; l += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&aux[snap_bin(joints[joint_offset(l, 0, JP)], lo, scale)], 1u);
+}
+
+// one block of 1024 threads: exclusive scan of the histogram into bin_off (and the cursor)
+__global__ void __launch_bounds__(1024) snap_scan_kernel(uint32_t* __restrict__ aux, int32_t* __restrict__ bin_off) {
+  constexpr int per = kSnapBins / 1024;
+  __shared__ uint32_t wsum[32];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  uint32_t run = 0;
+  for (int i = 0; i < per; ++i) run += aux[tid * per + i];
+  uint32_t incl = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[w] = incl;
+  __syncthreads();
+  uint32_t base = 0;
+  for (int i = 0; i < w; ++i) base += wsum[i];
+  base += incl - run;
+  for (int i = 0; i < per; ++i) {
+    const uint32_t c = aux[tid * per + i];
+    bin_off[tid * per + i] = (int32_t)base;
+    aux[tid * per + i] = base;   // cursor
+    base += c;
+  }
+  if (tid == 1023) bin_off[kSnapBins] = (int32_t)base;
+  if (tid == 0) {
+    float lo, scale;
+    snap_params(aux + kSnapBins, lo, scale);
+    reinterpret_cast<float*>(aux + kSnapBins + 2)[0] = lo;
+    reinterpret_cast<float*>(aux + kSnapBins + 2)[1] = scale;
+  }
+}
+
+__global__ void snap_scatter_kernel(const float* __restrict__ joints, int64_t L, int32_t JP,
+                                    uint32_t* __restrict__ aux, float* __restrict__ snap_j,
+                                    int32_t* __restrict__ snap_id) {
+  float lo, scale;
+  snap_params(aux + kSnapBins, lo, scale);
+  for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < L; l += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pos = atomicAdd(&aux[snap_bin(joints[joint_offset(l, 0, JP)], lo, scale)], 1u);
+    snap_id[pos] = (int32_t)l;
+    for (int t = 0; t < JP; ++t) snap_j[joint_offset(pos, t, JP)] = joints[joint_offset(l, t, JP)];
+  }
+}
+
+// (Re)build the index over the current local rows when it is missing or its unsorted
+// tail has grown past max(64 K, L / 32) rows.  Lazily allocated on first use.
+cudaError_t snap_refresh(Pool& p, cudaStream_t s) {
+  const int64_t L = p.local;
+  if (p.snap_L > 0 && L - p.snap_L <= std::max<int64_t>(65536, L / 32)) return cudaSuccess;
+  cudaError_t e;
+  if (p.snap_j == nullptr) {
+    if ((e = cudaMalloc((void**)&p.snap_j, (size_t)p.cap_pad * p.JP * 4)) != cudaSuccess ||
+        (e = cudaMalloc((void**)&p.snap_id, (size_t)p.cap_pad * 4)) != cudaSuccess ||
+        (e = cudaMalloc((void**)&p.snap_off, (size_t)(kSnapBins + 1) * 4)) != cudaSuccess ||
+        (e = cudaMalloc((void**)&p.snap_aux, (size_t)(kSnapBins + 4) * 4)) != cudaSuccess)
+      return e;
+  }
+  uint32_t* aux = p.snap_aux;
+  if ((e = cudaMemsetAsync(aux, 0, (size_t)(kSnapBins + 2) * 4, s)) != cudaSuccess ||
+      (e = cudaMemsetAsync(aux + kSnapBins, 0xFF, 4, s)) != cudaSuccess)
+    return e;
+  const int grid = 4 * p.num_sms;
+  snap_minmax_kernel<<<grid, 256, 0, s>>>(p.joints, L, p.JP, aux + kSnapBins);
+  snap_hist_kernel<<<grid, 256, 0, s>>>(p.joints, L, p.JP, aux);
+  snap_scan_kernel<<<1, 1024, 0, s>>>(aux, p.snap_off);
+  snap_scatter_kernel<<<grid, 256, 0, s>>>(p.joints, L, p.JP, aux, p.snap_j, p.snap_id);
+  p.launches += 4;
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  p.snap_L = L;
+  return cudaSuccess;
+}
+
 template <int JP>
 cudaError_t launch_gf_jp(Pool& p, const MatchArgs& a, int32_t cap, float* out_s, int64_t* out_i, uint8_t* out_hit,
                          bool sorted, cudaStream_t s) {
@@ -283,9 +441,27 @@ cudaError_t launch_gf_jp(Pool& p, const MatchArgs& a, int32_t cap, float* out_s,
                                                       (12 * (int64_t)p.num_sms + n_qg - 1) / n_qg));
   cudaError_t e = cudaMemsetAsync(p.gf_cnt, 0, (size_t)a.nq * sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
-  if (p.local > 0) {
-    gate_scan_kernel<JP><<<dim3(n_qg, S), kGfThreads, 0, s>>>(p.joints, p.local, p.q_joints, a.nq, S, a.g2, cap,
-                                                                p.gf_cnt, p.gf_cand, sorted ? 1 : 0);
+  // Sorted batches on large pools scan the joint-0 index: each block of 256 queries
+  // visits only the rows within gamma of its joint-0 interval (plus the unsorted tail).
+  const bool snap = sorted && p.local >= kSnapMinRows;
+  if (snap && (e = snap_refresh(p, s)) != cudaSuccess) return e;
+  const int64_t plain_begin = snap ? p.snap_L : 0;
+  if (snap) {
+    const GfRows rows{p.snap_j, p.snap_id, 0, p.snap_L, p.snap_off,
+                      reinterpret_cast<const float*>(p.snap_aux + kSnapBins + 2)};
+    gate_scan_kernel<JP><<<dim3(n_qg, S), kGfThreads, 0, s>>>(rows, p.q_joints, a.nq, S, a.g2, cap, p.gf_cnt,
+                                                                p.gf_cand, 1);
+    ++p.launches;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  if (p.local > plain_begin) {
+    const int64_t tail_tiles = (p.local + kGfTile - 1) / kGfTile - plain_begin / kGfTile;
+    const int St = snap ? (int)std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(1, tail_tiles / 8),
+                                                                      (12 * (int64_t)p.num_sms + n_qg - 1) / n_qg))
+                        : S;
+    const GfRows rows{p.joints, nullptr, plain_begin, p.local, nullptr, nullptr};
+    gate_scan_kernel<JP><<<dim3(n_qg, St), kGfThreads, 0, s>>>(rows, p.q_joints, a.nq, St, a.g2, cap, p.gf_cnt,
+                                                                 p.gf_cand, sorted ? 1 : 0);
     ++p.launches;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }

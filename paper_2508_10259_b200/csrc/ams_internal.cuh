@@ -17,6 +17,7 @@ constexpr int kBlockK = 64;      // bf16 elements per stage row = one 128-B swiz
 constexpr int kRowAlign = 256;   // shard storage is padded to a multiple of this
 constexpr int kEpiHalves = 2;    // epilogue warps per TMEM lane group (column halves)
 constexpr int kSimtThreads = 128;
+constexpr int kSnapBins = 65536;  // joint-0 bins of the gate-first index
 
 // --------------------------------------------------------------------------- shard map
 // Block-cyclic: global ordinal o -> block b = o / B, owner b % G, local (b / G) * B + o % B.
@@ -120,6 +121,14 @@ struct Pool {
   int32_t gf_cap = 0;
   uint32_t* gf_cnt = nullptr;  // [q_pad]
   int32_t* gf_cand = nullptr;  // [q_pad, gf_cap] local rows
+  // gate-first joint-0 index (built lazily by the first sorted gate-first call): local rows
+  // [0, snap_L) bucket-sorted by joint 0 into kSnapBins linear bins; rows appended since
+  // are scanned in plain order until the next rebuild
+  int64_t snap_L = 0;
+  float* snap_j = nullptr;      // [cap_pad/256][JP][256] joints in snapshot order
+  int32_t* snap_id = nullptr;   // [cap_pad] snapshot position -> local row
+  int32_t* snap_off = nullptr;  // [kSnapBins + 1] first snapshot position of each bin
+  uint32_t* snap_aux = nullptr; // [kSnapBins] histogram / cursor, then {min, max} (ordered u32), {lo, scale}
 
   CUtensorMap tmap_pool{};   // bf16 pool [cap_pad, d], box {64, 256}, SW128 (CTA tile)
   CUtensorMap tmap_pool2{};  // bf16 pool [cap_pad, d], box {64, 128}, SW128 (CTA-pair half tile)

@@ -166,3 +166,34 @@ def test_host_staging_pipeline(ams):
     for q, qj, o in zip(qs, qjs, outs):
         orc = oracle.match(pe, pj, q, qj, 10, 0.9, 0.3)
         check_bf16(*[t.cpu().numpy() for t in o], orc, 0.9)
+
+
+def test_gate_first_joint_index_and_tail(ams):
+    """Pools of >= 64 K local rows: sorted gate-first batches scan the joint-0 index
+    (bucket-sorted snapshot) for the rows within gamma of each block's joint-0 interval,
+    plus the rows appended since the snapshot in plain order; the snapshot is rebuilt
+    once that tail exceeds max(64 K, L/32).  Dense-gate joints (many eligible rows per
+    query, many near bin and gate boundaries) against the oracle after each stage:
+    fresh index, index + tail, rebuilt index."""
+    rng = np.random.default_rng(77)
+    d, J, k = 64, 3, 12
+    sizes = [70000, 20000, 60000]
+    M = sum(sizes)
+    pe = emb_bits(rng, M, d)
+    pj = rng.uniform(-0.6, 0.6, (M, J)).astype(np.float32)
+    pj[::97, 0] = np.round(pj[::97, 0], 1)   # exact ties in joint 0 at bin-friendly values
+    nq = 300
+    q = emb_bits(rng, nq, d)
+    qj = rng.uniform(-0.6, 0.6, (nq, J)).astype(np.float32)
+    qj[::7, 0] = np.round(qj[::7, 0], 1)
+    gamma = 0.12
+    with ams.Pool(d, J, M, nq, k) as pool:
+        lo = 0
+        for n in sizes:
+            pool.append(torch.from_numpy(pe[lo:lo + n]).cuda(), torch.from_numpy(pj[lo:lo + n]).cuda())
+            lo += n
+            g = [t.cpu().numpy() for t in pool.match(torch.from_numpy(q).cuda(), torch.from_numpy(qj).cuda(), k,
+                                                     0.5, gamma, gate_first=True)]
+            orc = oracle.match(pe[:lo], pj[:lo], q, qj, k, 0.5, gamma)
+            assert orc.nelig.mean() > 20, "case must exercise the gate"
+            check_bf16(*g, orc, 0.5)
