@@ -389,10 +389,16 @@ __global__ void __maxnreg__(168)
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer (leader)
-    if (lane == 0 && crank == 0) {
+    // The whole warp walks the (uniform) loop and waits; one elected lane issues.  The
+    // smem descriptors of a stage are the base descriptors plus the stage offset (the
+    // 14-bit start-address field never carries: smem < 256 KB), so an UMMA costs a few
+    // uniform integer ops instead of a per-issue descriptor rebuild.
+    if (crank == 0) {
       int stage = 0;
       uint32_t phase = 0;
       uint32_t tile_count = 0;
+      const uint64_t da0 = ptx::sdesc_k_sw128(ptx::smem_u32(sA));
+      const uint64_t db0 = ptx::sdesc_k_sw128(ptx::smem_u32(sB));
       for (int u = cid; u < prm.n_units; u += ncl) {
         const int sp = u / prm.n_qt;
         int t_lo, t_hi;
@@ -410,25 +416,28 @@ __global__ void __maxnreg__(168)
           for (int kb = 0; kb < n_kb; ++kb) {
             ptx::mbar_wait(&full[stage], phase);
             ptx::tc_fence_after();
-            const uint32_t a0 = ptx::smem_u32(sA + stage * kABytes);
-            const uint32_t b0 = ptx::smem_u32(sB + stage * BBYTES);
+            if (ptx::elect_one()) {
+              const uint64_t da = da0 + (uint64_t)((uint32_t)stage * (kABytes >> 4));
+              const uint64_t db = db0 + (uint64_t)((uint32_t)stage * (BBYTES >> 4));
 #pragma unroll
-            for (int kk = 0; kk < kBlockK / 16; ++kk) {
-              ptx::umma_f16<CG>(d_tmem, ptx::sdesc_k_sw128(a0 + kk * 32), ptx::sdesc_k_sw128(b0 + kk * 32),
-                                Geo<CG>::idesc, (kb | kk) != 0 ? 1u : 0u);
+              for (int kk = 0; kk < kBlockK / 16; ++kk)
+                ptx::umma_f16<CG>(d_tmem, da + (uint64_t)(2 * kk), db + (uint64_t)(2 * kk), Geo<CG>::idesc,
+                                  (kb | kk) != 0 ? 1u : 0u);
+              ptx::umma_commit<CG>(&empty[stage]);
             }
-            ptx::umma_commit<CG>(&empty[stage]);
+            __syncwarp();
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1u;
             }
           }
-          ptx::umma_commit<CG>(&tfull[buf]);
+          if (ptx::elect_one()) ptx::umma_commit<CG>(&tfull[buf]);
+          __syncwarp();
         }
 #ifdef AMS_DIAG_TIMELINE
         unsigned long long t1;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-        if (u < kDiagUnits) {
+        if (lane == 0 && u < kDiagUnits) {
           g_diag_tl[3 * u] = t0;
           g_diag_tl[3 * u + 1] = t1;
           g_diag_tl[3 * u + 2] = (unsigned long long)cid | ((unsigned long long)__smid() << 32);

@@ -197,6 +197,18 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
                : "memory");
 }
 
+// one lane of the (fully active) warp, always the same one: tcgen05.commit tracks the
+// MMAs of the issuing thread, so issue and commit must come from this lane
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "elect.sync _|P, 0xffffffff;\n\t"
+      "selp.b32 %0, 1, 0, P;\n}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 // 3-input max (FMNMX3, sm_100)
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float r;
