@@ -329,7 +329,9 @@ __global__ void __maxnreg__(168)
 
   if (warp == kProducerWarp) {
     // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
+    // Whole warp walks the loop and waits (uniform control flow), one elected lane issues.
+    {
+      const uint32_t full_leader0 = CG == 2 ? ptx::mapa(ptx::smem_u32(&full[0]), 0) : 0u;
       const uint64_t pol_q = ptx::policy_evict_last();
       const uint64_t pol_pool = prm.n_qt > 1 ? ptx::policy_evict_normal() : ptx::policy_evict_first();
       int stage = 0;
@@ -356,35 +358,43 @@ __global__ void __maxnreg__(168)
           const uint32_t need = wave * gridDim.x;
           for (int it = 0; it < (1 << 16) && *reinterpret_cast<volatile uint32_t*>(prm.wave_ctr) < need; ++it)
             __nanosleep(128);
+          __syncwarp();   // lanes may leave the spin at different iterations
         }
         for (int t = t_lo; t < t_hi; ++t, ++tile_count) {
           const int buf = tile_count & 1;
           const uint32_t use = tile_count >> 1;
           ptx::mbar_wait(&aempty[buf], (use & 1u) ^ 1u);
-          uint8_t* aux = sAux + buf * AUX;
-          ptx::mbar_arrive_expect_tx(&afull[buf], AUX);
-          ptx::bulk_load(aux, prm.pool_joints + (int64_t)t * kBlockN * JP, AUXJ, &afull[buf]);
-          ptx::bulk_load(aux + AUXJ, prm.pool_inv + (int64_t)t * kBlockN, kBlockN * 4, &afull[buf]);
+          if (ptx::elect_one()) {
+            uint8_t* aux = sAux + buf * AUX;
+            ptx::mbar_arrive_expect_tx(&afull[buf], AUX);
+            ptx::bulk_load(aux, prm.pool_joints + (int64_t)t * kBlockN * JP, AUXJ, &afull[buf]);
+            ptx::bulk_load(aux + AUXJ, prm.pool_inv + (int64_t)t * kBlockN, kBlockN * 4, &afull[buf]);
+          }
+          __syncwarp();
           const int prow0 = t * kBlockN + (int)crank * (int)Geo<CG>::b_rows;
           for (int kb = 0; kb < n_kb; ++kb) {
             ptx::mbar_wait(&empty[stage], phase ^ 1u);
-            if (CG == 1) {
-              ptx::mbar_arrive_expect_tx(&full[stage], STAGE);
-              ptx::tma_load_2d(sA + stage * kABytes, &tmap_q, &full[stage], kb * kBlockK, qrow0, pol_q);
-              ptx::tma_load_2d(sB + stage * BBYTES, &tmap_pool, &full[stage], kb * kBlockK, prow0, pol_pool);
-            } else {
-              if (crank == 0) ptx::mbar_arrive_expect_tx(&full[stage], CG * STAGE);
-              const uint32_t fb = ptx::mapa(ptx::smem_u32(&full[stage]), 0);
-              ptx::tma_load_2d_pair(sA + stage * kABytes, &tmap_q, fb, kb * kBlockK, qrow0, pol_q);
-              ptx::tma_load_2d_pair(sB + stage * BBYTES, &tmap_pool, fb, kb * kBlockK, prow0, pol_pool);
+            if (ptx::elect_one()) {
+              if (CG == 1) {
+                ptx::mbar_arrive_expect_tx(&full[stage], STAGE);
+                ptx::tma_load_2d(sA + stage * kABytes, &tmap_q, &full[stage], kb * kBlockK, qrow0, pol_q);
+                ptx::tma_load_2d(sB + stage * BBYTES, &tmap_pool, &full[stage], kb * kBlockK, prow0, pol_pool);
+              } else {
+                if (crank == 0) ptx::mbar_arrive_expect_tx(&full[stage], CG * STAGE);
+                const uint32_t fb = full_leader0 + (uint32_t)(stage * sizeof(uint64_t));
+                ptx::tma_load_2d_pair(sA + stage * kABytes, &tmap_q, fb, kb * kBlockK, qrow0, pol_q);
+                ptx::tma_load_2d_pair(sB + stage * BBYTES, &tmap_pool, fb, kb * kBlockK, prow0, pol_pool);
+              }
             }
+            __syncwarp();
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1u;
             }
           }
         }
-        atomicAdd(prm.wave_ctr, 1u);
+        if (ptx::elect_one()) atomicAdd(prm.wave_ctr, 1u);
+        __syncwarp();
       }
     }
   } else if (warp == kMmaWarp) {
