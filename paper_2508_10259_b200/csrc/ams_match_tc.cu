@@ -493,7 +493,7 @@ __global__ void __maxnreg__(168)
       uint32_t* bnd = prm.bound + (active ? qout : 0);
       float bound = -CUDART_INF_F;
       if (active) {
-        const uint32_t b = *reinterpret_cast<volatile uint32_t*>(bnd);
+        const uint32_t b = ptx::ld_relaxed_gpu(bnd);
         if (b) bound = ptx::ord2f(b);
       }
       TopK<KT, int32_t> top;
@@ -552,7 +552,7 @@ __global__ void __maxnreg__(168)
           since = 0;
           if (active) {
             if (top.kth_s > -CUDART_INF_F) atomicMax(bnd, ptx::f2ord(top.kth_s));
-            const uint32_t b = *reinterpret_cast<volatile uint32_t*>(bnd);
+            const uint32_t b = ptx::ld_relaxed_gpu(bnd);
             if (b) bound = fmaxf(bound, ptx::ord2f(b));
             if (prm.slots != nullptr) {
               // union bound: list l keeps its best score in slot l mod k; slots hold

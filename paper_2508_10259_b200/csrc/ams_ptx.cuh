@@ -197,6 +197,14 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
                : "memory");
 }
 
+// relaxed gpu-scope load (the shared bounds are only ever raised; any value read is a
+// valid, possibly stale, lower bound -- no ordering needed, no system-scope traffic)
+__device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // one lane of the (fully active) warp, always the same one: tcgen05.commit tracks the
 // MMAs of the issuing thread, so issue and commit must come from this lane
 __device__ __forceinline__ bool elect_one() {
