@@ -11,9 +11,21 @@
 #include <new>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>   // header-only; ranges cost a pointer check unless a profiler is attached
+
 #include "ams_internal.cuh"
 
 using ams::Pool;
+
+namespace {
+// host-side NVTX range around an entry point (nsys / ncu --nvtx show the call structure)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+}  // namespace
 
 struct ams_pool_s {
   Pool p;
@@ -346,6 +358,7 @@ ams_status_t ams_pool_create(const ams_pool_config_t* cfg, ams_pool_t* out) {
 
 ams_status_t ams_pool_append(ams_pool_t pool, const void* emb, const float* joints, int64_t n,
                              int64_t* first_index, void* stream) {
+  NvtxRange nvtx("ams_pool_append");
   if (pool == nullptr || n < 0) return AMS_ERR_INVALID_ARGUMENT;
   Pool& p = pool->p;
   if (p.broken) return AMS_ERR_CUDA;
@@ -381,6 +394,7 @@ ams_status_t ams_pool_append(ams_pool_t pool, const void* emb, const float* join
 static ams_status_t match_impl(ams_pool_t pool, const void* q_emb, const float* q_joints, int32_t nq, int32_t k,
                                float threshold, float gate_radius, int64_t* out_index, float* out_score,
                                uint8_t* out_hit, void* stream, bool gate_first) {
+  NvtxRange nvtx(gate_first ? "ams_match_gate_first" : "ams_match");
   if (pool == nullptr) return AMS_ERR_INVALID_ARGUMENT;
   Pool& p = pool->p;
   if (p.broken) return AMS_ERR_CUDA;
