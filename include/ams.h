@@ -102,7 +102,9 @@ ams_status_t ams_pool_create(const ams_pool_config_t* cfg, ams_pool_t* out);
  * Rows receive the global append ordinals [size, size + n); *first_index (host, may
  * be NULL) receives `size`.  Each rank keeps the rows its shard map owns and computes
  * their inverse L2 norms from the STORED values (bf16: fp64 sum, rounded once to fp32;
- * fp32: canonical in-order fmaf chain, IEEE sqrt and division).
+ * fp32: canonical in-order fmaf chain, IEEE sqrt and division).  With DEVICE buffers
+ * only the rows this rank owns are read (a rank that owns none of [size, size + n) may
+ * pass any valid device pointer); host buffers are staged in full.
  * Errors: AMS_ERR_INVALID_ARGUMENT (null pool, n < 0, null data with n > 0),
  * AMS_ERR_CAPACITY (size + n > capacity; nothing is appended), AMS_ERR_CUDA. */
 ams_status_t ams_pool_append(ams_pool_t pool, const void* emb, const float* joints, int64_t n,
