@@ -270,7 +270,7 @@ __device__ __forceinline__ bool epi_chunk_sorted(uint32_t taddr, int64_t jbase, 
 }
 
 template <int KT, int JP, int CG>
-__global__ void __maxnreg__(168)
+__global__ void __maxnreg__(KT >= 64 ? 200 : 168)
     match_tc_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_pool,
                     const TcParams prm) {
   constexpr int STAGES = stages_for<JP, CG>();
