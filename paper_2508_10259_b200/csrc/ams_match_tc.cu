@@ -269,8 +269,11 @@ __device__ __forceinline__ bool epi_chunk_sorted(uint32_t taddr, int64_t jbase, 
   return true;
 }
 
+// 168 registers is the ceiling for 10 warps per CTA: warps are spread over the 4 SM
+// sub-partitions (3 + 3 + 2 + 2) and each holds 16 K registers, so 3 x 32 x 168 = 16128
+// fits while 176 fails at launch ("too many resources").  KT = 64 spills a little.
 template <int KT, int JP, int CG>
-__global__ void __maxnreg__(KT >= 64 ? 200 : 168)
+__global__ void __maxnreg__(168)
     match_tc_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_pool,
                     const TcParams prm) {
   constexpr int STAGES = stages_for<JP, CG>();
