@@ -132,6 +132,9 @@ def parse():
     ap.add_argument("--gate-first", action="store_true",
                     help="time ams_match_gate_first (SURVEY 8(f) f3 variant) instead of the dense ams_match")
     ap.add_argument("--no-variant", action="store_true", help="skip the gate-first side measurement")
+    ap.add_argument("--kernel-policy", type=int, default=0, choices=[0, 1],
+                    help="1: batches of <= 128 queries use the 128-query-tile kernel instead of the "
+                         "small-batch kernel (A/B measurement)")
     return ap.parse_args()
 
 
@@ -231,6 +234,7 @@ def run_stream(args):
     cap = cfg.M + per_step * (T + W)
     block = 256
     pool = adist.create_pool(cfg.d, cfg.J, cap, per_step, cfg.k, dtype="bf16", shard_block=block)
+    ams.ams_pool_set_kernel_policy(pool.handle, args.kernel_policy)
     dummy = torch.zeros(1, cfg.d, dtype=torch.bfloat16, device=dev)
     dummy_j = torch.zeros(1, cfg.J, dtype=torch.float32, device=dev)
 
@@ -314,6 +318,10 @@ def run_stream(args):
     launches = ams.ams_pool_launch_count(pool.handle) - l0
     clocks = clk.stop()
     lat = np.array([a.elapsed_time(b) for a, b in evs])
+    bsz = np.array([b for s in range(W, T + W) for b in queries[s][2]])
+    by_batch = {name: {"calls": int(m.sum()), "p50": float(np.percentile(lat[m], 50)),
+                       "p99": float(np.percentile(lat[m], 99))}
+                for name, m in (("nq<=128", bsz <= 128), ("nq>128", bsz > 128)) if m.any()}
     steps_ms = np.array([a.elapsed_time(b) for a, b in step_ev])
     total = t0.elapsed_time(t1)
     if world > 1:
@@ -341,7 +349,8 @@ def run_stream(args):
                            "gate_radius": cfg.gamma, "appends_per_step": per_step, "queries_per_step": per_step,
                            "batches": "log-uniform 1..256 (seeded)", "shard": f"block-cyclic 256 over {world} rank(s)",
                            "l2": "inputs larger than L2 (pool %.1f GB)" % (m_now * cfg.d * 2 / 1e9)},
-                "latency_ms": {"p50": p50, "p99": p99, "max": float(lat.max()), "calls": int(lat.size)},
+                "latency_ms": {"p50": p50, "p99": p99, "max": float(lat.max()), "calls": int(lat.size),
+                               "by_batch_size_rank0": by_batch},
                 "step_ms": {"p50": float(np.percentile(steps_ms, 50)), "max": float(steps_ms.max()),
                             "fits_20ms_step": bool(steps_ms.max() < 20.0)},
                 "pool_scan_gbps_per_gpu_p50": gbs,
@@ -434,6 +443,7 @@ def main():
 
     # ------------------------------------------------------------------ pool + queries
     pool = adist.create_pool(cfg.d, cfg.J, cfg.M, cfg.Q, cfg.k, dtype="bf16", shard_block=0)
+    ams.ams_pool_set_kernel_policy(pool.handle, args.kernel_policy)
     dummy = torch.zeros(1, cfg.d, dtype=torch.bfloat16, device=dev)
     dummy_j = torch.zeros(1, cfg.J, dtype=torch.float32, device=dev)
 
@@ -509,6 +519,16 @@ def main():
                 "frac_vs_sustained": achieved_tf / peaks["bf16_tflops_sustained"]
                 if peaks.get("bf16_tflops_sustained") else None,
                 "frac_vs_datasheet_2250": achieved_tf / 2250.0}
+
+    if not args.gate_first and cfg.Q <= 128:   # below the ridge (~250 flop/B): HBM-bound scan
+        gbs = (bytes_step / world) / (kern_avg / 1e3) / 1e9
+        roofline = {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                    "frac": gbs / peaks["hbm_gbs"], "traffic": load_traffic(args.workload, "match_tc"),
+                    "kernel": "match_scan_kernel" if plan.get("kernel_id") == 4 else "match_tc_kernel",
+                    "algorithmic_per_launch": {"bytes": bytes_step / world, "flop": flops_launch},
+                    "kernel_ms_avg": kern_avg, "kernel_share_of_step": kern_avg / (t_ms / args.steps),
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks["source"] == "measured"
+                    else "fallback 6650 GB/s (B200_PROFILING.md; MEASURED_PEAKS.json absent)"}
 
     if args.gate_first:   # the dominant kernels read only joints: report against HBM
         jp = 4 if cfg.J <= 4 else 8 if cfg.J <= 8 else 16

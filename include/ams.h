@@ -344,8 +344,18 @@ ams_status_t ams_pool_read_profile(ams_pool_t pool, double* kernel_ms, int64_t* 
 ams_status_t ams_pool_launch_count(ams_pool_t pool, int64_t* launches);
 
 /* Describes the last ams_match launch plan: number of row splits, partial lists per
- * query, grid size, dominant-kernel id (0 = fp32 SIMT, 1 = tcgen05). Any pointer may
- * be NULL. */
+ * query, grid size, dominant-kernel id (0 = fp32 SIMT; 1 = tcgen05, one CTA per
+ * 128-query tile; 2 = tcgen05 CTA pair per 256-query tile; 4 = tcgen05 small-batch
+ * kernel with pool rows on the MMA M side and the nq <= 128 queries on N). Any pointer
+ * may be NULL. */
+/* Kernel choice for bf16 ams_match calls (results are the same either way, within the
+ * bf16 tolerances: the fp32 tensor-core sums of a pair may round differently).
+ * policy 0 (default): batches of nq <= 128 (ungrouped, k <= 32, lists fitting shared
+ * memory) use the small-batch kernel (plan id 4); policy 1: they use the 128-query-tile
+ * kernel (plan id 1).  For A/B measurements and tests.  Host-only; takes effect at the
+ * next ams_match.  AMS_ERR_INVALID_ARGUMENT for a NULL pool or another policy. */
+ams_status_t ams_pool_set_kernel_policy(ams_pool_t pool, int32_t policy);
+
 ams_status_t ams_pool_last_plan(ams_pool_t pool, int32_t* splits, int32_t* partials,
                                 int32_t* grid, int32_t* kernel_id);
 

@@ -30,7 +30,7 @@ EXPORTS = ("ams_get_nccl_unique_id", "ams_pool_create", "ams_pool_append", "ams_
            "ams_merge_topk", "ams_pool_enable_peer_exchange", "ams_exchange_selftest",
            "ams_pool_size",
            "ams_pool_destroy", "ams_status_string", "ams_pool_set_profiling", "ams_pool_read_profile",
-           "ams_pool_launch_count", "ams_pool_last_plan", "ams_shard_locate", "ams_shard_capacity",
+           "ams_pool_launch_count", "ams_pool_last_plan", "ams_pool_set_kernel_policy", "ams_shard_locate", "ams_shard_capacity",
            "ams_abi_version", "ams_hasher_create", "ams_hash_actions", "ams_hasher_destroy",
            "ams_vstore_create", "ams_vstore_intern", "ams_vstore_release", "ams_vstore_resolve",
            "ams_vstore_arena", "ams_vstore_stats", "ams_vstore_destroy", "ams_tier_create", "ams_tier_admit",
@@ -69,6 +69,7 @@ def _load():
         "ams_pool_size": [V, ctypes.POINTER(I64)],
         "ams_pool_destroy": [V],
         "ams_pool_set_profiling": [V, I32],
+        "ams_pool_set_kernel_policy": [V, I32],
         "ams_pool_read_profile": [V, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64)],
         "ams_pool_launch_count": [V, ctypes.POINTER(I64)],
         "ams_pool_last_plan": [V, ctypes.POINTER(I32), ctypes.POINTER(I32), ctypes.POINTER(I32),
@@ -221,6 +222,11 @@ def ams_pool_destroy(pool: int) -> None:
 
 def ams_pool_set_profiling(pool: int, enable: bool) -> None:
     _check(lib.ams_pool_set_profiling(pool, 1 if enable else 0), "ams_pool_set_profiling")
+
+
+def ams_pool_set_kernel_policy(pool: int, policy: int) -> None:
+    """0: auto (small-batch kernel for nq <= 128 where eligible); 1: never use it."""
+    _check(lib.ams_pool_set_kernel_policy(pool, int(policy)), "ams_pool_set_kernel_policy")
 
 
 def ams_pool_read_profile(pool: int):

@@ -131,6 +131,27 @@ void plan_tc(const Pool& p, int nq, int KT, int& S, int& grid, int& cg) {
   grid = (int)std::min<int64_t>((int64_t)n_qt * S, clusters) * cg;
 }
 
+// Plan of the small-batch kernel: one query tile, so units are row splits only; same
+// cost model as plan_tc (busiest CTA's tile count, ties -> fewer splits).
+void plan_scan(const Pool& p, int nq, int KT, int& S, int& grid) {
+  const int64_t n_pt = (p.local + ams::kBlockN - 1) / ams::kBlockN;
+  const int ctas = p.num_sms;
+  const int64_t per_split = (int64_t)nq * ams::scan_lists_per_split() * KT;
+  int64_t s_cap = std::max<int64_t>(1, p.part_cap / per_split);
+  s_cap = std::min<int64_t>({s_cap, std::max<int64_t>(1, n_pt), (int64_t)8 * ctas});
+  int64_t best_cost = LLONG_MAX;
+  int best = 1;
+  for (int64_t s = 1; s <= s_cap; ++s) {
+    const int64_t cost = ((s + ctas - 1) / ctas) * ((n_pt + s - 1) / s) * 64 + s;
+    if (cost < best_cost) {
+      best_cost = cost;
+      best = (int)s;
+    }
+  }
+  S = best;
+  grid = (int)std::min<int64_t>(S, ctas);
+}
+
 void plan_simt(const Pool& p, int nq, int KT, int& S) {
   const int64_t per_split = (int64_t)nq * ams::kSimtThreads * KT;
   int64_t s_cap = std::max<int64_t>(1, p.part_cap / per_split);
@@ -325,7 +346,11 @@ ams_status_t ams_pool_create(const ams_pool_config_t* cfg, ams_pool_t* out) {
   if (c.dtype == AMS_DTYPE_BF16) {
     if (!encode_bf16_map(&p.tmap_pool, p.emb, p.cap_pad, d, ams::kBlockN) ||
         !encode_bf16_map(&p.tmap_pool2, p.emb, p.cap_pad, d, ams::kBlockN / 2) ||
-        !encode_bf16_map(&p.tmap_q, p.q_stage, p.q_pad, d, ams::kBlockM)) {
+        !encode_bf16_map(&p.tmap_q, p.q_stage, p.q_pad, d, ams::kBlockM) ||
+        !encode_bf16_map(&p.tmap_qs[0], p.q_stage, p.q_pad, d, 16) ||
+        !encode_bf16_map(&p.tmap_qs[1], p.q_stage, p.q_pad, d, 32) ||
+        !encode_bf16_map(&p.tmap_qs[2], p.q_stage, p.q_pad, d, 64) ||
+        !encode_bf16_map(&p.tmap_qs[3], p.q_stage, p.q_pad, d, ams::kBlockM)) {
       free_all(p);
       delete pool;
       return AMS_ERR_CUDA;
@@ -492,10 +517,22 @@ static ams_status_t match_impl(ams_pool_t pool, const void* q_emb, const float* 
       p.last_splits = S;
       p.last_grid = nq * S;
       p.last_kernel = 0;
+    } else if (p.kernel_policy == 0 && !sorted && ams::scan_stages(p, nq, a.KT) > 0) {
+      int S, grid;
+      plan_scan(p, nq, a.KT, S, grid);
+      P = S * ams::scan_lists_per_split();
+      a.slots = (!a.gated && P >= a.k) ? 1 : 0;   // union-bound slots (launch_match_scan)
+      if (e0) AMS_CUDA_TRY(cudaEventRecord(e0, s));
+      AMS_CUDA_TRY(ams::launch_match_scan(p, a, S, grid, s));
+      if (e1) AMS_CUDA_TRY(cudaEventRecord(e1, s));
+      p.last_splits = S;
+      p.last_grid = grid;
+      p.last_kernel = 4;
     } else {
       int S, grid, cg;
       plan_tc(p, nq, a.KT, S, grid, cg);
       P = S * ams::kEpiHalves;
+      a.slots = (!a.gated && P >= a.k) ? 1 : 0;   // as launch_match_tc
       if (e0) AMS_CUDA_TRY(cudaEventRecord(e0, s));
       AMS_CUDA_TRY(ams::launch_match_tc(p, a, S, grid, cg, sorted, s));
       if (e1) AMS_CUDA_TRY(cudaEventRecord(e1, s));
@@ -710,6 +747,12 @@ ams_status_t ams_pool_read_profile(ams_pool_t pool, double* kernel_ms, int64_t* 
 ams_status_t ams_pool_launch_count(ams_pool_t pool, int64_t* launches) {
   if (pool == nullptr || launches == nullptr) return AMS_ERR_INVALID_ARGUMENT;
   *launches = pool->p.launches;
+  return AMS_OK;
+}
+
+ams_status_t ams_pool_set_kernel_policy(ams_pool_t pool, int32_t policy) {
+  if (pool == nullptr || policy < 0 || policy > 1) return AMS_ERR_INVALID_ARGUMENT;
+  pool->p.kernel_policy = policy;
   return AMS_OK;
 }
 

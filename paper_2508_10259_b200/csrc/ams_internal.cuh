@@ -133,6 +133,8 @@ struct Pool {
   CUtensorMap tmap_pool{};   // bf16 pool [cap_pad, d], box {64, 256}, SW128 (CTA tile)
   CUtensorMap tmap_pool2{};  // bf16 pool [cap_pad, d], box {64, 128}, SW128 (CTA-pair half tile)
   CUtensorMap tmap_q{};      // bf16 queries [q_pad, d], box {64, 128}, SW128
+  CUtensorMap tmap_qs[4]{};  // bf16 queries [q_pad, d], box {64, 16/32/64/128}, SW128 (small-batch kernel)
+  int32_t kernel_policy = 0; // 0: auto; 1: never the small-batch kernel (ams_pool_set_kernel_policy)
 
   void* nccl_comm = nullptr;  // ncclComm_t
 
@@ -160,6 +162,7 @@ struct MatchArgs {
   float g2;           // fp32(gate_radius^2); +inf disables the gate
   int32_t gated;      // g2 < +inf
   float threshold;
+  int32_t slots;      // the tcgen05 kernel filled p.slots (union bound) for the merge
 };
 
 cudaError_t launch_append(Pool& p, const void* emb_src, const float* joints_src, int64_t n_src,
@@ -175,6 +178,12 @@ cudaError_t launch_match_simt(Pool& p, const MatchArgs& a, int32_t splits, cudaS
 cudaError_t launch_match_tc(Pool& p, const MatchArgs& a, int32_t splits, int32_t grid, int32_t cg, bool sorted,
                             cudaStream_t s);
 int tc_query_tile(int cg);
+// small-batch kernel (pool rows on the MMA M side, queries on N): pipeline stages that fit
+// shared memory for this batch, 0 if the batch is not eligible (nq > 128, KT > 32, or
+// the per-warp lists would not fit)
+int scan_stages(const Pool& p, int nq, int KT);
+int scan_lists_per_split();
+cudaError_t launch_match_scan(Pool& p, const MatchArgs& a, int32_t splits, int32_t grid, cudaStream_t s);
 // merge [nq][P][KT] local lists -> [nq][k] (fp32, global int64); writes hit if out_hit != null
 // tc_bounds: the lists come from launch_match_tc, whose per-query lower bounds (p.bound,
 // p.slots) prune entries that cannot reach the top k

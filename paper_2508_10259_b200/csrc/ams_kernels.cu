@@ -472,7 +472,7 @@ cudaError_t launch_merge_partials(Pool& p, const MatchArgs& a, int32_t P, float*
   const auto& c = p.cfg;
   const unsigned g = blocks_for(a.nq, wpb);
   const uint32_t* bnd = tc_bounds ? p.bound : nullptr;
-  const uint32_t* sl = (tc_bounds && !a.gated && P >= a.k) ? p.slots : nullptr;   // as launch_match_tc
+  const uint32_t* sl = (tc_bounds && a.slots) ? p.slots : nullptr;   // filled by launch_match_tc
 #define AMS_MERGE(KT_)                                                                                 \
   merge_partials_kernel<KT_><<<g, wpb * 32, 0, s>>>(p.part_s, p.part_i, a.nq, P, a.k, out_s, out_i, out_hit, \
                                                      a.threshold, c.rank, c.world, p.B, bnd, sl, a.KT)

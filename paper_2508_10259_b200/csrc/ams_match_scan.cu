@@ -1,0 +1,534 @@
+// ams_match_scan.cu -- small-batch tcgen05 matcher (nq <= 128): pool rows on the MMA M
+// side, queries on N.
+//
+// Same method as ams_match_tc.cu (3.2.1 "comparing the similarity";
+// north_star metric, gate, top-k, tie rule):
+//   acc(i,j)  = sum_t q_it * e_jt          bf16 x bf16 -> fp32 on the tensor cores
+//   s(i,j)    = (acc * inv_q_i) * inv_e_j  fp32
+//   gate(i,j) = canonical fp32 sum_t (r_it - p_jt)^2 <= g2
+//   top-k by (s desc, j asc) per query.
+//
+// Why a second kernel.  A batch of nq <= 128 queries is HBM-bound (one pool row is
+// 2d bytes for 2*nq*d flop).  In match_tc_kernel the queries are the MMA M side, which
+// is 128 rows whatever nq is: a 1-query lookup does 128x the tensor work it needs.  On a
+// long scan at the 1 kW cap that wasted work is what sets the clock (C5 streaming: SM
+// clock 611-645 MHz median, and at that clock an M = 128 scan of d = 4096 rows is
+// tensor-bound, not HBM-bound).  Here the pool tile is the M side (two M = 128 MMAs per
+// 256-row tile) and the queries are N = round_up(nq, 32): the tensor work follows nq.
+//
+// Tiling: a tile is 256 pool rows (two 128-row MMA halves) x NQ queries, K advances 64
+// bf16 per pipeline stage (one 128-B swizzle atom).  TMEM: two accumulator buffers of
+// 2*NQ columns; half h of buffer b at columns b*2NQ + h*NQ, lane = pool row (mod 128).
+//
+// Warp roles (192 threads, 1 CTA/SM): warps 0..3 epilogue (warp w reads TMEM lanes
+// 32w.. = pool rows 32w+lane and 128+32w+lane of each tile), warp 4 TMA producer
+// (pool + query tiles into a STAGES ring, per-tile joints/inv_norm into a 2-deep aux
+// ring), warp 5 TMEM allocator + tcgen05.mma issuer.
+//
+// Epilogue, per warp, half tile (32 rows) and 32-query slot: one tcgen05.ld.x32 gives
+// lane r the raw scores of row r against the slot's 32 queries.  Lanes are rows here,
+// but the running top-k lists are per query, so each warp keeps them in registers
+// with lane q owning query (slot*32 + q) -- the same register TopK as match_tc_kernel.
+// A row-side filter decides whether the block can touch any list: gated, the
+// canonical partial distance over joints 0..3 (a lower bound of the full sum: RN is
+// monotone and every term >= 0), then the exact canonical gate for the pairs that
+// pass; ungated, the exact score against the query's threshold (mirrored in shared
+// memory as max(KT-th best, shared bound)).  Only then is the 32x32 block of scores
+// (-inf where ineligible) transposed through shared memory (padded rows: conflict-
+// free) so lane q scans its query's 32 rows in increasing row order and inserts with
+// TopK::insert_monotone.  Lists are per (query, split, warp) and go to the same
+// [nq][P][KT] partial layout merge_partials_kernel merges; the per-query bound in
+// global memory is shared across CTAs exactly as in match_tc_kernel (a list's KT-th
+// best is <= the global k-th best, so s < bound can never enter; s == bound is kept
+// for the index tie rule), refreshed on a geometric tile schedule.
+#include <cuda_bf16.h>
+#include <math_constants.h>
+
+#include "ams_internal.cuh"
+#include "ams_ptx.cuh"
+#include "ams_topk.cuh"
+
+namespace ams {
+namespace {
+
+constexpr int kScanEpiWarps = 4;
+constexpr int kScanThreads = 32 * (kScanEpiWarps + 2);   // 192
+constexpr uint32_t kScanABytes = kBlockN * kBlockK * 2;  // 32 KB: 256 pool rows x 128 B
+constexpr uint32_t kScanHalfBytes = kScanABytes / 2;     // 128 rows: the second MMA half
+constexpr int kScanListRegs = 1024;                      // max (32-query slots) x KT per lane
+constexpr size_t kSmemLimit = 232448;                    // max dynamic smem per CTA (227 KB)
+constexpr int kTPad = 33;                                // transpose row stride (floats)
+
+struct ScanParams {
+  const float* inv_q;        // [q_pad]
+  const float* q_joints;     // [q_pad, JP]
+  const float* pool_inv;     // [cap_pad]
+  const float* pool_joints;  // [cap_pad/256][JP][256]
+  float* part_s;             // [nq][P][KT]
+  int32_t* part_i;
+  uint32_t* bound;           // [nq] ordered-u32 admission lower bound (0 = none)
+  uint32_t* slots;           // [nq][KT] union-bound slots (ordered-u32; ungated with P >= k, else null)
+  int64_t L;                 // local rows
+  int32_t nq, NQ, d, n_pt, S, P, stages, k;
+  uint32_t b_bytes;          // query stage bytes (box rows x 128 B)
+  uint32_t idesc;            // kind::f16, M = 128, N = NQ
+  float g2;
+};
+
+// shared-memory layout (byte offsets from the 1024-aligned base), host and device
+struct ScanLayout {
+  uint32_t a, b, aux, tr, qj, iq, thr, bars, total;
+};
+
+__host__ __device__ inline ScanLayout scan_layout(int stages, uint32_t b_bytes, int JP, int NQ) {
+  ScanLayout l{};
+  uint32_t o = 0;
+  l.a = o;
+  o += (uint32_t)stages * kScanABytes;
+  l.b = o;
+  o += (uint32_t)stages * b_bytes;
+  l.aux = o;
+  o += 2u * (uint32_t)(kBlockN * JP * 4 + kBlockN * 4);
+  l.tr = o;
+  o += (uint32_t)(kScanEpiWarps * 32 * kTPad * 4 + 64);   // + keep 16-B alignment below
+  l.qj = o;
+  o += (uint32_t)(JP * NQ * 4);
+  l.iq = o;
+  o += (uint32_t)(NQ * 4);
+  l.thr = o;
+  o += (uint32_t)(kScanEpiWarps * NQ * 4);
+  l.bars = o;
+  o += 256;
+  l.total = o + 1024;   // alignment slack
+  return l;
+}
+
+__device__ __forceinline__ void scan_split(int sp, int S, int n_pt, int& t_lo, int& t_hi) {
+  t_lo = (int)((int64_t)sp * n_pt / S);
+  t_hi = (int)((int64_t)(sp + 1) * n_pt / S);
+}
+
+template <int KT, int JP, bool GATED>
+__global__ void __launch_bounds__(kScanThreads, 1)
+    match_scan_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_pool,
+                      const ScanParams prm) {
+  constexpr uint32_t AUXJ = kBlockN * JP * 4;
+  constexpr uint32_t AUX = AUXJ + kBlockN * 4;
+  constexpr int NSL = kScanListRegs / (32 * KT);   // 32-query slots a lane can own
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+  const int NQ = prm.NQ;
+  const int STAGES = prm.stages;
+  const ScanLayout lay = scan_layout(STAGES, prm.b_bytes, JP, NQ);
+  uint8_t* sA = smem + lay.a;
+  uint8_t* sB = smem + lay.b;
+  uint8_t* sAux = smem + lay.aux;
+  float* trs = reinterpret_cast<float*>(smem + lay.tr);   // [warps][32][kTPad]
+  float* qjs = reinterpret_cast<float*>(smem + lay.qj);   // [JP][NQ]
+  float* iqs = reinterpret_cast<float*>(smem + lay.iq);   // [NQ]
+  float* thr = reinterpret_cast<float*>(smem + lay.thr);  // [warps][NQ]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + lay.bars);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + STAGES;
+  uint64_t* tfull = bars + 2 * STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* afull = tfull + 4;
+  uint64_t* aempty = tfull + 6;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tfull + 8);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  constexpr int kProducerWarp = kScanEpiWarps, kMmaWarp = kScanEpiWarps + 1;
+  if (warp == kProducerWarp && lane == 0) {
+    ptx::prefetch_tmap(&tmap_q);
+    ptx::prefetch_tmap(&tmap_pool);
+    for (int i = 0; i < STAGES; ++i) {
+      ptx::mbar_init(&full[i], 1);
+      ptx::mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&tfull[i], 1);
+      ptx::mbar_init(&tempty[i], kScanEpiWarps);
+      ptx::mbar_init(&afull[i], 1);
+      ptx::mbar_init(&aempty[i], kScanEpiWarps);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == kMmaWarp) {
+    ptx::tmem_alloc<1>(tmem_holder, 512);
+    ptx::tmem_relinquish<1>();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  const int n_kb = prm.d / kBlockK;
+
+  if (warp == kProducerWarp) {
+    // ------------------------------------------------------------ TMA producer
+    const uint64_t pol_q = ptx::policy_evict_last();
+    const uint64_t pol_pool = ptx::policy_evict_first();   // every pool byte is read once
+    const uint32_t tx = kScanABytes + prm.b_bytes;
+    int stage = 0;
+    uint32_t phase = 0, tile_count = 0;
+    for (int u = blockIdx.x; u < prm.S; u += gridDim.x) {
+      int t_lo, t_hi;
+      scan_split(u, prm.S, prm.n_pt, t_lo, t_hi);
+      for (int t = t_lo; t < t_hi; ++t, ++tile_count) {
+        const int buf = tile_count & 1;
+        const uint32_t use = tile_count >> 1;
+        ptx::mbar_wait(&aempty[buf], (use & 1u) ^ 1u);
+        if (ptx::elect_one()) {
+          uint8_t* aux = sAux + buf * AUX;
+          ptx::mbar_arrive_expect_tx(&afull[buf], AUX);
+          ptx::bulk_load(aux, prm.pool_joints + (int64_t)t * kBlockN * JP, AUXJ, &afull[buf]);
+          ptx::bulk_load(aux + AUXJ, prm.pool_inv + (int64_t)t * kBlockN, kBlockN * 4, &afull[buf]);
+        }
+        __syncwarp();
+        for (int kb = 0; kb < n_kb; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1u);
+          if (ptx::elect_one()) {
+            ptx::mbar_arrive_expect_tx(&full[stage], tx);
+            ptx::tma_load_2d(sA + stage * kScanABytes, &tmap_pool, &full[stage], kb * kBlockK, t * kBlockN, pol_pool);
+            ptx::tma_load_2d(sB + stage * prm.b_bytes, &tmap_q, &full[stage], kb * kBlockK, 0, pol_q);
+          }
+          __syncwarp();
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    // ------------------------------------------------------------ MMA issuer
+    const uint64_t da0 = ptx::sdesc_k_sw128(ptx::smem_u32(sA));
+    const uint64_t db0 = ptx::sdesc_k_sw128(ptx::smem_u32(sB));
+    int stage = 0;
+    uint32_t phase = 0, tile_count = 0;
+    for (int u = blockIdx.x; u < prm.S; u += gridDim.x) {
+      int t_lo, t_hi;
+      scan_split(u, prm.S, prm.n_pt, t_lo, t_hi);
+      for (int t = t_lo; t < t_hi; ++t, ++tile_count) {
+        const int buf = tile_count & 1;
+        const uint32_t use = tile_count >> 1;
+        ptx::mbar_wait(&tempty[buf], (use & 1u) ^ 1u);
+        ptx::tc_fence_after();
+        const uint32_t d0 = tmem_base + (uint32_t)(buf * 2 * NQ);
+        for (int kb = 0; kb < n_kb; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          if (ptx::elect_one()) {
+            const uint64_t da = da0 + (uint64_t)((uint32_t)stage * (kScanABytes >> 4));
+            const uint64_t db = db0 + (uint64_t)((uint32_t)stage * (prm.b_bytes >> 4));
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+              for (int kk = 0; kk < kBlockK / 16; ++kk)
+                ptx::umma_f16<1>(d0 + (uint32_t)(h * NQ), da + (uint64_t)(h * (kScanHalfBytes >> 4) + 2 * kk),
+                                 db + (uint64_t)(2 * kk), prm.idesc, (kb | kk) != 0 ? 1u : 0u);
+            ptx::umma_commit<1>(&empty[stage]);
+          }
+          __syncwarp();
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+        if (ptx::elect_one()) ptx::umma_commit<1>(&tfull[buf]);
+        __syncwarp();
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int lg = warp;   // TMEM lanes 32*lg..: rows 32*lg + lane and 128 + 32*lg + lane
+    const int nq = prm.nq;
+    const int nsl = NQ / 32;   // 32-query slots in use (<= NSL)
+    for (int i = threadIdx.x; i < NQ * JP; i += 32 * kScanEpiWarps) {
+      const int c = i / JP, t = i % JP;
+      qjs[t * NQ + c] = c < nq ? prm.q_joints[(int64_t)c * JP + t] : 0.0f;
+    }
+    for (int c = threadIdx.x; c < NQ; c += 32 * kScanEpiWarps) iqs[c] = c < nq ? prm.inv_q[c] : 0.0f;
+    ptx::named_bar_sync(1, 32 * kScanEpiWarps);
+    float* tr = trs + lg * 32 * kTPad;
+    float* mythr = thr + lg * NQ;
+    uint32_t tile_count = 0;
+    for (int u = blockIdx.x; u < prm.S; u += gridDim.x) {
+      int t_lo, t_hi;
+      scan_split(u, prm.S, prm.n_pt, t_lo, t_hi);
+      // lane q owns query sl*32 + q of every slot sl: its list and its shared bound
+      TopK<KT, int32_t> top[NSL];
+      float bnd[NSL];
+#pragma unroll
+      for (int sl = 0; sl < NSL; ++sl) {
+        const int c = sl * 32 + lane;
+        const bool act = sl < nsl && c < nq;
+        top[sl].init(act);   // inactive: kth = +inf, never admits
+        bnd[sl] = -CUDART_INF_F;
+        if (act) {
+          const uint32_t v = ptx::ld_relaxed_gpu(prm.bound + c);
+          if (v) bnd[sl] = ptx::ord2f(v);
+        }
+        if (sl < nsl) mythr[c] = act ? bnd[sl] : CUDART_INF_F;
+      }
+      __syncwarp();
+      for (int t = t_lo; t < t_hi; ++t, ++tile_count) {
+        const int buf = tile_count & 1;
+        const uint32_t use = tile_count >> 1;
+        ptx::mbar_wait(&afull[buf], use & 1u);
+        ptx::mbar_wait(&tfull[buf], use & 1u);
+        ptx::tc_fence_after();
+        const float* jsm = reinterpret_cast<const float*>(sAux + buf * AUX);
+        const float* inv_sm = reinterpret_cast<const float*>(sAux + buf * AUX + AUXJ);
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+          const int r = h * 128 + lg * 32 + lane;   // row within the tile
+          const int32_t rowbase = t * kBlockN + h * 128 + lg * 32;
+          const bool valid = (int64_t)rowbase + lane < prm.L;
+          float pj[JP];
+#pragma unroll
+          for (int tj = 0; tj < JP; ++tj) pj[tj] = jsm[tj * kBlockN + r];
+          const float ie = inv_sm[r];
+          const uint64_t IE2 = ptx::pack2(ie, ie);
+#pragma unroll
+          for (int sl = 0; sl < NSL; ++sl) {
+            if (sl >= nsl) break;
+            const int c0 = sl * 32;
+            const uint32_t taddr =
+                tmem_base + ((uint32_t)(lg * 32) << 16) + (uint32_t)(buf * 2 * NQ + h * NQ + c0);
+            uint32_t elig = valid ? 0xFFFFFFFFu : 0u;   // pairs (this row, query c0 + c) that may enter
+            if (GATED) {
+              // partial canonical distance over joints 0..3 for the 32 queries, two at a time
+              uint32_t fire = 0;
+              uint64_t PP[4];
+#pragma unroll
+              for (int tj = 0; tj < 4; ++tj) PP[tj] = ptx::pack2(pj[tj], pj[tj]);   // JP >= 4
+#pragma unroll
+              for (int g = 0; g < 32; g += 4) {
+                uint64_t da = 0ull, db = 0ull;
+#pragma unroll
+                for (int tj = 0; tj < 4; ++tj) {
+                  const ulonglong2 q4 = *reinterpret_cast<const ulonglong2*>(qjs + tj * NQ + c0 + g);
+                  const uint64_t a = ptx::sub2(q4.x, PP[tj]);
+                  da = ptx::fma2(a, a, da);
+                  const uint64_t b = ptx::sub2(q4.y, PP[tj]);
+                  db = ptx::fma2(b, b, db);
+                }
+                fire |= (ptx::lo2(da) <= prm.g2 ? 1u : 0u) << g;
+                fire |= (ptx::hi2(da) <= prm.g2 ? 1u : 0u) << (g + 1);
+                fire |= (ptx::lo2(db) <= prm.g2 ? 1u : 0u) << (g + 2);
+                fire |= (ptx::hi2(db) <= prm.g2 ? 1u : 0u) << (g + 3);
+              }
+              fire &= elig;
+              if (__reduce_or_sync(0xffffffffu, fire) == 0u) continue;   // the common case
+              // exact canonical gate for the surviving pairs of this lane
+              elig = 0u;
+              while (fire != 0u) {
+                const int c = __ffs(fire) - 1;
+                fire &= fire - 1u;
+                float ds = 0.0f;
+#pragma unroll
+                for (int tj = 0; tj < JP; ++tj) {
+                  const float df = __fsub_rn(qjs[tj * NQ + c0 + c], pj[tj]);
+                  ds = __fmaf_rn(df, df, ds);
+                }
+                if (ds <= prm.g2) elig |= 1u << c;
+              }
+              if (__reduce_or_sync(0xffffffffu, elig) == 0u) continue;
+            }
+            // exact scores of the block (kept in v), then the threshold test
+            uint32_t v[32];
+            __syncwarp();
+            ptx::tmem_ld32(taddr, v);
+            ptx::tmem_wait_ld();
+            uint32_t fire = 0;
+#pragma unroll
+            for (int g = 0; g < 32; g += 2) {
+              const uint64_t a = ptx::pack2(__uint_as_float(v[g]), __uint_as_float(v[g + 1]));
+              const uint64_t iq2 = *reinterpret_cast<const uint64_t*>(iqs + c0 + g);
+              const uint64_t s2 = ptx::mul2(ptx::mul2(a, iq2), IE2);   // RN(RN(acc * iq) * ie)
+              const float2 th = *reinterpret_cast<const float2*>(mythr + c0 + g);
+              v[g] = __float_as_uint(ptx::lo2(s2));
+              v[g + 1] = __float_as_uint(ptx::hi2(s2));
+              fire |= (ptx::lo2(s2) >= th.x ? 1u : 0u) << g;
+              fire |= (ptx::hi2(s2) >= th.y ? 1u : 0u) << (g + 1);
+            }
+            fire &= elig;
+            if (__reduce_or_sync(0xffffffffu, fire) == 0u) continue;
+            // transpose (-inf where the pair cannot enter): lane q gets query c0 + q's
+            // scores of the warp's 32 rows
+#pragma unroll
+            for (int c = 0; c < 32; ++c)
+              tr[c * kTPad + lane] = ((fire >> c) & 1u) != 0u ? __uint_as_float(v[c]) : -CUDART_INF_F;
+            __syncwarp();
+            {
+              TopK<KT, int32_t>& tp = top[sl];
+              const float b = bnd[sl];
+#pragma unroll 4
+              for (int rr = 0; rr < 32; ++rr) {
+                const float x = tr[lane * kTPad + rr];
+                if (x > tp.kth_s && x >= b) tp.insert_monotone(x, rowbase + rr, 0);
+              }
+              mythr[c0 + lane] = fmaxf(mythr[c0 + lane], tp.kth_s);
+            }
+            __syncwarp();
+          }
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          ptx::mbar_arrive(&tempty[buf]);
+          ptx::mbar_arrive(&aempty[buf]);
+        }
+        // share the admission bound with the other CTAs (publish improvements only).
+        // Geometric schedule (after 1, 2, 4, 8, ... tiles of the unit, and at its end):
+        // thresholds move fast early and slowly later, and each refresh is a chain of
+        // L2 round trips that one epilogue warp per sub-partition cannot hide (ncu: the
+        // per-tile refresh was the top stall of the ungated scan).
+        const int done = t - t_lo + 1;
+        const bool refresh = (done & (done - 1)) == 0 || t + 1 == t_hi;
+#pragma unroll
+        for (int sl = 0; sl < NSL; ++sl) {
+          const int c = sl * 32 + lane;
+          if (refresh && sl < nsl && c < nq) {
+            uint32_t b = ptx::ld_relaxed_gpu(prm.bound + c);
+            const float kth = top[sl].kth_s;
+            if (kth > -CUDART_INF_F) {
+              const uint32_t o = ptx::f2ord(kth);
+              if (o > b) {
+                atomicMax(prm.bound + c, o);
+                b = o;
+              }
+            }
+            if (b) bnd[sl] = fmaxf(bnd[sl], ptx::ord2f(b));
+            if (prm.slots != nullptr) {
+              // union bound (as match_tc_kernel): list l keeps its best score in slot
+              // l mod k; the lists hold disjoint rows, so once all k slots are filled
+              // their minimum is the score of one of k distinct rows, <= the k-th best
+              uint32_t* sq = prm.slots + (int64_t)c * KT;
+              const int l = u * kScanEpiWarps + lg;
+              if (top[sl].s[0] > -CUDART_INF_F) atomicMax(sq + l % prm.k, ptx::f2ord(top[sl].s[0]));
+              uint32_t mn = 0xFFFFFFFFu;
+#pragma unroll
+              for (int rr = 0; rr < KT; rr += 4) {
+                const uint4 w = __ldcg(reinterpret_cast<const uint4*>(sq + rr));
+                mn = min(mn, min(min(rr < prm.k ? w.x : ~0u, rr + 1 < prm.k ? w.y : ~0u),
+                                 min(rr + 2 < prm.k ? w.z : ~0u, rr + 3 < prm.k ? w.w : ~0u)));
+              }
+              if (mn != 0u) bnd[sl] = fmaxf(bnd[sl], ptx::ord2f(mn));
+            }
+            mythr[c] = fmaxf(bnd[sl], kth);
+          }
+        }
+        __syncwarp();
+      }
+      // this unit's lists -> partials [nq][P][KT] (list index = split * warps + warp)
+#pragma unroll
+      for (int sl = 0; sl < NSL; ++sl) {
+        const int c = sl * 32 + lane;
+        if (sl < nsl && c < nq) {
+          const int64_t base = ((int64_t)c * prm.P + (int64_t)u * kScanEpiWarps + lg) * KT;
+#pragma unroll
+          for (int rr = 0; rr < KT; rr += 4) {
+            *reinterpret_cast<float4*>(prm.part_s + base + rr) =
+                make_float4(top[sl].s[rr], top[sl].s[rr + 1], top[sl].s[rr + 2], top[sl].s[rr + 3]);
+            *reinterpret_cast<int4*>(prm.part_i + base + rr) =
+                make_int4(top[sl].i[rr], top[sl].i[rr + 1], top[sl].i[rr + 2], top[sl].i[rr + 3]);
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == kMmaWarp) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<1>(tmem_base, 512);
+  }
+}
+
+// Query-tile box (TMA rows) for a batch: the smallest encoded box >= NQ.
+int scan_box(int NQ) { return NQ <= 32 ? 32 : NQ <= 64 ? 64 : 128; }
+int box_index(int box) { return box == 16 ? 0 : box == 32 ? 1 : box == 64 ? 2 : 3; }
+
+template <int KT, int JP, bool G>
+cudaError_t launch_scan_t(Pool& p, const ScanParams& prm, int box, int grid, cudaStream_t s) {
+  auto kern = match_scan_kernel<KT, JP, G>;
+  const size_t smem = scan_layout(prm.stages, prm.b_bytes, JP, prm.NQ).total;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<grid, kScanThreads, smem, s>>>(p.tmap_qs[box_index(box)], p.tmap_pool, prm);
+  return cudaGetLastError();
+}
+
+template <int KT, bool G>
+cudaError_t launch_scan_kt(Pool& p, const ScanParams& prm, int box, int grid, cudaStream_t s) {
+  switch (p.JP) {
+    case 4: return launch_scan_t<KT, 4, G>(p, prm, box, grid, s);
+    case 8: return launch_scan_t<KT, 8, G>(p, prm, box, grid, s);
+    default: return launch_scan_t<KT, 16, G>(p, prm, box, grid, s);
+  }
+}
+
+template <bool G>
+cudaError_t launch_scan_g(Pool& p, const MatchArgs& a, const ScanParams& prm, int box, int grid, cudaStream_t s) {
+  switch (a.KT) {
+    case 8: return launch_scan_kt<8, G>(p, prm, box, grid, s);
+    case 16: return launch_scan_kt<16, G>(p, prm, box, grid, s);
+    default: return launch_scan_kt<32, G>(p, prm, box, grid, s);
+  }
+}
+
+}  // namespace
+
+int scan_stages(const Pool& p, int nq, int KT) {
+  if (nq < 1 || nq > kBlockM || KT > 32) return 0;
+  const int NQ = (nq + 31) / 32 * 32;
+  if (NQ * KT > kScanListRegs) return 0;   // register lists: (NQ / 32) x KT entries per lane
+  const uint32_t b_bytes = (uint32_t)scan_box(NQ) * kBlockK * 2;
+  for (int st = 6; st >= 3; --st)
+    if (scan_layout(st, b_bytes, p.JP, NQ).total <= kSmemLimit) return st;
+  return 0;
+}
+
+cudaError_t launch_match_scan(Pool& p, const MatchArgs& a, int32_t S, int32_t grid, cudaStream_t s) {
+  ScanParams prm{};
+  const int NQ = (a.nq + 31) / 32 * 32;
+  const int box = scan_box(NQ);
+  prm.inv_q = p.q_inv;
+  prm.q_joints = p.q_joints;
+  prm.pool_inv = p.inv_norm;
+  prm.pool_joints = p.joints;
+  prm.part_s = p.part_s;
+  prm.part_i = p.part_i;
+  prm.bound = p.bound;
+  prm.L = p.local;
+  prm.nq = a.nq;
+  prm.NQ = NQ;
+  prm.d = p.cfg.dim;
+  prm.n_pt = (int32_t)((p.local + kBlockN - 1) / kBlockN);
+  prm.S = S;
+  prm.P = S * kScanEpiWarps;
+  prm.stages = scan_stages(p, a.nq, a.KT);
+  prm.b_bytes = (uint32_t)box * kBlockK * 2;
+  prm.idesc = ptx::idesc_bf16_f32(kBlockM, (uint32_t)NQ);
+  prm.g2 = a.g2;
+  prm.k = a.k;
+  if (prm.stages == 0) return cudaErrorInvalidValue;
+  cudaError_t e = cudaMemsetAsync(p.bound, 0, (size_t)(a.nq + 1) * sizeof(uint32_t), s);
+  if (e != cudaSuccess) return e;
+  prm.slots = a.slots ? p.slots : nullptr;
+  if (prm.slots != nullptr) {
+    e = cudaMemsetAsync(p.slots, 0, (size_t)a.nq * a.KT * sizeof(uint32_t), s);
+    if (e != cudaSuccess) return e;
+  }
+  e = a.gated ? launch_scan_g<true>(p, a, prm, box, grid, s) : launch_scan_g<false>(p, a, prm, box, grid, s);
+  ++p.launches;
+  return e;
+}
+
+int scan_lists_per_split() { return kScanEpiWarps; }
+
+}  // namespace ams

@@ -667,7 +667,7 @@ cudaError_t launch_match_tc(Pool& p, const MatchArgs& a, int32_t S, int32_t grid
   cudaError_t e = cudaMemsetAsync(p.bound, 0, (size_t)(a.nq + 1) * sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
   // ungated: the union bound needs >= k lists per query (each list fills one slot)
-  prm.slots = (!a.gated && prm.P >= a.k) ? p.slots : nullptr;
+  prm.slots = (!a.gated && prm.P >= a.k) ? p.slots : nullptr;   // a.slots says so to the merge
   if (prm.slots != nullptr) {
     e = cudaMemsetAsync(p.slots, 0, (size_t)prm.n_qt * kBlockM * cg * a.KT * sizeof(uint32_t), s);
     if (e != cudaSuccess) return e;

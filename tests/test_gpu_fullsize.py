@@ -83,13 +83,16 @@ def test_c3_full_size_ungated_sampled(ams, c3):
 
 
 def test_c3_scan_64_sampled(ams, c3):
-    """The north_star 64-query scan (single-CTA kernel, 148 row splits)."""
+    """The north_star 64-query scan: the small-batch kernel (plan id 4) and the
+    128-query-tile kernel (plan id 1), both on 100+ row splits."""
     cfg, pool, q, qj, labels, host_e, host_j = c3
-    for gamma in (cfg.gamma, INF):
+    for gamma, policy in ((cfg.gamma, 0), (INF, 0), (cfg.gamma, 1), (INF, 1)):
+        ams.ams_pool_set_kernel_policy(pool.handle, policy)
         gi, gs, gh = (t.cpu().numpy() for t in pool.match(q[:64].contiguous(), qj[:64].contiguous(), cfg.k,
                                                            cfg.theta, gamma))
+        ams.ams_pool_set_kernel_policy(pool.handle, 0)
         plan = ams.ams_pool_last_plan(pool.handle)
-        assert plan["kernel_id"] == 1 and plan["splits"] >= 100
+        assert plan["kernel_id"] == (4 if policy == 0 else 1) and plan["splits"] >= 100
         qn = q[:64].view(torch.int16).cpu().numpy().view(np.uint16)
         sel = np.arange(0, 64, 2) if gamma == INF else np.arange(64)
         orc = oracle.match(host_e, host_j, qn[sel], qj[:64].cpu().numpy()[sel], cfg.k, cfg.theta, gamma,

@@ -190,6 +190,10 @@ def test_plan_uses_cta_pairs_and_splits(ams):
         assert plan["kernel_id"] == 2 and plan["grid"] % 2 == 0 and plan["splits"] >= 1
         pool.match(to_dev(w.q_emb[:64]), to_dev(w.q_joints[:64]), cfg.k, cfg.theta, INF)
         plan = ams.ams_pool_last_plan(pool.handle)
+        assert plan["kernel_id"] == 4 and plan["splits"] > 1 and plan["partials"] == 4 * plan["splits"]
+        ams.ams_pool_set_kernel_policy(pool.handle, 1)
+        pool.match(to_dev(w.q_emb[:64]), to_dev(w.q_joints[:64]), cfg.k, cfg.theta, INF)
+        plan = ams.ams_pool_last_plan(pool.handle)
         assert plan["kernel_id"] == 1 and plan["splits"] > 1
         torch.cuda.synchronize()
 
