@@ -523,7 +523,8 @@ def main():
     if not args.gate_first and cfg.Q <= 128:   # below the ridge (~250 flop/B): HBM-bound scan
         gbs = (bytes_step / world) / (kern_avg / 1e3) / 1e9
         roofline = {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                    "frac": gbs / peaks["hbm_gbs"], "traffic": load_traffic(args.workload, "match_tc"),
+                    "frac": gbs / peaks["hbm_gbs"],
+                    "traffic": load_traffic(args.workload, "match_scan" if plan.get("kernel_id") == 4 else "match_tc"),
                     "kernel": "match_scan_kernel" if plan.get("kernel_id") == 4 else "match_tc_kernel",
                     "algorithmic_per_launch": {"bytes": bytes_step / world, "flop": flops_launch},
                     "kernel_ms_avg": kern_avg, "kernel_share_of_step": kern_avg / (t_ms / args.steps),
@@ -561,6 +562,7 @@ def main():
         barrier()
         ams.ams_pool_set_profiling(pool.handle, False)
         s_ms = max_over_ranks(ev0.elapsed_time(ev1)) / reps
+        s_plan = ams.ams_pool_last_plan(pool.handle)
         k_ms, k_n = ams.ams_pool_read_profile(pool.handle)
         k_avg = max_over_ranks(k_ms / max(k_n, 1))
         gbs_kernel = (bytes_step / world) / (k_avg / 1e3) / 1e9
@@ -570,7 +572,9 @@ def main():
                              "frac": gbs_kernel / peaks["hbm_gbs"],
                              "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks["source"] == "measured"
                              else "fallback 6650 GB/s (B200_PROFILING.md; MEASURED_PEAKS.json absent)",
-                             "traffic": load_traffic(args.workload, "match_tc_scan"),
+                             "traffic": load_traffic(args.workload, "match_scan" if s_plan["kernel_id"] == 4
+                                                     else "match_tc_scan"),
+                             "kernel": "match_scan_kernel" if s_plan["kernel_id"] == 4 else "match_tc_kernel",
                              "kernel_ms_avg": k_avg, "frac_vs_datasheet_8000": gbs_kernel / 8000.0,
                              "algorithmic_bytes_per_launch": bytes_step / world}}
 
