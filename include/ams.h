@@ -350,8 +350,9 @@ ams_status_t ams_pool_launch_count(ams_pool_t pool, int64_t* launches);
  * may be NULL. */
 /* Kernel choice for bf16 ams_match calls (results are the same either way, within the
  * bf16 tolerances: the fp32 tensor-core sums of a pair may round differently).
- * policy 0 (default): batches of nq <= 128 (ungrouped, k <= 32, lists fitting shared
- * memory) use the small-batch kernel (plan id 4); policy 1: they use the 128-query-tile
+ * policy 0 (default): batches of nq <= 128 with k <= 32 and round_up(nq, 32) * KT <= 2048
+ * (KT = k rounded up to 8/16/32; the per-lane register lists) use the small-batch kernel
+ * (plan id 4); policy 1: they use the 128-query-tile
  * kernel (plan id 1).  For A/B measurements and tests.  Host-only; takes effect at the
  * next ams_match.  AMS_ERR_INVALID_ARGUMENT for a NULL pool or another policy. */
 ams_status_t ams_pool_set_kernel_policy(ams_pool_t pool, int32_t policy);

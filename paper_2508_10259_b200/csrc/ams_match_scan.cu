@@ -55,7 +55,7 @@ constexpr int kScanEpiWarps = 4;
 constexpr int kScanThreads = 32 * (kScanEpiWarps + 2);   // 192
 constexpr uint32_t kScanABytes = kBlockN * kBlockK * 2;  // 32 KB: 256 pool rows x 128 B
 constexpr uint32_t kScanHalfBytes = kScanABytes / 2;     // 128 rows: the second MMA half
-constexpr int kScanListRegs = 1024;                      // max (32-query slots) x KT per lane
+constexpr int kScanListRegs = 2048;                      // max (32-query slots) x KT per lane
 constexpr size_t kSmemLimit = 232448;                    // max dynamic smem per CTA (227 KB)
 constexpr int kTPad = 33;                                // transpose row stride (floats)
 
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(kScanThreads, 1)
                       const ScanParams prm) {
   constexpr uint32_t AUXJ = kBlockN * JP * 4;
   constexpr uint32_t AUX = AUXJ + kBlockN * 4;
-  constexpr int NSL = kScanListRegs / (32 * KT);   // 32-query slots a lane can own
+  constexpr int NSL = kScanListRegs / (32 * KT) < 4 ? kScanListRegs / (32 * KT) : 4;   // 32-query slots per lane (nq <= 128)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   const int NQ = prm.NQ;

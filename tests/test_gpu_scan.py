@@ -5,7 +5,7 @@ kernel (plan id 1) on the same inputs.
 Covers every query-box size (NQ = 32, 64, 128 = round_up(nq, 32)),
 KT in {8, 16, 32}, the JP = 4 / 8 / 16 joint strides, ragged pools (tiles of 256 rows
 with a partial last tile, pools smaller than one tile), both gate modes, the
-eligibility limits (k > 32 or round_up(nq, 32) * KT > 1024 fall back to plan id 1), exact ties across
+eligibility limits (k > 32 or round_up(nq, 32) * KT > 2048 fall back to plan id 1), exact ties across
 splits, and appends between calls.  Expected values come only from oracle/.
 """
 import numpy as np
@@ -31,10 +31,10 @@ def dev_t(a):
 
 
 def scan_eligible(nq, k):
-    """The library's rule: nq <= 128, KT <= 32 and round_up(nq, 32) * KT <= 1024 (the
+    """The library's rule: nq <= 128, KT <= 32 and round_up(nq, 32) * KT <= 2048 (the
     per-lane register lists)."""
     KT = 8 if k <= 8 else 16 if k <= 16 else 32 if k <= 32 else 64
-    return nq <= 128 and KT <= 32 and -(-nq // 32) * 32 * KT <= 1024
+    return nq <= 128 and KT <= 32 and -(-nq // 32) * 32 * KT <= 2048
 
 
 def run(ams, pool, q, qj, k, theta, gamma, policy=0):
