@@ -132,9 +132,10 @@ def parse():
     ap.add_argument("--gate-first", action="store_true",
                     help="time ams_match_gate_first (SURVEY 8(f) f3 variant) instead of the dense ams_match")
     ap.add_argument("--no-variant", action="store_true", help="skip the gate-first side measurement")
-    ap.add_argument("--kernel-policy", type=int, default=0, choices=[0, 1],
-                    help="1: batches of <= 128 queries use the 128-query-tile kernel instead of the "
-                         "small-batch kernel (A/B measurement)")
+    ap.add_argument("--kernel-policy", type=int, default=0, choices=[0, 1, 2, 3],
+                    help="bit mask for A/B measurements: 1 = batches of <= 128 queries use the 128-query-tile "
+                         "kernel instead of the small-batch kernel; 2 = two CTA pairs per 4-CTA cluster sharing "
+                         "multicast pool rows (opt-in)")
     return ap.parse_args()
 
 

@@ -345,16 +345,23 @@ ams_status_t ams_pool_launch_count(ams_pool_t pool, int64_t* launches);
 
 /* Describes the last ams_match launch plan: number of row splits, partial lists per
  * query, grid size, dominant-kernel id (0 = fp32 SIMT; 1 = tcgen05, one CTA per
- * 128-query tile; 2 = tcgen05 CTA pair per 256-query tile; 4 = tcgen05 small-batch
- * kernel with pool rows on the MMA M side and the nq <= 128 queries on N). Any pointer
- * may be NULL. */
-/* Kernel choice for bf16 ams_match calls (results are the same either way, within the
- * bf16 tolerances: the fp32 tensor-core sums of a pair may round differently).
- * policy 0 (default): batches of nq <= 128 with k <= 32 and round_up(nq, 32) * KT <= 2048
- * (KT = k rounded up to 8/16/32; the per-lane register lists) use the small-batch kernel
- * (plan id 4); policy 1: they use the 128-query-tile
- * kernel (plan id 1).  For A/B measurements and tests.  Host-only; takes effect at the
- * next ams_match.  AMS_ERR_INVALID_ARGUMENT for a NULL pool or another policy. */
+ * 128-query tile; 2 = tcgen05 CTA pair per 256-query tile; 3 = gate-first variant;
+ * 4 = tcgen05 small-batch kernel with pool rows on the MMA M side and the nq <= 128
+ * queries on N; 5 = as 2, with two CTA pairs per 4-CTA cluster sharing multicast pool
+ * rows). Any pointer may be NULL. */
+/* Kernel choice for bf16 ams_match calls, for A/B measurements and tests (results are
+ * the same either way, within the bf16 tolerances: the small-batch kernel's fp32
+ * tensor-core sums of a pair may round differently; the cluster modes are bit-identical).
+ * policy is a bit mask, 0 = default:
+ *   bit 0 set: batches of nq <= 128 use the 128-query-tile kernel (plan id 1) instead of
+ *     the small-batch kernel (plan id 4; used when k <= 32 and round_up(nq, 32) * KT <=
+ *     2048, KT = k rounded up to 8/16/32: the per-lane register lists);
+ *   bit 1 set: batches with an even number of 256-query tiles use two CTA pairs per
+ *     4-CTA cluster sharing multicast pool rows (plan id 5) instead of one pair per
+ *     cluster (plan id 2).  Opt-in: only the co-resident 4-CTA clusters are launched
+ *     (33 = 132 SMs on a B200), which costs more than the multicast saves.
+ * Host-only; takes effect at the next ams_match.  AMS_ERR_INVALID_ARGUMENT for a NULL
+ * pool or a policy outside [0, 3]. */
 ams_status_t ams_pool_set_kernel_policy(ams_pool_t pool, int32_t policy);
 
 ams_status_t ams_pool_last_plan(ams_pool_t pool, int32_t* splits, int32_t* partials,

@@ -101,20 +101,28 @@ size_t esize(const Pool& p) { return p.cfg.dtype == AMS_DTYPE_BF16 ? 2 : 4; }
 // (the HBM-bound scan).  Row splits S: units = n_qt * S are dealt round-robin to the
 // persistent clusters; minimise the busiest cluster's tile count
 // ceil(U / clusters) * ceil(n_pt / S), ties -> fewer splits (fewer partial lists).
-void plan_tc(const Pool& p, int nq, int KT, int& S, int& grid, int& cg) {
+void plan_tc(const Pool& p, int nq, int KT, int& S, int& grid, int& cg, int& cl) {
   cg = nq > ams::kBlockM ? 2 : 1;
   const int qtile = ams::tc_query_tile(cg);
   const int n_qt = (nq + qtile - 1) / qtile;
   const int64_t n_pt = (p.local + ams::kBlockN - 1) / ams::kBlockN;
-  const int clusters = p.num_sms / cg;
+  // Opt-in (policy bit 1): two CTA pairs per 4-CTA cluster share (multicast) the pool
+  // rows when the query tiles pair up.  Off by default: clusters must fit within a GPC
+  // and only 33 four-CTA clusters (132 of 148 SMs) are co-resident on a B200; the grid is
+  // limited to them because the wave lockstep needs the whole grid resident.  Measured
+  // at the 1 kW cap: +9.5 % per SM (clock 1305 -> 1425 MHz) but -10.8 % SMs, net -2.4 %.
+  cl = (cg == 2 && n_qt % 2 == 0 && p.max_clusters4 >= 1 && (p.kernel_policy & 2) != 0) ? 4 : cg;
+  const int clusters = std::min(p.num_sms / cl, std::max(1, cl == 4 ? p.max_clusters4 : cl == 2 ? p.max_clusters2
+                                                                                               : p.num_sms));
+  const int n_qg = n_qt / (cl / cg);   // units per row split
   const int64_t nq_pad = (int64_t)n_qt * qtile;
   int64_t s_cap = std::max<int64_t>(1, p.part_cap / (nq_pad * ams::kEpiHalves * KT));
   s_cap = std::min<int64_t>(s_cap, std::max<int64_t>(1, n_pt));
-  s_cap = std::min<int64_t>(s_cap, std::max<int64_t>(1, (int64_t)64 * clusters / n_qt + 1));
+  s_cap = std::min<int64_t>(s_cap, std::max<int64_t>(1, (int64_t)64 * clusters / n_qg + 1));
   int64_t best_cost = LLONG_MAX;
   int best = 1;
   for (int64_t s = 1; s <= s_cap; ++s) {
-    const int64_t U = (int64_t)n_qt * s;
+    const int64_t U = (int64_t)n_qg * s;
     const int64_t waves = (U + clusters - 1) / clusters;
     const int64_t per = (n_pt + s - 1) / s;
     const int64_t cost = waves * per * 64 + s;  // + small penalty per split (merge work)
@@ -128,7 +136,7 @@ void plan_tc(const Pool& p, int nq, int KT, int& S, int& grid, int& cg) {
   S = (int)std::min<int64_t>({(int64_t)best * AMS_DIAG_SPLIT_MULT, std::max<int64_t>(1, n_pt),
                               std::max<int64_t>(1, p.part_cap / (nq_pad * ams::kEpiHalves * KT))});
 #endif
-  grid = (int)std::min<int64_t>((int64_t)n_qt * S, clusters) * cg;
+  grid = (int)std::min<int64_t>((int64_t)n_qg * S, clusters) * cl;
 }
 
 // Plan of the small-batch kernel: one query tile, so units are row splits only; same
@@ -280,6 +288,8 @@ ams_status_t ams_pool_create(const ams_pool_config_t* cfg, ams_pool_t* out) {
   p.cfg = c;
   p.cfg.nccl_id = nullptr;
   p.num_sms = prop.multiProcessorCount;
+  p.max_clusters2 = ams::tc_max_active_clusters(2);
+  p.max_clusters4 = ams::tc_max_active_clusters(4);
   p.JP = c.joint_dim <= 4 ? 4 : c.joint_dim <= 8 ? 8 : 16;
   p.B = ams::shard_block_size(c.capacity, c.world, c.shard_block);
   p.cap_shard = ams::shard_count(c.capacity, c.rank, c.world, p.B);
@@ -346,6 +356,7 @@ ams_status_t ams_pool_create(const ams_pool_config_t* cfg, ams_pool_t* out) {
   if (c.dtype == AMS_DTYPE_BF16) {
     if (!encode_bf16_map(&p.tmap_pool, p.emb, p.cap_pad, d, ams::kBlockN) ||
         !encode_bf16_map(&p.tmap_pool2, p.emb, p.cap_pad, d, ams::kBlockN / 2) ||
+        !encode_bf16_map(&p.tmap_pool4, p.emb, p.cap_pad, d, ams::kBlockN / 4) ||
         !encode_bf16_map(&p.tmap_q, p.q_stage, p.q_pad, d, ams::kBlockM) ||
         !encode_bf16_map(&p.tmap_qs[0], p.q_stage, p.q_pad, d, 16) ||
         !encode_bf16_map(&p.tmap_qs[1], p.q_stage, p.q_pad, d, 32) ||
@@ -517,7 +528,7 @@ static ams_status_t match_impl(ams_pool_t pool, const void* q_emb, const float* 
       p.last_splits = S;
       p.last_grid = nq * S;
       p.last_kernel = 0;
-    } else if (p.kernel_policy == 0 && !sorted && ams::scan_stages(p, nq, a.KT) > 0) {
+    } else if ((p.kernel_policy & 1) == 0 && !sorted && ams::scan_stages(p, nq, a.KT) > 0) {
       int S, grid;
       plan_scan(p, nq, a.KT, S, grid);
       P = S * ams::scan_lists_per_split();
@@ -529,16 +540,16 @@ static ams_status_t match_impl(ams_pool_t pool, const void* q_emb, const float* 
       p.last_grid = grid;
       p.last_kernel = 4;
     } else {
-      int S, grid, cg;
-      plan_tc(p, nq, a.KT, S, grid, cg);
+      int S, grid, cg, cl;
+      plan_tc(p, nq, a.KT, S, grid, cg, cl);
       P = S * ams::kEpiHalves;
       a.slots = (!a.gated && P >= a.k) ? 1 : 0;   // as launch_match_tc
       if (e0) AMS_CUDA_TRY(cudaEventRecord(e0, s));
-      AMS_CUDA_TRY(ams::launch_match_tc(p, a, S, grid, cg, sorted, s));
+      AMS_CUDA_TRY(ams::launch_match_tc(p, a, S, grid, cg, cl, sorted, s));
       if (e1) AMS_CUDA_TRY(cudaEventRecord(e1, s));
       p.last_splits = S;
       p.last_grid = grid;
-      p.last_kernel = cg;
+      p.last_kernel = cl == 4 ? 5 : cg;
     }
     p.last_partials = P;
   }
@@ -751,7 +762,7 @@ ams_status_t ams_pool_launch_count(ams_pool_t pool, int64_t* launches) {
 }
 
 ams_status_t ams_pool_set_kernel_policy(ams_pool_t pool, int32_t policy) {
-  if (pool == nullptr || policy < 0 || policy > 1) return AMS_ERR_INVALID_ARGUMENT;
+  if (pool == nullptr || policy < 0 || policy > 3) return AMS_ERR_INVALID_ARGUMENT;
   pool->p.kernel_policy = policy;
   return AMS_OK;
 }

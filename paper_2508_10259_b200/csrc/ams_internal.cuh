@@ -72,6 +72,8 @@ struct Pool {
   int64_t size = 0;           // global rows appended
   int64_t local = 0;          // rows held by this rank
   int32_t num_sms = 148;
+  int32_t max_clusters2 = 0;  // co-resident 2-CTA / 4-CTA clusters of the CTA-pair kernel
+  int32_t max_clusters4 = 0;
   int32_t KT_max = 8;
   bool broken = false;
   bool collective = false;    // world > 1, or world == 1 with an nccl_id: shard lists go
@@ -132,9 +134,10 @@ struct Pool {
 
   CUtensorMap tmap_pool{};   // bf16 pool [cap_pad, d], box {64, 256}, SW128 (CTA tile)
   CUtensorMap tmap_pool2{};  // bf16 pool [cap_pad, d], box {64, 128}, SW128 (CTA-pair half tile)
+  CUtensorMap tmap_pool4{};  // bf16 pool [cap_pad, d], box {64, 64}, SW128 (multicast quarter tile)
   CUtensorMap tmap_q{};      // bf16 queries [q_pad, d], box {64, 128}, SW128
   CUtensorMap tmap_qs[4]{};  // bf16 queries [q_pad, d], box {64, 16/32/64/128}, SW128 (small-batch kernel)
-  int32_t kernel_policy = 0; // 0: auto; 1: never the small-batch kernel (ams_pool_set_kernel_policy)
+  int32_t kernel_policy = 0; // bit 0: never the small-batch kernel; bit 1: no 4-CTA multicast clusters
 
   void* nccl_comm = nullptr;  // ncclComm_t
 
@@ -175,9 +178,12 @@ cudaError_t launch_query_order(Pool& p, const float* qj_src, int32_t nq, cudaStr
 cudaError_t launch_match_simt(Pool& p, const MatchArgs& a, int32_t splits, cudaStream_t s);
 // cg = 1: one CTA per 128x256 tile; cg = 2: CTA pair (cta_group::2) per 256x256 tile
 // sorted: queries were staged through p.q_perm (partials land at the caller's query index)
-cudaError_t launch_match_tc(Pool& p, const MatchArgs& a, int32_t splits, int32_t grid, int32_t cg, bool sorted,
-                            cudaStream_t s);
+// cl: CTAs per cluster (cg, or 4 for cg = 2: two CTA pairs sharing multicast pool rows;
+// needs an even number of 256-query tiles)
+cudaError_t launch_match_tc(Pool& p, const MatchArgs& a, int32_t splits, int32_t grid, int32_t cg, int32_t cl,
+                            bool sorted, cudaStream_t s);
 int tc_query_tile(int cg);
+int tc_max_active_clusters(int cl);   // co-resident clusters of cl CTAs (CTA-pair kernel); 0 on error
 // small-batch kernel (pool rows on the MMA M side, queries on N): pipeline stages that fit
 // shared memory for this batch, 0 if the batch is not eligible (nq > 128, KT > 32, or
 // the per-warp lists would not fit)

@@ -272,7 +272,7 @@ __device__ __forceinline__ bool epi_chunk_sorted(uint32_t taddr, int64_t jbase, 
 // 168 registers is the ceiling for 10 warps per CTA: warps are spread over the 4 SM
 // sub-partitions (3 + 3 + 2 + 2) and each holds 16 K registers, so 3 x 32 x 168 = 16128
 // fits while 176 fails at launch ("too many resources").  KT = 64 spills a little.
-template <int KT, int JP, int CG>
+template <int KT, int JP, int CG, int CL>
 __global__ void __maxnreg__(168)
     match_tc_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_pool,
                     const TcParams prm) {
@@ -299,8 +299,15 @@ __global__ void __maxnreg__(168)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const uint32_t crank = CG == 2 ? ptx::cluster_ctarank() : 0u;
-  const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;
+  // CL = CTAs per cluster: CG (one tile per cluster), or 2 * CG = two CTA pairs that
+  // work on the same pool rows with different query tiles, each CTA loading half of its
+  // pool rows and multicasting them to its counterpart in the other pair (the pool
+  // operand's L2 -> SM traffic halves)
+  constexpr int NPAIR = CL / CG;
+  const uint32_t crank = CL > 1 ? ptx::cluster_ctarank() : 0u;
+  const uint32_t pair = crank / CG, prank = crank % CG;   // pair in the cluster, rank in the pair
+  const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
+  const int n_qg = prm.n_qt / NPAIR;                      // query-tile groups (one per unit)
 
   constexpr int kProducerWarp = 4 * kEpiHalves, kMmaWarp = 4 * kEpiHalves + 1;
   if (warp == kProducerWarp && lane == 0) {
@@ -308,7 +315,7 @@ __global__ void __maxnreg__(168)
     ptx::prefetch_tmap(&tmap_pool);
     for (int i = 0; i < STAGES; ++i) {
       ptx::mbar_init(&full[i], 1);
-      ptx::mbar_init(&empty[i], 1);
+      ptx::mbar_init(&empty[i], NPAIR);   // one MMA commit per pair whose loads land here
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&tfull[i], 1);
@@ -324,7 +331,7 @@ __global__ void __maxnreg__(168)
   }
   ptx::tc_fence_before();
   __syncthreads();
-  if (CG == 2) ptx::cluster_sync();   // peer barriers initialised before any remote traffic
+  if (CL > 1) ptx::cluster_sync();   // peer barriers initialised before any remote traffic
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
@@ -334,7 +341,8 @@ __global__ void __maxnreg__(168)
     // ------------------------------------------------------------ TMA producer
     // Whole warp walks the loop and waits (uniform control flow), one elected lane issues.
     {
-      const uint32_t full_leader0 = CG == 2 ? ptx::mapa(ptx::smem_u32(&full[0]), 0) : 0u;
+      const uint32_t full_leader0 = CG == 2 ? ptx::mapa(ptx::smem_u32(&full[0]), pair * CG) : 0u;
+      const uint16_t mc_mask = (uint16_t)((1u << crank) | (1u << (crank ^ (uint32_t)CG)));   // NPAIR == 2
       const uint64_t pol_q = ptx::policy_evict_last();
       const uint64_t pol_pool = prm.n_qt > 1 ? ptx::policy_evict_normal() : ptx::policy_evict_first();
       int stage = 0;
@@ -342,10 +350,10 @@ __global__ void __maxnreg__(168)
       uint32_t tile_count = 0;
       uint32_t wave = 0;
       for (int u = cid; u < prm.n_units; u += ncl, ++wave) {
-        const int sp = u / prm.n_qt, qt = u % prm.n_qt;
+        const int sp = u / n_qg, qt = (u % n_qg) * NPAIR + (int)pair;
         int t_lo, t_hi;
         split_tiles(sp, prm.S, prm.n_pt, t_lo, t_hi);
-        const int qrow0 = qt * kBlockM * CG + (int)crank * kBlockM;
+        const int qrow0 = qt * kBlockM * CG + (int)prank * kBlockM;
         // Wave lockstep: the units sharing a row split run in the same wave (split-major
         // order) and re-read its rows from L2 only while they stay within ~1 ms of each
         // other.  Static striding lets per-unit jitter accumulate across waves (measured
@@ -374,19 +382,43 @@ __global__ void __maxnreg__(168)
             ptx::bulk_load(aux + AUXJ, prm.pool_inv + (int64_t)t * kBlockN, kBlockN * 4, &afull[buf]);
           }
           __syncwarp();
-          const int prow0 = t * kBlockN + (int)crank * (int)Geo<CG>::b_rows;
+          const int prow0 = t * kBlockN + (int)prank * (int)Geo<CG>::b_rows;
           for (int kb = 0; kb < n_kb; ++kb) {
             ptx::mbar_wait(&empty[stage], phase ^ 1u);
             if (ptx::elect_one()) {
+#if defined(AMS_DIAG_NO_B_LOAD) || defined(AMS_DIAG_NO_A_LOAD)
+              // diagnostic builds only (power attribution): after the first tile, one operand is
+              // not re-staged (the MMA reads stale shared memory; results are meaningless)
+              const bool skip = tile_count > 0;
+#ifdef AMS_DIAG_NO_B_LOAD
+              const bool load_a = true, load_b = !skip;
+#else
+              const bool load_a = !skip, load_b = true;
+#endif
+              const uint32_t bytes = (load_a ? kABytes : 0u) + (load_b ? BBYTES : 0u);
+#else
+              constexpr bool load_a = true, load_b = true;
+              constexpr uint32_t bytes = STAGE;
+#endif
               if (CG == 1) {
-                ptx::mbar_arrive_expect_tx(&full[stage], STAGE);
-                ptx::tma_load_2d(sA + stage * kABytes, &tmap_q, &full[stage], kb * kBlockK, qrow0, pol_q);
-                ptx::tma_load_2d(sB + stage * BBYTES, &tmap_pool, &full[stage], kb * kBlockK, prow0, pol_pool);
+                ptx::mbar_arrive_expect_tx(&full[stage], bytes);
+                if (load_a) ptx::tma_load_2d(sA + stage * kABytes, &tmap_q, &full[stage], kb * kBlockK, qrow0, pol_q);
+                if (load_b)
+                  ptx::tma_load_2d(sB + stage * BBYTES, &tmap_pool, &full[stage], kb * kBlockK, prow0, pol_pool);
               } else {
-                if (crank == 0) ptx::mbar_arrive_expect_tx(&full[stage], CG * STAGE);
+                if (prank == 0) ptx::mbar_arrive_expect_tx(&full[stage], CG * bytes);
                 const uint32_t fb = full_leader0 + (uint32_t)(stage * sizeof(uint64_t));
-                ptx::tma_load_2d_pair(sA + stage * kABytes, &tmap_q, fb, kb * kBlockK, qrow0, pol_q);
-                ptx::tma_load_2d_pair(sB + stage * BBYTES, &tmap_pool, fb, kb * kBlockK, prow0, pol_pool);
+                if (load_a) ptx::tma_load_2d_pair(sA + stage * kABytes, &tmap_q, fb, kb * kBlockK, qrow0, pol_q);
+                if (NPAIR == 1) {
+                  if (load_b)
+                    ptx::tma_load_2d_pair(sB + stage * BBYTES, &tmap_pool, fb, kb * kBlockK, prow0, pol_pool);
+                } else if (load_b) {
+                  // half of this CTA's pool rows, into both pairs (same CTA-relative offset);
+                  // completion goes to each destination pair's leader barrier
+                  constexpr uint32_t half = BBYTES / 2;
+                  ptx::tma_load_2d_pair_mc(sB + stage * BBYTES + pair * half, &tmap_pool, &full[stage], mc_mask,
+                                           kb * kBlockK, prow0 + (int)pair * (int)(Geo<CG>::b_rows / 2), pol_pool);
+                }
               }
             }
             __syncwarp();
@@ -406,14 +438,19 @@ __global__ void __maxnreg__(168)
     // smem descriptors of a stage are the base descriptors plus the stage offset (the
     // 14-bit start-address field never carries: smem < 256 KB), so an UMMA costs a few
     // uniform integer ops instead of a per-issue descriptor rebuild.
-    if (crank == 0) {
+    if (prank == 0) {
+      // commits: stage release to every CTA whose shared memory the stage's loads filled
+      // (this pair, plus the other pair's when the pool rows are multicast); accumulator
+      // ready to this pair only
+      const uint16_t empty_mask = (uint16_t)(NPAIR == 1 ? 0x3u : 0xFu);
+      const uint16_t tfull_mask = (uint16_t)(0x3u << (pair * CG));
       int stage = 0;
       uint32_t phase = 0;
       uint32_t tile_count = 0;
       const uint64_t da0 = ptx::sdesc_k_sw128(ptx::smem_u32(sA));
       const uint64_t db0 = ptx::sdesc_k_sw128(ptx::smem_u32(sB));
       for (int u = cid; u < prm.n_units; u += ncl) {
-        const int sp = u / prm.n_qt;
+        const int sp = u / n_qg;
         int t_lo, t_hi;
         split_tiles(sp, prm.S, prm.n_pt, t_lo, t_hi);
 #ifdef AMS_DIAG_TIMELINE
@@ -436,7 +473,10 @@ __global__ void __maxnreg__(168)
               for (int kk = 0; kk < kBlockK / 16; ++kk)
                 ptx::umma_f16<CG>(d_tmem, da + (uint64_t)(2 * kk), db + (uint64_t)(2 * kk), Geo<CG>::idesc,
                                   (kb | kk) != 0 ? 1u : 0u);
-              ptx::umma_commit<CG>(&empty[stage]);
+              if (CG == 1)
+                ptx::umma_commit<CG>(&empty[stage]);
+              else
+                ptx::umma_commit_mc(&empty[stage], empty_mask);
             }
             __syncwarp();
             if (++stage == STAGES) {
@@ -444,7 +484,12 @@ __global__ void __maxnreg__(168)
               phase ^= 1u;
             }
           }
-          if (ptx::elect_one()) ptx::umma_commit<CG>(&tfull[buf]);
+          if (ptx::elect_one()) {
+            if (CG == 1)
+              ptx::umma_commit<CG>(&tfull[buf]);
+            else
+              ptx::umma_commit_mc(&tfull[buf], tfull_mask);
+          }
           __syncwarp();
         }
 #ifdef AMS_DIAG_TIMELINE
@@ -465,13 +510,13 @@ __global__ void __maxnreg__(168)
     const int h = warp >> 2;           // column half
     uint32_t tile_count = 0;
     const bool gated = prm.gated != 0;
-    const uint32_t tempty_leader0 = CG == 2 ? ptx::mapa(ptx::smem_u32(&tempty[0]), 0) : 0u;
+    const uint32_t tempty_leader0 = CG == 2 ? ptx::mapa(ptx::smem_u32(&tempty[0]), pair * CG) : 0u;
     for (int u = cid; u < prm.n_units; u += ncl) {
-      const int sp = u / prm.n_qt, qt = u % prm.n_qt;
+      const int sp = u / n_qg, qt = (u % n_qg) * NPAIR + (int)pair;
       int t_lo, t_hi;
       split_tiles(sp, prm.S, prm.n_pt, t_lo, t_hi);
       const int64_t row_end = min((int64_t)t_hi * kBlockN, prm.L);
-      const int qrow = qt * kBlockM * CG + (int)crank * kBlockM + lg * 32 + lane;
+      const int qrow = qt * kBlockM * CG + (int)prank * kBlockM + lg * 32 + lane;
       const bool active = qrow < prm.nq;
       float qj[JP];
 #pragma unroll
@@ -589,16 +634,16 @@ __global__ void __maxnreg__(168)
 
   ptx::tc_fence_before();
   __syncthreads();
-  if (CG == 2) ptx::cluster_sync();   // no CTA leaves while its peer may still signal it
+  if (CL > 1) ptx::cluster_sync();   // no CTA leaves while a peer may still signal it
   if (warp == kMmaWarp) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<CG>(tmem_base, kTmemCols);
   }
 }
 
-template <int KT, int JP, int CG>
+template <int KT, int JP, int CG, int CL>
 cudaError_t launch_tc_t(Pool& p, const TcParams& prm, int grid, cudaStream_t s) {
-  auto kern = match_tc_kernel<KT, JP, CG>;
+  auto kern = match_tc_kernel<KT, JP, CG, CL>;
   const size_t smem = smem_for<JP, CG>();
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -609,30 +654,31 @@ cudaError_t launch_tc_t(Pool& p, const TcParams& prm, int grid, cudaStream_t s) 
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.x = CL;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, p.tmap_q, CG == 1 ? p.tmap_pool : p.tmap_pool2, prm);
+  return cudaLaunchKernelEx(&cfg, kern, p.tmap_q, CG == 1 ? p.tmap_pool : CL == CG ? p.tmap_pool2 : p.tmap_pool4,
+                            prm);
 }
 
-template <int KT, int CG>
+template <int KT, int CG, int CL>
 cudaError_t launch_tc_kt(Pool& p, const TcParams& prm, int grid, cudaStream_t s) {
   switch (p.JP) {
-    case 4: return launch_tc_t<KT, 4, CG>(p, prm, grid, s);
-    case 8: return launch_tc_t<KT, 8, CG>(p, prm, grid, s);
-    default: return launch_tc_t<KT, 16, CG>(p, prm, grid, s);
+    case 4: return launch_tc_t<KT, 4, CG, CL>(p, prm, grid, s);
+    case 8: return launch_tc_t<KT, 8, CG, CL>(p, prm, grid, s);
+    default: return launch_tc_t<KT, 16, CG, CL>(p, prm, grid, s);
   }
 }
 
-template <int CG>
+template <int CG, int CL>
 cudaError_t launch_tc_cg(Pool& p, const MatchArgs& a, const TcParams& prm, int grid, cudaStream_t s) {
   switch (a.KT) {
-    case 8: return launch_tc_kt<8, CG>(p, prm, grid, s);
-    case 16: return launch_tc_kt<16, CG>(p, prm, grid, s);
-    case 32: return launch_tc_kt<32, CG>(p, prm, grid, s);
-    default: return launch_tc_kt<64, CG>(p, prm, grid, s);
+    case 8: return launch_tc_kt<8, CG, CL>(p, prm, grid, s);
+    case 16: return launch_tc_kt<16, CG, CL>(p, prm, grid, s);
+    case 32: return launch_tc_kt<32, CG, CL>(p, prm, grid, s);
+    default: return launch_tc_kt<64, CG, CL>(p, prm, grid, s);
   }
 }
 
@@ -640,8 +686,33 @@ cudaError_t launch_tc_cg(Pool& p, const MatchArgs& a, const TcParams& prm, int g
 
 int tc_query_tile(int cg) { return kBlockM * cg; }
 
-cudaError_t launch_match_tc(Pool& p, const MatchArgs& a, int32_t S, int32_t grid, int32_t cg, bool sorted,
-                            cudaStream_t s) {
+// Clusters of `cl` CTAs of the CTA-pair kernel that can be co-resident (clusters must fit
+// within a GPC, so this can be below num_sms / cl).  0 on error.
+int tc_max_active_clusters(int cl) {
+  auto kern = cl == 4 ? match_tc_kernel<16, 16, 2, 4> : match_tc_kernel<16, 16, 2, 2>;
+  const size_t smem = smem_for<16, 2>();
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(cl * 64));
+  cfg.blockDim = dim3(kThreadsTc);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, (void*)kern, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+cudaError_t launch_match_tc(Pool& p, const MatchArgs& a, int32_t S, int32_t grid, int32_t cg, int32_t cl,
+                            bool sorted, cudaStream_t s) {
   TcParams prm{};
   prm.inv_q = p.q_inv;
   prm.q_joints = p.q_joints;
@@ -659,7 +730,7 @@ cudaError_t launch_match_tc(Pool& p, const MatchArgs& a, int32_t S, int32_t grid
   prm.n_qt = (a.nq + kBlockM * cg - 1) / (kBlockM * cg);
   prm.n_pt = (int32_t)((p.local + kBlockN - 1) / kBlockN);
   prm.S = S;
-  prm.n_units = prm.n_qt * S;
+  prm.n_units = prm.n_qt / (cl / cg) * S;   // units = (query-tile group, row split)
   prm.k = a.k;
   prm.gated = a.gated;
   prm.P = S * kEpiHalves;
@@ -672,7 +743,9 @@ cudaError_t launch_match_tc(Pool& p, const MatchArgs& a, int32_t S, int32_t grid
     e = cudaMemsetAsync(p.slots, 0, (size_t)prm.n_qt * kBlockM * cg * a.KT * sizeof(uint32_t), s);
     if (e != cudaSuccess) return e;
   }
-  e = cg == 2 ? launch_tc_cg<2>(p, a, prm, grid, s) : launch_tc_cg<1>(p, a, prm, grid, s);
+  if (cl != cg && (cg != 2 || cl != 4 || prm.n_qt % 2 != 0)) return cudaErrorInvalidValue;
+  e = cg == 1 ? launch_tc_cg<1, 1>(p, a, prm, grid, s)
+              : cl == 2 ? launch_tc_cg<2, 2>(p, a, prm, grid, s) : launch_tc_cg<2, 4>(p, a, prm, grid, s);
   ++p.launches;
   return e;
 }

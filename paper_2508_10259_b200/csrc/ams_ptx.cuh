@@ -80,6 +80,17 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m
       "l"(map), "r"(bar_cluster_addr), "r"(x), "r"(y), "l"(policy)
       : "memory");
 }
+// CTA-pair tile load multicast to the CTAs in `mask` (same CTA-relative dst offset in each);
+// the transaction bytes go to the leader (even) CTA's barrier of each destination pair:
+// the barrier operand is the CTA-local address with the peer bit cleared
+__device__ __forceinline__ void tma_load_2d_pair_mc(void* dst, const CUtensorMap* map, uint64_t* bar, uint16_t mask,
+                                                    int32_t x, int32_t y, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      ".L2::cache_hint [%0], [%1, {%4, %5}], [%2], %3, %6;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar) & 0xFEFFFFFFu), "h"(mask), "r"(x), "r"(y), "l"(policy)
+      : "memory");
+}
 // contiguous global -> shared bulk copy (bytes multiple of 16, both 16B aligned)
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -172,6 +183,14 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
             smem_u32(bar)),
         "h"((uint16_t)0x3)
         : "memory");
+}
+// cta_group::2 commit arriving on `bar` (same offset) in every CTA of `mask`
+__device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 

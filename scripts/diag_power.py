@@ -1,6 +1,6 @@
 """Power/clock diagnostic: full kernel vs the MMA+TMA pipeline alone (epilogue compiled
 out, build/diag/libams_diag.so) vs cuBLAS, each for ~3 s under nvidia-smi sampling.
-Run: AMS_LIBRARY=... python scripts/diag_power.py <label>"""
+Run: [AMS_LIBRARY=...] [AMS_POLICY=<ams_pool_set_kernel_policy mask>] python scripts/diag_power.py <label>"""
 import json, os, sys, time
 sys.path.insert(0, os.getcwd())
 import torch
@@ -30,6 +30,7 @@ import paper_2508_10259_b200 as ams
 print("lib", ams.LIB_PATH)
 cfg = ams_gen.CONFIGS["c3"]
 pool = ams.Pool(cfg.d, cfg.J, cfg.M, cfg.Q, cfg.k)
+ams.ams_pool_set_kernel_policy(pool.handle, int(os.environ.get("AMS_POLICY", "0")))
 q, qj, lab = ams_gen.build_device_workload(cfg, dev, lambda e, j, n: pool.append(e, j, n))
 out = pool.match(q, qj, cfg.k, cfg.theta, cfg.gamma)
 for gamma in (cfg.gamma, float("inf")):
