@@ -143,8 +143,9 @@ void plan_tc(const Pool& p, int nq, int KT, int& S, int& grid, int& cg, int& cl)
 // cost model as plan_tc (busiest CTA's tile count, ties -> fewer splits).
 void plan_scan(const Pool& p, int nq, int KT, int& S, int& grid) {
   const int64_t n_pt = (p.local + ams::kBlockN - 1) / ams::kBlockN;
-  const int ctas = p.num_sms;
-  const int64_t per_split = (int64_t)nq * ams::scan_lists_per_split() * KT;
+  const int cg = ams::scan_cg(nq);
+  const int ctas = std::min(p.num_sms / cg, cg == 2 ? std::max(1, p.max_clusters2) : p.num_sms);   // tiles in flight
+  const int64_t per_split = (int64_t)nq * ams::scan_lists_per_split(nq) * KT;
   int64_t s_cap = std::max<int64_t>(1, p.part_cap / per_split);
   s_cap = std::min<int64_t>({s_cap, std::max<int64_t>(1, n_pt), (int64_t)8 * ctas});
   int64_t best_cost = LLONG_MAX;
@@ -157,7 +158,7 @@ void plan_scan(const Pool& p, int nq, int KT, int& S, int& grid) {
     }
   }
   S = best;
-  grid = (int)std::min<int64_t>(S, ctas);
+  grid = (int)std::min<int64_t>(S, ctas) * cg;
 }
 
 void plan_simt(const Pool& p, int nq, int KT, int& S) {
@@ -318,6 +319,8 @@ ams_status_t ams_pool_create(const ams_pool_config_t* cfg, ams_pool_t* out) {
     const int64_t s_max = std::min<int64_t>(n_pt_max, (int64_t)64 * p.num_sms + 1);
     part = std::min<int64_t>((int64_t)p.q_pad * s_max, (int64_t)ams::kBlockM * 64 * p.num_sms + p.q_pad) *
            ams::kEpiHalves * p.KT_max;
+    // the small-batch kernel keeps 4 (8 on a CTA pair) lists per row split for nq <= 256
+    part = std::max<int64_t>(part, (int64_t)std::min(p.q_pad, 256) * 8 * p.KT_max * std::min<int64_t>(n_pt_max, 8));
   } else {
     const int64_t s_max = std::max<int64_t>(1, std::min<int64_t>(p.cap_pad / ams::kSimtThreads, 2 * p.num_sms));
     part = std::min<int64_t>((int64_t)c.max_queries * s_max, (int64_t)c.max_queries + 2 * p.num_sms) *
@@ -481,7 +484,11 @@ static ams_status_t match_impl(ams_pool_t pool, const void* q_emb, const float* 
   // Gated batches are staged in (joint 0, joint 1) order (the epilogue's warp-level gate
   // test then rejects most columns for all 32 queries of a warp at once).  The order is
   // invisible to the caller: partial lists land at the caller's query index.
-  const bool sorted = p.cfg.dtype == AMS_DTYPE_BF16 && a.gated && p.local > 0 && nq >= kSortMinQueries;
+  // The small-batch kernel (pool rows on the MMA M side) needs no query order.
+  const bool use_scan = !gate_first && p.cfg.dtype == AMS_DTYPE_BF16 && p.local > 0 && (p.kernel_policy & 1) == 0 &&
+                        ams::scan_stages(p, nq, a.KT) > 0 &&
+                        (int64_t)nq * ams::scan_lists_per_split(nq) * a.KT <= p.part_cap;   // >= 1 split fits
+  const bool sorted = p.cfg.dtype == AMS_DTYPE_BF16 && a.gated && p.local > 0 && nq >= kSortMinQueries && !use_scan;
   if (sorted) AMS_CUDA_TRY(ams::launch_query_order(p, qj_src, nq, s));
   AMS_CUDA_TRY(ams::launch_query_prep(p, q_src, qj_src, nq, sorted ? p.q_perm : nullptr, s));
   if (b >= 0) AMS_CUDA_TRY(cudaEventRecord(p.consumed[b], s));   // staging b read (order + prep)
@@ -528,10 +535,10 @@ static ams_status_t match_impl(ams_pool_t pool, const void* q_emb, const float* 
       p.last_splits = S;
       p.last_grid = nq * S;
       p.last_kernel = 0;
-    } else if ((p.kernel_policy & 1) == 0 && !sorted && ams::scan_stages(p, nq, a.KT) > 0) {
+    } else if (use_scan) {
       int S, grid;
       plan_scan(p, nq, a.KT, S, grid);
-      P = S * ams::scan_lists_per_split();
+      P = S * ams::scan_lists_per_split(nq);
       a.slots = (!a.gated && P >= a.k) ? 1 : 0;   // union-bound slots (launch_match_scan)
       if (e0) AMS_CUDA_TRY(cudaEventRecord(e0, s));
       AMS_CUDA_TRY(ams::launch_match_scan(p, a, S, grid, s));

@@ -185,10 +185,11 @@ cudaError_t launch_match_tc(Pool& p, const MatchArgs& a, int32_t splits, int32_t
 int tc_query_tile(int cg);
 int tc_max_active_clusters(int cl);   // co-resident clusters of cl CTAs (CTA-pair kernel); 0 on error
 // small-batch kernel (pool rows on the MMA M side, queries on N): pipeline stages that fit
-// shared memory for this batch, 0 if the batch is not eligible (nq > 128, KT > 32, or
-// the per-warp lists would not fit)
+// shared memory for this batch, 0 if the batch is not eligible (nq > 256, KT > 32, KT != 8
+// above 128 queries, or the per-lane register lists would not fit)
 int scan_stages(const Pool& p, int nq, int KT);
-int scan_lists_per_split();
+int scan_cg(int nq);                 // CTAs per tile: 1 (nq <= 128) or 2 (CTA pair)
+int scan_lists_per_split(int nq);    // partial lists per row split
 cudaError_t launch_match_scan(Pool& p, const MatchArgs& a, int32_t splits, int32_t grid, cudaStream_t s);
 // merge [nq][P][KT] local lists -> [nq][k] (fp32, global int64); writes hit if out_hit != null
 // tc_bounds: the lists come from launch_match_tc, whose per-query lower bounds (p.bound,

@@ -80,11 +80,12 @@ struct ScanLayout {
   uint32_t a, b, aux, tr, qj, iq, thr, bars, total;
 };
 
-__host__ __device__ inline ScanLayout scan_layout(int stages, uint32_t b_bytes, int JP, int NQ) {
+// cg = 2: a CTA stages 128 of the pair's 256 pool rows per stage
+__host__ __device__ inline ScanLayout scan_layout(int stages, uint32_t b_bytes, int JP, int NQ, int cg) {
   ScanLayout l{};
   uint32_t o = 0;
   l.a = o;
-  o += (uint32_t)stages * kScanABytes;
+  o += (uint32_t)stages * (kScanABytes / (uint32_t)cg);
   l.b = o;
   o += (uint32_t)stages * b_bytes;
   l.aux = o;
@@ -108,18 +109,25 @@ __device__ __forceinline__ void scan_split(int sp, int S, int n_pt, int& t_lo, i
   t_hi = (int)((int64_t)(sp + 1) * n_pt / S);
 }
 
-template <int KT, int JP, bool GATED>
+// CG = 1: one CTA per 256-row tile (two M = 128 MMAs), nq <= 128.  CG = 2: a CTA pair
+// per 256-row tile (one tcgen05.mma.cta_group::2 with M = 256: each CTA stages 128 pool
+// rows and half of the N query rows), 128 < nq <= 256; each CTA's epilogue owns its 128
+// rows against all N queries.
+template <int KT, int JP, bool GATED, int CG>
 __global__ void __launch_bounds__(kScanThreads, 1)
     match_scan_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_pool,
                       const ScanParams prm) {
   constexpr uint32_t AUXJ = kBlockN * JP * 4;
   constexpr uint32_t AUX = AUXJ + kBlockN * 4;
-  constexpr int NSL = kScanListRegs / (32 * KT) < 4 ? kScanListRegs / (32 * KT) : 4;   // 32-query slots per lane (nq <= 128)
+  constexpr uint32_t ABYTES = kScanABytes / CG;   // pool rows staged per CTA and stage
+  constexpr int NQMAX = 128 * CG;
+  constexpr int NSL0 = kScanListRegs / (32 * KT);
+  constexpr int NSL = NSL0 < NQMAX / 32 ? NSL0 : NQMAX / 32;   // 32-query slots per lane
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   const int NQ = prm.NQ;
   const int STAGES = prm.stages;
-  const ScanLayout lay = scan_layout(STAGES, prm.b_bytes, JP, NQ);
+  const ScanLayout lay = scan_layout(STAGES, prm.b_bytes, JP, NQ, CG);
   uint8_t* sA = smem + lay.a;
   uint8_t* sB = smem + lay.b;
   uint8_t* sAux = smem + lay.aux;
@@ -138,6 +146,8 @@ __global__ void __launch_bounds__(kScanThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t crank = CG == 2 ? ptx::cluster_ctarank() : 0u;
+  const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;
   constexpr int kProducerWarp = kScanEpiWarps, kMmaWarp = kScanEpiWarps + 1;
   if (warp == kProducerWarp && lane == 0) {
     ptx::prefetch_tmap(&tmap_q);
@@ -148,18 +158,19 @@ __global__ void __launch_bounds__(kScanThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&tfull[i], 1);
-      ptx::mbar_init(&tempty[i], kScanEpiWarps);
+      ptx::mbar_init(&tempty[i], kScanEpiWarps * CG);
       ptx::mbar_init(&afull[i], 1);
       ptx::mbar_init(&aempty[i], kScanEpiWarps);
     }
     ptx::fence_mbar_init();
   }
   if (warp == kMmaWarp) {
-    ptx::tmem_alloc<1>(tmem_holder, 512);
-    ptx::tmem_relinquish<1>();
+    ptx::tmem_alloc<CG>(tmem_holder, 512);
+    ptx::tmem_relinquish<CG>();
   }
   ptx::tc_fence_before();
   __syncthreads();
+  if (CG == 2) ptx::cluster_sync();   // peer barriers initialised before any remote traffic
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
   const int n_kb = prm.d / kBlockK;
@@ -168,10 +179,12 @@ __global__ void __launch_bounds__(kScanThreads, 1)
     // ------------------------------------------------------------ TMA producer
     const uint64_t pol_q = ptx::policy_evict_last();
     const uint64_t pol_pool = ptx::policy_evict_first();   // every pool byte is read once
-    const uint32_t tx = kScanABytes + prm.b_bytes;
+    const uint32_t tx = ABYTES + prm.b_bytes;
+    const uint32_t full_leader0 = CG == 2 ? ptx::mapa(ptx::smem_u32(&full[0]), 0) : 0u;
+    const int qrow0 = (int)crank * (NQ / CG);   // this CTA's query rows (the B half)
     int stage = 0;
     uint32_t phase = 0, tile_count = 0;
-    for (int u = blockIdx.x; u < prm.S; u += gridDim.x) {
+    for (int u = cid; u < prm.S; u += ncl) {
       int t_lo, t_hi;
       scan_split(u, prm.S, prm.n_pt, t_lo, t_hi);
       for (int t = t_lo; t < t_hi; ++t, ++tile_count) {
@@ -188,9 +201,17 @@ __global__ void __launch_bounds__(kScanThreads, 1)
         for (int kb = 0; kb < n_kb; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1u);
           if (ptx::elect_one()) {
-            ptx::mbar_arrive_expect_tx(&full[stage], tx);
-            ptx::tma_load_2d(sA + stage * kScanABytes, &tmap_pool, &full[stage], kb * kBlockK, t * kBlockN, pol_pool);
-            ptx::tma_load_2d(sB + stage * prm.b_bytes, &tmap_q, &full[stage], kb * kBlockK, 0, pol_q);
+            if (CG == 1) {
+              ptx::mbar_arrive_expect_tx(&full[stage], tx);
+              ptx::tma_load_2d(sA + stage * ABYTES, &tmap_pool, &full[stage], kb * kBlockK, t * kBlockN, pol_pool);
+              ptx::tma_load_2d(sB + stage * prm.b_bytes, &tmap_q, &full[stage], kb * kBlockK, 0, pol_q);
+            } else {
+              if (crank == 0) ptx::mbar_arrive_expect_tx(&full[stage], CG * tx);
+              const uint32_t fb = full_leader0 + (uint32_t)(stage * sizeof(uint64_t));
+              ptx::tma_load_2d_pair(sA + stage * ABYTES, &tmap_pool, fb, kb * kBlockK, t * kBlockN + (int)crank * 128,
+                                    pol_pool);
+              ptx::tma_load_2d_pair(sB + stage * prm.b_bytes, &tmap_q, fb, kb * kBlockK, qrow0, pol_q);
+            }
           }
           __syncwarp();
           if (++stage == STAGES) {
@@ -201,12 +222,12 @@ __global__ void __launch_bounds__(kScanThreads, 1)
       }
     }
   } else if (warp == kMmaWarp) {
-    // ------------------------------------------------------------ MMA issuer
+    // ------------------------------------------------------------ MMA issuer (pair leader)
     const uint64_t da0 = ptx::sdesc_k_sw128(ptx::smem_u32(sA));
     const uint64_t db0 = ptx::sdesc_k_sw128(ptx::smem_u32(sB));
     int stage = 0;
     uint32_t phase = 0, tile_count = 0;
-    for (int u = blockIdx.x; u < prm.S; u += gridDim.x) {
+    for (int u = cid; u < prm.S && crank == 0; u += ncl) {
       int t_lo, t_hi;
       scan_split(u, prm.S, prm.n_pt, t_lo, t_hi);
       for (int t = t_lo; t < t_hi; ++t, ++tile_count) {
@@ -214,20 +235,20 @@ __global__ void __launch_bounds__(kScanThreads, 1)
         const uint32_t use = tile_count >> 1;
         ptx::mbar_wait(&tempty[buf], (use & 1u) ^ 1u);
         ptx::tc_fence_after();
-        const uint32_t d0 = tmem_base + (uint32_t)(buf * 2 * NQ);
+        const uint32_t d0 = tmem_base + (uint32_t)(buf * (2 / CG) * NQ);
         for (int kb = 0; kb < n_kb; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
           if (ptx::elect_one()) {
-            const uint64_t da = da0 + (uint64_t)((uint32_t)stage * (kScanABytes >> 4));
+            const uint64_t da = da0 + (uint64_t)((uint32_t)stage * (ABYTES >> 4));
             const uint64_t db = db0 + (uint64_t)((uint32_t)stage * (prm.b_bytes >> 4));
 #pragma unroll
-            for (int h = 0; h < 2; ++h)
+            for (int h = 0; h < 2 / CG; ++h)
 #pragma unroll
               for (int kk = 0; kk < kBlockK / 16; ++kk)
-                ptx::umma_f16<1>(d0 + (uint32_t)(h * NQ), da + (uint64_t)(h * (kScanHalfBytes >> 4) + 2 * kk),
-                                 db + (uint64_t)(2 * kk), prm.idesc, (kb | kk) != 0 ? 1u : 0u);
-            ptx::umma_commit<1>(&empty[stage]);
+                ptx::umma_f16<CG>(d0 + (uint32_t)(h * NQ), da + (uint64_t)(h * (kScanHalfBytes >> 4) + 2 * kk),
+                                  db + (uint64_t)(2 * kk), prm.idesc, (kb | kk) != 0 ? 1u : 0u);
+            ptx::umma_commit<CG>(&empty[stage]);
           }
           __syncwarp();
           if (++stage == STAGES) {
@@ -235,7 +256,7 @@ __global__ void __launch_bounds__(kScanThreads, 1)
             phase ^= 1u;
           }
         }
-        if (ptx::elect_one()) ptx::umma_commit<1>(&tfull[buf]);
+        if (ptx::elect_one()) ptx::umma_commit<CG>(&tfull[buf]);
         __syncwarp();
       }
     }
@@ -252,8 +273,9 @@ __global__ void __launch_bounds__(kScanThreads, 1)
     ptx::named_bar_sync(1, 32 * kScanEpiWarps);
     float* tr = trs + lg * 32 * kTPad;
     float* mythr = thr + lg * NQ;
+    const uint32_t tempty_leader0 = CG == 2 ? ptx::mapa(ptx::smem_u32(&tempty[0]), 0) : 0u;
     uint32_t tile_count = 0;
-    for (int u = blockIdx.x; u < prm.S; u += gridDim.x) {
+    for (int u = cid; u < prm.S; u += ncl) {
       int t_lo, t_hi;
       scan_split(u, prm.S, prm.n_pt, t_lo, t_hi);
       // lane q owns query sl*32 + q of every slot sl: its list and its shared bound
@@ -281,9 +303,9 @@ __global__ void __launch_bounds__(kScanThreads, 1)
         const float* jsm = reinterpret_cast<const float*>(sAux + buf * AUX);
         const float* inv_sm = reinterpret_cast<const float*>(sAux + buf * AUX + AUXJ);
 #pragma unroll 1
-        for (int h = 0; h < 2; ++h) {
-          const int r = h * 128 + lg * 32 + lane;   // row within the tile
-          const int32_t rowbase = t * kBlockN + h * 128 + lg * 32;
+        for (int h = 0; h < 2 / CG; ++h) {
+          const int r = (h + (int)crank) * 128 + lg * 32 + lane;   // row within the tile
+          const int32_t rowbase = t * kBlockN + (h + (int)crank) * 128 + lg * 32;
           const bool valid = (int64_t)rowbase + lane < prm.L;
           float pj[JP];
 #pragma unroll
@@ -295,7 +317,7 @@ __global__ void __launch_bounds__(kScanThreads, 1)
             if (sl >= nsl) break;
             const int c0 = sl * 32;
             const uint32_t taddr =
-                tmem_base + ((uint32_t)(lg * 32) << 16) + (uint32_t)(buf * 2 * NQ + h * NQ + c0);
+                tmem_base + ((uint32_t)(lg * 32) << 16) + (uint32_t)(buf * (2 / CG) * NQ + h * NQ + c0);
             uint32_t elig = valid ? 0xFFFFFFFFu : 0u;   // pairs (this row, query c0 + c) that may enter
             if (GATED) {
               // partial canonical distance over joints 0..3 for the 32 queries, two at a time
@@ -377,7 +399,10 @@ __global__ void __launch_bounds__(kScanThreads, 1)
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          ptx::mbar_arrive(&tempty[buf]);
+          if (CG == 1)
+            ptx::mbar_arrive(&tempty[buf]);
+          else
+            ptx::mbar_arrive_cluster(tempty_leader0 + (uint32_t)(buf * sizeof(uint64_t)));
           ptx::mbar_arrive(&aempty[buf]);
         }
         // share the admission bound with the other CTAs (publish improvements only).
@@ -406,7 +431,7 @@ __global__ void __launch_bounds__(kScanThreads, 1)
               // l mod k; the lists hold disjoint rows, so once all k slots are filled
               // their minimum is the score of one of k distinct rows, <= the k-th best
               uint32_t* sq = prm.slots + (int64_t)c * KT;
-              const int l = u * kScanEpiWarps + lg;
+              const int l = (u * CG + (int)crank) * kScanEpiWarps + lg;
               if (top[sl].s[0] > -CUDART_INF_F) atomicMax(sq + l % prm.k, ptx::f2ord(top[sl].s[0]));
               uint32_t mn = 0xFFFFFFFFu;
 #pragma unroll
@@ -427,7 +452,7 @@ __global__ void __launch_bounds__(kScanThreads, 1)
       for (int sl = 0; sl < NSL; ++sl) {
         const int c = sl * 32 + lane;
         if (sl < nsl && c < nq) {
-          const int64_t base = ((int64_t)c * prm.P + (int64_t)u * kScanEpiWarps + lg) * KT;
+          const int64_t base = ((int64_t)c * prm.P + ((int64_t)u * CG + crank) * kScanEpiWarps + lg) * KT;
 #pragma unroll
           for (int rr = 0; rr < KT; rr += 4) {
             *reinterpret_cast<float4*>(prm.part_s + base + rr) =
@@ -443,9 +468,10 @@ __global__ void __launch_bounds__(kScanThreads, 1)
 
   ptx::tc_fence_before();
   __syncthreads();
+  if (CG == 2) ptx::cluster_sync();   // no CTA leaves while its peer may still signal it
   if (warp == kMmaWarp) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<1>(tmem_base, 512);
+    ptx::tmem_dealloc<CG>(tmem_base, 512);
   }
 }
 
@@ -453,50 +479,67 @@ __global__ void __launch_bounds__(kScanThreads, 1)
 int scan_box(int NQ) { return NQ <= 32 ? 32 : NQ <= 64 ? 64 : 128; }
 int box_index(int box) { return box == 16 ? 0 : box == 32 ? 1 : box == 64 ? 2 : 3; }
 
-template <int KT, int JP, bool G>
+template <int KT, int JP, bool G, int CG>
 cudaError_t launch_scan_t(Pool& p, const ScanParams& prm, int box, int grid, cudaStream_t s) {
-  auto kern = match_scan_kernel<KT, JP, G>;
-  const size_t smem = scan_layout(prm.stages, prm.b_bytes, JP, prm.NQ).total;
+  auto kern = match_scan_kernel<KT, JP, G, CG>;
+  const size_t smem = scan_layout(prm.stages, prm.b_bytes, JP, prm.NQ, CG).total;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kern<<<grid, kScanThreads, smem, s>>>(p.tmap_qs[box_index(box)], p.tmap_pool, prm);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kScanThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, p.tmap_qs[box_index(box)], CG == 1 ? p.tmap_pool : p.tmap_pool2, prm);
 }
 
-template <int KT, bool G>
+template <int KT, bool G, int CG>
 cudaError_t launch_scan_kt(Pool& p, const ScanParams& prm, int box, int grid, cudaStream_t s) {
   switch (p.JP) {
-    case 4: return launch_scan_t<KT, 4, G>(p, prm, box, grid, s);
-    case 8: return launch_scan_t<KT, 8, G>(p, prm, box, grid, s);
-    default: return launch_scan_t<KT, 16, G>(p, prm, box, grid, s);
+    case 4: return launch_scan_t<KT, 4, G, CG>(p, prm, box, grid, s);
+    case 8: return launch_scan_t<KT, 8, G, CG>(p, prm, box, grid, s);
+    default: return launch_scan_t<KT, 16, G, CG>(p, prm, box, grid, s);
   }
 }
 
 template <bool G>
-cudaError_t launch_scan_g(Pool& p, const MatchArgs& a, const ScanParams& prm, int box, int grid, cudaStream_t s) {
+cudaError_t launch_scan_g(Pool& p, const MatchArgs& a, const ScanParams& prm, int box, int grid, int cg,
+                          cudaStream_t s) {
+  if (cg == 2) return launch_scan_kt<8, G, 2>(p, prm, box, grid, s);   // eligibility: KT = 8 only
   switch (a.KT) {
-    case 8: return launch_scan_kt<8, G>(p, prm, box, grid, s);
-    case 16: return launch_scan_kt<16, G>(p, prm, box, grid, s);
-    default: return launch_scan_kt<32, G>(p, prm, box, grid, s);
+    case 8: return launch_scan_kt<8, G, 1>(p, prm, box, grid, s);
+    case 16: return launch_scan_kt<16, G, 1>(p, prm, box, grid, s);
+    default: return launch_scan_kt<32, G, 1>(p, prm, box, grid, s);
   }
 }
 
 }  // namespace
 
+int scan_cg(int nq) { return nq > kBlockM ? 2 : 1; }
+
 int scan_stages(const Pool& p, int nq, int KT) {
-  if (nq < 1 || nq > kBlockM || KT > 32) return 0;
+  const int cg = scan_cg(nq);
+  if (nq < 1 || nq > kBlockM * cg || KT > 32 || (cg == 2 && KT != 8)) return 0;
   const int NQ = (nq + 31) / 32 * 32;
   if (NQ * KT > kScanListRegs) return 0;   // register lists: (NQ / 32) x KT entries per lane
-  const uint32_t b_bytes = (uint32_t)scan_box(NQ) * kBlockK * 2;
+  const uint32_t b_bytes = (uint32_t)scan_box(NQ / cg) * kBlockK * 2;
   for (int st = 6; st >= 3; --st)
-    if (scan_layout(st, b_bytes, p.JP, NQ).total <= kSmemLimit) return st;
+    if (scan_layout(st, b_bytes, p.JP, NQ, cg).total <= kSmemLimit) return st;
   return 0;
 }
 
 cudaError_t launch_match_scan(Pool& p, const MatchArgs& a, int32_t S, int32_t grid, cudaStream_t s) {
   ScanParams prm{};
+  const int cg = scan_cg(a.nq);
   const int NQ = (a.nq + 31) / 32 * 32;
-  const int box = scan_box(NQ);
+  const int box = scan_box(NQ / cg);
   prm.inv_q = p.q_inv;
   prm.q_joints = p.q_joints;
   prm.pool_inv = p.inv_norm;
@@ -510,13 +553,13 @@ cudaError_t launch_match_scan(Pool& p, const MatchArgs& a, int32_t S, int32_t gr
   prm.d = p.cfg.dim;
   prm.n_pt = (int32_t)((p.local + kBlockN - 1) / kBlockN);
   prm.S = S;
-  prm.P = S * kScanEpiWarps;
+  prm.P = S * kScanEpiWarps * cg;
   prm.stages = scan_stages(p, a.nq, a.KT);
   prm.b_bytes = (uint32_t)box * kBlockK * 2;
-  prm.idesc = ptx::idesc_bf16_f32(kBlockM, (uint32_t)NQ);
+  prm.idesc = ptx::idesc_bf16_f32(kBlockM * cg, (uint32_t)NQ);
   prm.g2 = a.g2;
   prm.k = a.k;
-  if (prm.stages == 0) return cudaErrorInvalidValue;
+  if (prm.stages == 0 || grid % cg != 0) return cudaErrorInvalidValue;
   cudaError_t e = cudaMemsetAsync(p.bound, 0, (size_t)(a.nq + 1) * sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
   prm.slots = a.slots ? p.slots : nullptr;
@@ -524,11 +567,11 @@ cudaError_t launch_match_scan(Pool& p, const MatchArgs& a, int32_t S, int32_t gr
     e = cudaMemsetAsync(p.slots, 0, (size_t)a.nq * a.KT * sizeof(uint32_t), s);
     if (e != cudaSuccess) return e;
   }
-  e = a.gated ? launch_scan_g<true>(p, a, prm, box, grid, s) : launch_scan_g<false>(p, a, prm, box, grid, s);
+  e = a.gated ? launch_scan_g<true>(p, a, prm, box, grid, cg, s) : launch_scan_g<false>(p, a, prm, box, grid, cg, s);
   ++p.launches;
   return e;
 }
 
-int scan_lists_per_split() { return kScanEpiWarps; }
+int scan_lists_per_split(int nq) { return kScanEpiWarps * scan_cg(nq); }
 
 }  // namespace ams

@@ -1,5 +1,6 @@
 """GPU parity of the small-batch tcgen05 kernel (plan id 4: pool rows on the MMA M side,
-the nq <= 128 queries on N) against the CPU oracle, and against the 128-query-tile
+the queries on N; nq <= 128 on one CTA per 256-row tile, 128 < nq <= 256 with k <= 8 on
+a CTA pair) against the CPU oracle, and against the 128-query-tile
 kernel (plan id 1) on the same inputs.
 
 Covers every query-box size (NQ = 32, 64, 128 = round_up(nq, 32)),
@@ -31,10 +32,13 @@ def dev_t(a):
 
 
 def scan_eligible(nq, k):
-    """The library's rule: nq <= 128, KT <= 32 and round_up(nq, 32) * KT <= 2048 (the
-    per-lane register lists)."""
+    """The library's rule: KT <= 32 and round_up(nq, 32) * KT <= 2048 (the per-lane
+    register lists); nq <= 128 on one CTA per tile, 128 < nq <= 256 on a CTA pair with
+    KT = 8 only."""
     KT = 8 if k <= 8 else 16 if k <= 16 else 32 if k <= 32 else 64
-    return nq <= 128 and KT <= 32 and -(-nq // 32) * 32 * KT <= 2048
+    if nq > 128:
+        return nq <= 256 and KT == 8
+    return KT <= 32 and -(-nq // 32) * 32 * KT <= 2048
 
 
 def run(ams, pool, q, qj, k, theta, gamma, policy=0):
@@ -46,7 +50,7 @@ def run(ams, pool, q, qj, k, theta, gamma, policy=0):
 
 
 @pytest.mark.parametrize("name,M", [("c2", 3001), ("c3", 2600), ("c5", 700)])
-@pytest.mark.parametrize("nq", [1, 5, 16, 17, 33, 64, 100, 128])
+@pytest.mark.parametrize("nq", [1, 5, 16, 17, 33, 64, 100, 128, 129, 200, 256])
 def test_scan_kernel_parity(ams, name, M, nq):
     cfg = ams_gen.small_variant(name, M, nq)
     w = ams_gen.generate_host(cfg)
@@ -55,7 +59,7 @@ def test_scan_kernel_parity(ams, name, M, nq):
         for gamma in (cfg.gamma, 1.5, INF):
             orc = oracle.match(w.emb, w.joints, w.q_emb, w.q_joints, cfg.k, cfg.theta, gamma)
             g, plan = run(ams, pool, w.q_emb, w.q_joints, cfg.k, cfg.theta, gamma)
-            assert plan["kernel_id"] == (4 if scan_eligible(nq, cfg.k) else 1)
+            assert plan["kernel_id"] == (4 if scan_eligible(nq, cfg.k) else 1 if nq <= 128 else 2)
             stats = check_bf16(*g, orc, cfg.theta)
             if gamma == cfg.gamma:
                 assert np.array_equal(g[2].astype(bool), w.labels >= 0)   # P10 by construction
@@ -84,12 +88,13 @@ def test_scan_kernel_topk_widths_and_fallback(ams, k, nq):
 
 
 @pytest.mark.parametrize("M", [1, 37, 255, 256, 257, 513])
-def test_scan_kernel_tiny_and_ragged_pools(ams, M):
-    cfg = ams_gen.small_variant("c3", M, 20)
+@pytest.mark.parametrize("nq", [20, 150])
+def test_scan_kernel_tiny_and_ragged_pools(ams, M, nq):
+    cfg = ams_gen.small_variant("c3", M, nq)
     w = ams_gen.generate_host(cfg)
-    with ams.Pool(cfg.d, cfg.J, cfg.M, 64, 16) as pool:
+    with ams.Pool(cfg.d, cfg.J, cfg.M, 256, 16) as pool:
         pool.append(dev_t(w.emb), dev_t(w.joints))
-        for k in (1, 16):
+        for k in ((1, 16) if nq <= 128 else (1, 8)):
             for gamma in (0.3, INF):
                 orc = oracle.match(w.emb, w.joints, w.q_emb, w.q_joints, k, cfg.theta, gamma)
                 g, plan = run(ams, pool, w.q_emb, w.q_joints, k, cfg.theta, gamma)
