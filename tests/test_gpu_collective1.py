@@ -53,8 +53,9 @@ def run(ams, w, cfg, k, gamma, collective, peer=False, gate_first=False, block=0
 
 @pytest.mark.parametrize("gamma", [0.3, math.inf])
 @pytest.mark.parametrize("peer", [False, True])
-def test_collective_path_bf16(ams, gamma, peer):
-    cfg = ams_gen.small_variant("c2", 7000, 600)
+@pytest.mark.parametrize("name,nq", [("c2", 600), ("c2", 64), ("c5", 200)])   # CTA-pair tiles; small-batch kernel
+def test_collective_path_bf16(ams, gamma, peer, name, nq):
+    cfg = ams_gen.small_variant(name, 7000, nq)
     w = ams_gen.generate_host(cfg)
     orc = oracle.match(w.emb, w.joints, w.q_emb, w.q_joints, cfg.k, cfg.theta, gamma)
     got = run(ams, w, cfg, cfg.k, gamma, collective=True, peer=peer)
