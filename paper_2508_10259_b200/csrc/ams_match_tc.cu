@@ -73,7 +73,6 @@ constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kABytes = kBlockM * kBlockK * 2;   // 16 KB: 128 query rows x 128 B
 constexpr int kColsPerHalf = kBlockN / kEpiHalves;    // 128
 constexpr int kChunk = 32;
-constexpr int kRefreshTiles = 1;                      // bound publish/refresh period (tiles)
 
 template <int CG>
 struct Geo {
@@ -106,6 +105,11 @@ struct Aux {
   static constexpr uint32_t bytes = j_bytes + kBlockN * 4;
 };
 
+// Per-tile joints / inverse norms ring.  Three deep: the producer loads tile t+1's aux
+// before its k-blocks, and with two buffers it waited for the epilogue of tile t-1,
+// which only starts when the MMA of t-1 ends -- a slow epilogue then starved the MMA.
+constexpr int kAuxDepth = 3;
+
 template <int JP, int CG>
 __host__ __device__ constexpr int stages_for() {
   return CG == 1 ? (JP >= 16 ? 3 : 4) : (JP >= 16 ? 5 : 6);
@@ -113,7 +117,7 @@ __host__ __device__ constexpr int stages_for() {
 
 template <int JP, int CG>
 __host__ __device__ constexpr size_t smem_for() {
-  return 1024 /*align slack*/ + (size_t)stages_for<JP, CG>() * Geo<CG>::stage_bytes + 2 * Aux<JP>::bytes + 256;
+  return 1024 /*align slack*/ + (size_t)stages_for<JP, CG>() * Geo<CG>::stage_bytes + kAuxDepth * Aux<JP>::bytes + 256;
 }
 
 __device__ __forceinline__ void split_tiles(int sp, int S, int n_pt, int& t_lo, int& t_hi) {
@@ -287,15 +291,15 @@ __global__ void __maxnreg__(168)
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;                                   // STAGES x 16 KB
   uint8_t* sB = smem + STAGES * kABytes;                // STAGES x BBYTES
-  uint8_t* sAux = smem + STAGES * STAGE;                // 2 x AUX
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sAux + 2 * AUX);
+  uint8_t* sAux = smem + STAGES * STAGE;                // kAuxDepth x AUX
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sAux + kAuxDepth * AUX);
   uint64_t* full = bars;
   uint64_t* empty = bars + STAGES;
   uint64_t* tfull = bars + 2 * STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* afull = tfull + 4;
-  uint64_t* aempty = tfull + 6;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tfull + 8);
+  uint64_t* aempty = afull + kAuxDepth;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(aempty + kAuxDepth);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -320,6 +324,8 @@ __global__ void __maxnreg__(168)
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&tfull[i], 1);
       ptx::mbar_init(&tempty[i], 4 * kEpiHalves * CG);
+    }
+    for (int i = 0; i < kAuxDepth; ++i) {
       ptx::mbar_init(&afull[i], 1);
       ptx::mbar_init(&aempty[i], 4 * kEpiHalves);
     }
@@ -372,14 +378,14 @@ __global__ void __maxnreg__(168)
           __syncwarp();   // lanes may leave the spin at different iterations
         }
         for (int t = t_lo; t < t_hi; ++t, ++tile_count) {
-          const int buf = tile_count & 1;
-          const uint32_t use = tile_count >> 1;
-          ptx::mbar_wait(&aempty[buf], (use & 1u) ^ 1u);
+          const int abuf = (int)(tile_count % kAuxDepth);
+          const uint32_t ause = tile_count / kAuxDepth;
+          ptx::mbar_wait(&aempty[abuf], (ause & 1u) ^ 1u);
           if (ptx::elect_one()) {
-            uint8_t* aux = sAux + buf * AUX;
-            ptx::mbar_arrive_expect_tx(&afull[buf], AUX);
-            ptx::bulk_load(aux, prm.pool_joints + (int64_t)t * kBlockN * JP, AUXJ, &afull[buf]);
-            ptx::bulk_load(aux + AUXJ, prm.pool_inv + (int64_t)t * kBlockN, kBlockN * 4, &afull[buf]);
+            uint8_t* aux = sAux + abuf * AUX;
+            ptx::mbar_arrive_expect_tx(&afull[abuf], AUX);
+            ptx::bulk_load(aux, prm.pool_joints + (int64_t)t * kBlockN * JP, AUXJ, &afull[abuf]);
+            ptx::bulk_load(aux + AUXJ, prm.pool_inv + (int64_t)t * kBlockN, kBlockN * 4, &afull[abuf]);
           }
           __syncwarp();
           const int prow0 = t * kBlockN + (int)prank * (int)Geo<CG>::b_rows;
@@ -546,14 +552,14 @@ __global__ void __maxnreg__(168)
       }
       TopK<KT, int32_t> top;
       top.init(active);
-      int since = 0;
       for (int t = t_lo; t < t_hi; ++t, ++tile_count) {
         const int buf = tile_count & 1;
         const uint32_t use = tile_count >> 1;
-        ptx::mbar_wait(&afull[buf], use & 1u);
+        const int abuf = (int)(tile_count % kAuxDepth);
+        ptx::mbar_wait(&afull[abuf], (tile_count / kAuxDepth) & 1u);
         ptx::mbar_wait(&tfull[buf], use & 1u);
         ptx::tc_fence_after();
-        const uint8_t* aux = sAux + buf * AUX;
+        const uint8_t* aux = sAux + abuf * AUX;
         const float* joints_sm = reinterpret_cast<const float*>(aux);
         const float* inv_sm = reinterpret_cast<const float*>(aux + AUXJ);
         float ie_min = 0.0f, ie_max = 0.0f;   // inverse-norm range of this warp's column half
@@ -593,11 +599,16 @@ __global__ void __maxnreg__(168)
             ptx::mbar_arrive(&tempty[buf]);
           else
             ptx::mbar_arrive_cluster(tempty_leader0 + (uint32_t)(buf * sizeof(uint64_t)));
-          ptx::mbar_arrive(&aempty[buf]);
+          ptx::mbar_arrive(&aempty[abuf]);
         }
         // share the admission bound with the other splits of this query
-        if (++since == kRefreshTiles || t + 1 == t_hi) {
-          since = 0;
+        // Geometric schedule (after 1, 2, 4, 8, ... tiles of the unit, and at its end):
+        // bounds move fast early and slowly later, and the reload is an L2 round trip
+        // whose latency the two epilogue warps of a sub-partition cannot hide when the
+        // MMA of a tile is short (d = 768: the per-tile refresh left the tensor pipe
+        // idle ~20 % of the time).
+        const int done = t - t_lo + 1;
+        if ((done & (done - 1)) == 0 || t + 1 == t_hi) {
           if (active) {
             if (top.kth_s > -CUDART_INF_F) atomicMax(bnd, ptx::f2ord(top.kth_s));
             const uint32_t b = ptx::ld_relaxed_gpu(bnd);
