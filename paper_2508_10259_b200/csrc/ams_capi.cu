@@ -196,7 +196,8 @@ void free_all(Pool& p) {
   }
   if (p.copy_stream) cudaStreamDestroy(p.copy_stream);
   p.copy_stream = nullptr;
-  void* ptrs[] = {p.emb, p.inv_norm, p.joints, p.q_stage, p.q_inv, p.q_joints, p.q_joints_raw[0], p.q_joints_raw[1],
+  void* ptrs[] = {p.scan_glist_s, p.scan_glist_i, p.emb, p.inv_norm, p.joints, p.q_stage, p.q_inv, p.q_joints,
+                  p.q_joints_raw[0], p.q_joints_raw[1],
                   p.q_raw[0], p.q_raw[1], p.q_perm, p.bound, p.slots,
                   p.gf_cnt, p.gf_cand, p.snap_j, p.snap_id, p.snap_off, p.snap_aux,
                   p.part_s, p.part_i, p.shard_s, p.shard_i, p.gath_s, p.gath_i, p.stage_emb,
@@ -343,6 +344,10 @@ ams_status_t ams_pool_create(const ams_pool_config_t* cfg, ams_pool_t* out) {
             alloc((void**)&p.shard_i, (size_t)c.max_queries * c.max_k * 8) &&
             alloc(&p.stage_emb, (size_t)p.stage_rows * d * es) &&
             alloc((void**)&p.stage_joints, (size_t)p.stage_rows * c.joint_dim * 4);
+  if (ok && c.dtype == AMS_DTYPE_BF16) {
+    const size_t gl = (size_t)p.num_sms * 4 * 8 * 8 * 32;   // see Pool::scan_glist_s
+    ok = alloc((void**)&p.scan_glist_s, gl * 4) && alloc((void**)&p.scan_glist_i, gl * 4);
+  }
   if (ok && c.dtype == AMS_DTYPE_BF16) {
     p.gf_cap = std::max(256, 8 * c.max_k);
     ok = alloc((void**)&p.gf_cnt, (size_t)p.q_pad * 4) && alloc((void**)&p.gf_cand, (size_t)p.q_pad * p.gf_cap * 4);

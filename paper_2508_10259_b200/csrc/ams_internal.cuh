@@ -116,6 +116,10 @@ struct Pool {
   void* stage_emb = nullptr;
   float* stage_joints = nullptr;
 
+  // small-batch kernel on CTA pairs: per (CTA, epilogue warp) list workspace,
+  // [num_sms][4 warps][8 slots][8 entries][32 lanes] scores and local rows
+  float* scan_glist_s = nullptr;
+  int32_t* scan_glist_i = nullptr;
   uint32_t* bound = nullptr;  // [q_pad] per-query admission lower bound (tcgen05 path)
   uint32_t* slots = nullptr;  // [q_pad][KT_max] union-bound slots (tcgen05 path, ungated)
 

@@ -68,6 +68,8 @@ struct ScanParams {
   int32_t* part_i;
   uint32_t* bound;           // [nq] ordered-u32 admission lower bound (0 = none)
   uint32_t* slots;           // [nq][KT] union-bound slots (ordered-u32; ungated with P >= k, else null)
+  float* glist_s;            // CG = 2: per (CTA, epilogue warp) lists [slot][KT][32 lanes]
+  int32_t* glist_i;
   int64_t L;                 // local rows
   int32_t nq, NQ, d, n_pt, S, P, stages, k;
   uint32_t b_bytes;          // query stage bytes (box rows x 128 B)
@@ -77,11 +79,11 @@ struct ScanParams {
 
 // shared-memory layout (byte offsets from the 1024-aligned base), host and device
 struct ScanLayout {
-  uint32_t a, b, aux, tr, qj, iq, thr, bars, total;
+  uint32_t a, b, aux, tr, qj, iq, thr, ls, li, bars, total;
 };
 
 // cg = 2: a CTA stages 128 of the pair's 256 pool rows per stage
-__host__ __device__ inline ScanLayout scan_layout(int stages, uint32_t b_bytes, int JP, int NQ, int cg) {
+__host__ __device__ inline ScanLayout scan_layout(int stages, uint32_t b_bytes, int JP, int NQ, int cg, int KT) {
   ScanLayout l{};
   uint32_t o = 0;
   l.a = o;
@@ -89,7 +91,7 @@ __host__ __device__ inline ScanLayout scan_layout(int stages, uint32_t b_bytes, 
   l.b = o;
   o += (uint32_t)stages * b_bytes;
   l.aux = o;
-  o += 2u * (uint32_t)(kBlockN * JP * 4 + kBlockN * 4);
+  o += 2u * (uint32_t)((kBlockN / cg) * JP * 4 + (kBlockN / cg) * 4);   // joints + inv of this CTA's rows
   l.tr = o;
   o += (uint32_t)(kScanEpiWarps * 32 * kTPad * 4 + 64);   // + keep 16-B alignment below
   l.qj = o;
@@ -98,6 +100,7 @@ __host__ __device__ inline ScanLayout scan_layout(int stages, uint32_t b_bytes, 
   o += (uint32_t)(NQ * 4);
   l.thr = o;
   o += (uint32_t)(kScanEpiWarps * NQ * 4);
+  l.ls = l.li = o;   // (lists: registers for cg = 1, global memory for cg = 2)
   l.bars = o;
   o += 256;
   l.total = o + 1024;   // alignment slack
@@ -117,8 +120,14 @@ template <int KT, int JP, bool GATED, int CG>
 __global__ void __launch_bounds__(kScanThreads, 1)
     match_scan_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_pool,
                       const ScanParams prm) {
-  constexpr uint32_t AUXJ = kBlockN * JP * 4;
-  constexpr uint32_t AUX = AUXJ + kBlockN * 4;
+  // CG = 2 keeps the lists in global memory (L2-resident, private to each warp, touched
+  // only on inserts): in registers 8 slots (112 registers) made ptxas serialise the gate
+  // filter's loads and spill; in shared memory they cost pipeline stages, and the
+  // HBM stream needs the stages (C5: 3 stages 7.4 ms vs 6.3 ms per 129-256-query call)
+  constexpr bool SMEM_LISTS = CG == 2;   // (name kept: the lists are out of registers)
+  constexpr int AROWS = kBlockN / CG;              // tile rows this CTA owns (aux ring)
+  constexpr uint32_t AUXJ = AROWS * JP * 4;
+  constexpr uint32_t AUX = AUXJ + AROWS * 4;
   constexpr uint32_t ABYTES = kScanABytes / CG;   // pool rows staged per CTA and stage
   constexpr int NQMAX = 128 * CG;
   constexpr int NSL0 = kScanListRegs / (32 * KT);
@@ -127,7 +136,7 @@ __global__ void __launch_bounds__(kScanThreads, 1)
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   const int NQ = prm.NQ;
   const int STAGES = prm.stages;
-  const ScanLayout lay = scan_layout(STAGES, prm.b_bytes, JP, NQ, CG);
+  const ScanLayout lay = scan_layout(STAGES, prm.b_bytes, JP, NQ, CG, KT);
   uint8_t* sA = smem + lay.a;
   uint8_t* sB = smem + lay.b;
   uint8_t* sAux = smem + lay.aux;
@@ -135,6 +144,8 @@ __global__ void __launch_bounds__(kScanThreads, 1)
   float* qjs = reinterpret_cast<float*>(smem + lay.qj);   // [JP][NQ]
   float* iqs = reinterpret_cast<float*>(smem + lay.iq);   // [NQ]
   float* thr = reinterpret_cast<float*>(smem + lay.thr);  // [warps][NQ]
+  float* lsm = prm.glist_s + (int64_t)blockIdx.x * kScanEpiWarps * NSL * KT * 32;   // SMEM_LISTS
+  int32_t* lim = prm.glist_i + (int64_t)blockIdx.x * kScanEpiWarps * NSL * KT * 32;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + lay.bars);
   uint64_t* full = bars;
   uint64_t* empty = bars + STAGES;
@@ -194,8 +205,15 @@ __global__ void __launch_bounds__(kScanThreads, 1)
         if (ptx::elect_one()) {
           uint8_t* aux = sAux + buf * AUX;
           ptx::mbar_arrive_expect_tx(&afull[buf], AUX);
-          ptx::bulk_load(aux, prm.pool_joints + (int64_t)t * kBlockN * JP, AUXJ, &afull[buf]);
-          ptx::bulk_load(aux + AUXJ, prm.pool_inv + (int64_t)t * kBlockN, kBlockN * 4, &afull[buf]);
+          if (CG == 1) {
+            ptx::bulk_load(aux, prm.pool_joints + (int64_t)t * kBlockN * JP, AUXJ, &afull[buf]);
+          } else {   // this CTA's 128 columns of each joint row of the [JP][256] tile block
+#pragma unroll
+            for (int tj = 0; tj < JP; ++tj)
+              ptx::bulk_load(aux + tj * AROWS * 4, prm.pool_joints + ((int64_t)t * JP + tj) * kBlockN + crank * AROWS,
+                             AROWS * 4, &afull[buf]);
+          }
+          ptx::bulk_load(aux + AUXJ, prm.pool_inv + (int64_t)t * kBlockN + crank * AROWS, AROWS * 4, &afull[buf]);
         }
         __syncwarp();
         for (int kb = 0; kb < n_kb; ++kb) {
@@ -279,13 +297,27 @@ __global__ void __launch_bounds__(kScanThreads, 1)
       int t_lo, t_hi;
       scan_split(u, prm.S, prm.n_pt, t_lo, t_hi);
       // lane q owns query sl*32 + q of every slot sl: its list and its shared bound
-      TopK<KT, int32_t> top[NSL];
+      TopK<KT, int32_t> top[SMEM_LISTS ? 1 : NSL];
+      float kth_s[NSL], best_s[NSL];   // SMEM_LISTS: each list's KT-th and best score
+      float* wls = lsm + lg * NSL * KT * 32;   // this warp's lists (SMEM_LISTS)
+      int32_t* wli = lim + lg * NSL * KT * 32;
       float bnd[NSL];
 #pragma unroll
       for (int sl = 0; sl < NSL; ++sl) {
         const int c = sl * 32 + lane;
         const bool act = sl < nsl && c < nq;
-        top[sl].init(act);   // inactive: kth = +inf, never admits
+        if constexpr (SMEM_LISTS) {
+          kth_s[sl] = act ? -CUDART_INF_F : CUDART_INF_F;   // inactive: never admits
+          best_s[sl] = -CUDART_INF_F;
+          if (sl < nsl)
+#pragma unroll
+            for (int rr = 0; rr < KT; ++rr) {
+              wls[(sl * KT + rr) * 32 + lane] = -CUDART_INF_F;
+              wli[(sl * KT + rr) * 32 + lane] = -1;
+            }
+        } else {
+          top[SMEM_LISTS ? 0 : sl].init(act);   // inactive: kth = +inf, never admits
+        }
         bnd[sl] = -CUDART_INF_F;
         if (act) {
           const uint32_t v = ptx::ld_relaxed_gpu(prm.bound + c);
@@ -309,8 +341,9 @@ __global__ void __launch_bounds__(kScanThreads, 1)
           const bool valid = (int64_t)rowbase + lane < prm.L;
           float pj[JP];
 #pragma unroll
-          for (int tj = 0; tj < JP; ++tj) pj[tj] = jsm[tj * kBlockN + r];
-          const float ie = inv_sm[r];
+          const int ra = h * 128 + lg * 32 + lane;   // row within this CTA's aux block
+          for (int tj = 0; tj < JP; ++tj) pj[tj] = jsm[tj * AROWS + ra];
+          const float ie = inv_sm[ra];
           const uint64_t IE2 = ptx::pack2(ie, ie);
 #pragma unroll
           for (int sl = 0; sl < NSL; ++sl) {
@@ -383,8 +416,31 @@ __global__ void __launch_bounds__(kScanThreads, 1)
             for (int c = 0; c < 32; ++c)
               tr[c * kTPad + lane] = ((fire >> c) & 1u) != 0u ? __uint_as_float(v[c]) : -CUDART_INF_F;
             __syncwarp();
-            {
-              TopK<KT, int32_t>& tp = top[sl];
+            if constexpr (SMEM_LISTS) {
+              TopK<KT, int32_t> tp;
+#pragma unroll
+              for (int rr = 0; rr < KT; ++rr) {
+                tp.s[rr] = wls[(sl * KT + rr) * 32 + lane];
+                tp.i[rr] = wli[(sl * KT + rr) * 32 + lane];
+              }
+              tp.kth_s = kth_s[sl];
+              tp.kth_i = tp.i[KT - 1];
+              const float b = bnd[sl];
+#pragma unroll 4
+              for (int rr = 0; rr < 32; ++rr) {
+                const float x = tr[lane * kTPad + rr];
+                if (x > tp.kth_s && x >= b) tp.insert_monotone(x, rowbase + rr, 0);
+              }
+#pragma unroll
+              for (int rr = 0; rr < KT; ++rr) {
+                wls[(sl * KT + rr) * 32 + lane] = tp.s[rr];
+                wli[(sl * KT + rr) * 32 + lane] = tp.i[rr];
+              }
+              kth_s[sl] = tp.kth_s;
+              best_s[sl] = tp.s[0];
+              mythr[c0 + lane] = fmaxf(mythr[c0 + lane], tp.kth_s);
+            } else {
+              TopK<KT, int32_t>& tp = top[SMEM_LISTS ? 0 : sl];
               const float b = bnd[sl];
 #pragma unroll 4
               for (int rr = 0; rr < 32; ++rr) {
@@ -417,7 +473,8 @@ __global__ void __launch_bounds__(kScanThreads, 1)
           const int c = sl * 32 + lane;
           if (refresh && sl < nsl && c < nq) {
             uint32_t b = ptx::ld_relaxed_gpu(prm.bound + c);
-            const float kth = top[sl].kth_s;
+            const float kth = SMEM_LISTS ? kth_s[sl] : top[SMEM_LISTS ? 0 : sl].kth_s;
+            const float best = SMEM_LISTS ? best_s[sl] : top[SMEM_LISTS ? 0 : sl].s[0];
             if (kth > -CUDART_INF_F) {
               const uint32_t o = ptx::f2ord(kth);
               if (o > b) {
@@ -432,7 +489,7 @@ __global__ void __launch_bounds__(kScanThreads, 1)
               // their minimum is the score of one of k distinct rows, <= the k-th best
               uint32_t* sq = prm.slots + (int64_t)c * KT;
               const int l = (u * CG + (int)crank) * kScanEpiWarps + lg;
-              if (top[sl].s[0] > -CUDART_INF_F) atomicMax(sq + l % prm.k, ptx::f2ord(top[sl].s[0]));
+              if (best > -CUDART_INF_F) atomicMax(sq + l % prm.k, ptx::f2ord(best));
               uint32_t mn = 0xFFFFFFFFu;
 #pragma unroll
               for (int rr = 0; rr < KT; rr += 4) {
@@ -453,12 +510,22 @@ __global__ void __launch_bounds__(kScanThreads, 1)
         const int c = sl * 32 + lane;
         if (sl < nsl && c < nq) {
           const int64_t base = ((int64_t)c * prm.P + ((int64_t)u * CG + crank) * kScanEpiWarps + lg) * KT;
+          if constexpr (SMEM_LISTS) {
 #pragma unroll
-          for (int rr = 0; rr < KT; rr += 4) {
-            *reinterpret_cast<float4*>(prm.part_s + base + rr) =
-                make_float4(top[sl].s[rr], top[sl].s[rr + 1], top[sl].s[rr + 2], top[sl].s[rr + 3]);
-            *reinterpret_cast<int4*>(prm.part_i + base + rr) =
-                make_int4(top[sl].i[rr], top[sl].i[rr + 1], top[sl].i[rr + 2], top[sl].i[rr + 3]);
+            for (int rr = 0; rr < KT; ++rr) {
+              prm.part_s[base + rr] = wls[(sl * KT + rr) * 32 + lane];
+              prm.part_i[base + rr] = wli[(sl * KT + rr) * 32 + lane];
+            }
+          } else {
+#pragma unroll
+            for (int rr = 0; rr < KT; rr += 4) {
+              *reinterpret_cast<float4*>(prm.part_s + base + rr) =
+                  make_float4(top[SMEM_LISTS ? 0 : sl].s[rr], top[SMEM_LISTS ? 0 : sl].s[rr + 1],
+                              top[SMEM_LISTS ? 0 : sl].s[rr + 2], top[SMEM_LISTS ? 0 : sl].s[rr + 3]);
+              *reinterpret_cast<int4*>(prm.part_i + base + rr) =
+                  make_int4(top[SMEM_LISTS ? 0 : sl].i[rr], top[SMEM_LISTS ? 0 : sl].i[rr + 1],
+                            top[SMEM_LISTS ? 0 : sl].i[rr + 2], top[SMEM_LISTS ? 0 : sl].i[rr + 3]);
+            }
           }
         }
       }
@@ -482,7 +549,7 @@ int box_index(int box) { return box == 16 ? 0 : box == 32 ? 1 : box == 64 ? 2 : 
 template <int KT, int JP, bool G, int CG>
 cudaError_t launch_scan_t(Pool& p, const ScanParams& prm, int box, int grid, cudaStream_t s) {
   auto kern = match_scan_kernel<KT, JP, G, CG>;
-  const size_t smem = scan_layout(prm.stages, prm.b_bytes, JP, prm.NQ, CG).total;
+  const size_t smem = scan_layout(prm.stages, prm.b_bytes, JP, prm.NQ, CG, KT).total;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
@@ -531,7 +598,7 @@ int scan_stages(const Pool& p, int nq, int KT) {
   if (NQ * KT > kScanListRegs) return 0;   // register lists: (NQ / 32) x KT entries per lane
   const uint32_t b_bytes = (uint32_t)scan_box(NQ / cg) * kBlockK * 2;
   for (int st = 6; st >= 3; --st)
-    if (scan_layout(st, b_bytes, p.JP, NQ, cg).total <= kSmemLimit) return st;
+    if (scan_layout(st, b_bytes, p.JP, NQ, cg, KT).total <= kSmemLimit) return st;
   return 0;
 }
 
@@ -563,6 +630,9 @@ cudaError_t launch_match_scan(Pool& p, const MatchArgs& a, int32_t S, int32_t gr
   cudaError_t e = cudaMemsetAsync(p.bound, 0, (size_t)(a.nq + 1) * sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
   prm.slots = a.slots ? p.slots : nullptr;
+  prm.glist_s = p.scan_glist_s;
+  prm.glist_i = p.scan_glist_i;
+  if (cg == 2 && (prm.glist_s == nullptr || grid > p.num_sms)) return cudaErrorInvalidValue;
   if (prm.slots != nullptr) {
     e = cudaMemsetAsync(p.slots, 0, (size_t)a.nq * a.KT * sizeof(uint32_t), s);
     if (e != cudaSuccess) return e;

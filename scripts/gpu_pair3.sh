@@ -1,0 +1,6 @@
+PYTHONPATH=. timeout 300 python scripts/debug_pair_scan.py | grep -c "bad queries 0 "
+TIME=1 timeout 300 python scripts/scan_pair_calls.py
+timeout 900 python bench.py --workload c5 --steps 100 > gpurun_out/p3_c5.json 2> gpurun_out/p3_c5.err; echo "c5 rc=$?"
+python scripts/bench_summary.py gpurun_out/p3_c5.json c5
+python -c "import json; d=json.loads(open('gpurun_out/p3_c5.json').read().strip().splitlines()[-1]); print(d['clocks'], d['latency_ms'])"
+timeout 900 python -m pytest tests/test_gpu_scan.py tests/test_gpu_collective1.py -x -q 2>&1 | tail -2

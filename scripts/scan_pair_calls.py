@@ -12,3 +12,12 @@ for _ in range(4):
     pool.match(q[:200], qj[:200], 8, cfg.theta, cfg.gamma)
 torch.cuda.synchronize()
 print(ams.ams_pool_last_plan(pool.handle))
+if os.environ.get("TIME"):
+    for gamma in (cfg.gamma, float("inf")):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(20):
+            pool.match(q[:200], qj[:200], 8, cfg.theta, gamma)
+        e1.record(); torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 20
+        print("gamma", gamma, "ms/call", round(ms, 4), "GB/s", round(cfg.M * (2 * cfg.d + 4 * cfg.J + 4) / ms / 1e6))
