@@ -336,12 +336,11 @@ __global__ void __launch_bounds__(kScanThreads, 1)
         const float* inv_sm = reinterpret_cast<const float*>(sAux + buf * AUX + AUXJ);
 #pragma unroll 1
         for (int h = 0; h < 2 / CG; ++h) {
-          const int r = (h + (int)crank) * 128 + lg * 32 + lane;   // row within the tile
           const int32_t rowbase = t * kBlockN + (h + (int)crank) * 128 + lg * 32;
           const bool valid = (int64_t)rowbase + lane < prm.L;
+          const int ra = h * 128 + lg * 32 + lane;   // row within this CTA's aux block
           float pj[JP];
 #pragma unroll
-          const int ra = h * 128 + lg * 32 + lane;   // row within this CTA's aux block
           for (int tj = 0; tj < JP; ++tj) pj[tj] = jsm[tj * AROWS + ra];
           const float ie = inv_sm[ra];
           const uint64_t IE2 = ptx::pack2(ie, ie);
