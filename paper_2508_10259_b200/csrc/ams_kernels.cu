@@ -333,6 +333,62 @@ __device__ __forceinline__ float tc_lower_bound(const uint32_t* __restrict__ bou
   return b;
 }
 
+// One query's P partial lists into lane-held TopK lists: lanes take lists lane, lane +
+// stride, ... (heads loaded kHeads at a time so their loads are in flight together) and
+// walk each sorted list while its entries can still enter (>= lb, better than the lane's
+// KT-th).
+template <int KT>
+__device__ __forceinline__ void gather_lists(const float* __restrict__ part_s, const int32_t* __restrict__ part_i,
+                                             int q, int32_t P, int32_t k, float lb, int first, int stride,
+                                             TopK<KT, int32_t>& t) {
+  constexpr int kHeads = 8;
+  for (int p0 = first; p0 < P; p0 += stride * kHeads) {
+    float hs[kHeads];
+    int32_t hj[kHeads];
+#pragma unroll
+    for (int u = 0; u < kHeads; ++u) {
+      const int p = p0 + u * stride;
+      hj[u] = -1;
+      hs[u] = -CUDART_INF_F;
+      if (p < P) {
+        const int64_t base = ((int64_t)q * P + p) * KT;
+        hj[u] = part_i[base];
+        hs[u] = part_s[base];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kHeads; ++u) {
+      if (hj[u] < 0 || hs[u] < lb || !better(hs[u], hj[u], t.kth_s, t.kth_i)) continue;
+      t.insert(hs[u], hj[u], k);
+      const int64_t base = ((int64_t)q * P + p0 + u * stride) * KT;
+      if constexpr (KT <= 16) {
+        // the rest of the list in one round of 16-B loads (not one dependent load per entry)
+        float vs[KT];
+        int32_t vj[KT];
+#pragma unroll
+        for (int r = 0; r < KT; r += 4) {
+          const float4 a = *reinterpret_cast<const float4*>(part_s + base + r);
+          const int4 b = *reinterpret_cast<const int4*>(part_i + base + r);
+          vs[r] = a.x, vs[r + 1] = a.y, vs[r + 2] = a.z, vs[r + 3] = a.w;
+          vj[r] = b.x, vj[r + 1] = b.y, vj[r + 2] = b.z, vj[r + 3] = b.w;
+        }
+#pragma unroll
+        for (int r = 1; r < KT; ++r) {
+          if (r >= k || vj[r] < 0 || vs[r] < lb || !better(vs[r], vj[r], t.kth_s, t.kth_i)) break;
+          t.insert(vs[r], vj[r], k);
+        }
+      } else {   // long lists: registers would spill; walk entry by entry
+        for (int r = 1; r < k; ++r) {
+          const int32_t j = part_i[base + r];
+          const float v = part_s[base + r];
+          if (j < 0 || v < lb || !better(v, j, t.kth_s, t.kth_i)) break;
+          t.insert(v, j, k);
+        }
+      }
+    }
+  }
+}
+
 template <int KT>
 __global__ void merge_partials_kernel(const float* __restrict__ part_s, const int32_t* __restrict__ part_i,
                                       int32_t nq, int32_t P, int32_t k, float* __restrict__ out_s,
@@ -346,39 +402,55 @@ __global__ void merge_partials_kernel(const float* __restrict__ part_s, const in
   const float lb = tc_lower_bound(bound, slots, slot_stride, k, q);
   TopK<KT, int32_t> t;
   t.init(true);
-  // lists are sorted: walk each from its head while entries can still enter.  Heads are
-  // loaded kHeads lists at a time per lane so their loads are in flight together (most
-  // lists of a gated batch are empty).
-  constexpr int kHeads = 8;
-  for (int p0 = 0; p0 < P; p0 += 32 * kHeads) {
-    float hs[kHeads];
-    int32_t hj[kHeads];
-#pragma unroll
-    for (int u = 0; u < kHeads; ++u) {
-      const int p = p0 + u * 32 + lane;
-      hj[u] = -1;
-      hs[u] = -CUDART_INF_F;
-      if (p < P) {
-        const int64_t base = ((int64_t)q * P + p) * KT;
-        hj[u] = part_i[base];
-        hs[u] = part_s[base];
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kHeads; ++u) {
-      if (hj[u] < 0 || hs[u] < lb || !better(hs[u], hj[u], t.kth_s, t.kth_i)) continue;
-      t.insert(hs[u], hj[u], k);
-      const int64_t base = ((int64_t)q * P + p0 + u * 32 + lane) * KT;
-      for (int r = 1; r < k; ++r) {
-        const int32_t j = part_i[base + r];
-        const float v = part_s[base + r];
-        if (j < 0 || v < lb || !better(v, j, t.kth_s, t.kth_i)) break;
-        t.insert(v, j, k);
-      }
-    }
-  }
+  // lists are sorted: walk each from its head while entries can still enter (most lists
+  // of a gated batch are empty)
+  gather_lists<KT>(part_s, part_i, q, P, k, lb, lane, 32, t);
   warp_emit(t, k, lane, out_s + (int64_t)q * k, out_i + (int64_t)q * k,
             out_hit ? out_hit + q : nullptr, threshold, rank, world, B, true);
+}
+
+// Small batches with many partial lists (the small-batch kernel leaves 4-8 per row
+// split): one 128-thread block per query instead of one warp, so nq < ~1000 still fills
+// the GPU.  Each thread gathers lists t, t + 128, ... into its TopK; the lists are
+// staged in shared memory and warp 0 merges them (lane l: threads l, l + 32, l + 64,
+// l + 96) and emits the top k exactly as merge_partials_kernel does.
+constexpr int kMergeBlockThreads = 128;   // KT <= 32: <= 32 KB of staging
+
+template <int KT>
+__global__ void __launch_bounds__(kMergeBlockThreads)
+    merge_partials_block_kernel(const float* __restrict__ part_s, const int32_t* __restrict__ part_i, int32_t nq,
+                                int32_t P, int32_t k, float* __restrict__ out_s, int64_t* __restrict__ out_i,
+                                uint8_t* __restrict__ out_hit, float threshold, int32_t rank, int32_t world,
+                                int64_t B, const uint32_t* __restrict__ bound, const uint32_t* __restrict__ slots,
+                                int32_t slot_stride) {
+  __shared__ float ss[KT][kMergeBlockThreads];
+  __shared__ int32_t si[KT][kMergeBlockThreads];
+  const int q = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const float lb = tc_lower_bound(bound, slots, slot_stride, k, q);
+  TopK<KT, int32_t> t;
+  t.init(true);
+  gather_lists<KT>(part_s, part_i, q, P, k, lb, tid, kMergeBlockThreads, t);
+#pragma unroll
+  for (int r = 0; r < KT; ++r) {
+    ss[r][tid] = t.s[r];
+    si[r][tid] = t.i[r];
+  }
+  __syncthreads();
+  if (tid >= 32) return;
+  TopK<KT, int32_t> m;
+  m.init(true);
+  for (int w = 0; w < kMergeBlockThreads / 32; ++w) {
+    const int src = w * 32 + lane;
+    for (int r = 0; r < k; ++r) {
+      const int32_t j = si[r][src];
+      const float v = ss[r][src];
+      if (j < 0 || !better(v, j, m.kth_s, m.kth_i)) break;
+      m.insert(v, j, k);
+    }
+  }
+  warp_emit(m, k, lane, out_s + (int64_t)q * k, out_i + (int64_t)q * k, out_hit ? out_hit + q : nullptr,
+            threshold, rank, world, B, true);
 }
 
 template <int KT>
@@ -473,9 +545,17 @@ cudaError_t launch_merge_partials(Pool& p, const MatchArgs& a, int32_t P, float*
   const unsigned g = blocks_for(a.nq, wpb);
   const uint32_t* bnd = tc_bounds ? p.bound : nullptr;
   const uint32_t* sl = (tc_bounds && a.slots) ? p.slots : nullptr;   // filled by launch_match_tc
-#define AMS_MERGE(KT_)                                                                                 \
-  merge_partials_kernel<KT_><<<g, wpb * 32, 0, s>>>(p.part_s, p.part_i, a.nq, P, a.k, out_s, out_i, out_hit, \
-                                                     a.threshold, c.rank, c.world, p.B, bnd, sl, a.KT)
+  // few queries, many lists: a block per query (the warp-per-query grid would leave most
+  // SMs idle); KT = 64 keeps the warp kernel (64 KB of staging per block)
+  const bool per_block = a.nq < 8 * p.num_sms && P >= 64 && a.KT <= 32;
+#define AMS_MERGE(KT_)                                                                                  \
+  if (per_block)                                                                                        \
+    merge_partials_block_kernel<KT_ <= 32 ? KT_ : 32><<<(unsigned)a.nq, kMergeBlockThreads, 0, s>>>(     \
+        p.part_s, p.part_i, a.nq, P, a.k, out_s, out_i, out_hit, a.threshold, c.rank, c.world, p.B, bnd, sl, \
+        a.KT);                                                                                          \
+  else                                                                                                  \
+    merge_partials_kernel<KT_><<<g, wpb * 32, 0, s>>>(p.part_s, p.part_i, a.nq, P, a.k, out_s, out_i, out_hit, \
+                                                       a.threshold, c.rank, c.world, p.B, bnd, sl, a.KT)
   switch (a.KT) {
     case 8: AMS_MERGE(8); break;
     case 16: AMS_MERGE(16); break;
