@@ -132,6 +132,11 @@ void plan_tc(const Pool& p, int nq, int KT, int& S, int& grid, int& cg, int& cl)
     }
   }
   S = best;
+#ifdef AMS_DIAG_SPLITS_ENV   // diagnostic builds only: AMS_DIAG_SPLITS=<S> forces the split count
+  if (const char* e = getenv("AMS_DIAG_SPLITS"))
+    S = (int)std::min<int64_t>({(int64_t)atoi(e), std::max<int64_t>(1, n_pt),
+                                std::max<int64_t>(1, p.part_cap / (nq_pad * ams::kEpiHalves * KT))});
+#endif
 #ifdef AMS_DIAG_SPLIT_MULT   // diagnostic builds only: shorter units (L2-reuse experiments)
   S = (int)std::min<int64_t>({(int64_t)best * AMS_DIAG_SPLIT_MULT, std::max<int64_t>(1, n_pt),
                               std::max<int64_t>(1, p.part_cap / (nq_pad * ams::kEpiHalves * KT))});
