@@ -79,6 +79,13 @@ bool encode_bf16_map(CUtensorMap* m, void* base, int64_t rows, int32_t d, uint32
   return r == CUDA_SUCCESS;
 }
 
+// small-batch kernel: query tiles of exactly 16, 32, ..., 128 rows (box i = 16 (i + 1))
+bool encode_query_boxes(ams::Pool& p, int32_t d) {
+  for (int i = 0; i < 8; ++i)
+    if (!encode_bf16_map(&p.tmap_qs[i], p.q_stage, p.q_pad, d, (uint32_t)(16 * (i + 1)))) return false;
+  return true;
+}
+
 bool is_device_ptr(const void* ptr) {
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
@@ -371,10 +378,7 @@ ams_status_t ams_pool_create(const ams_pool_config_t* cfg, ams_pool_t* out) {
         !encode_bf16_map(&p.tmap_pool2, p.emb, p.cap_pad, d, ams::kBlockN / 2) ||
         !encode_bf16_map(&p.tmap_pool4, p.emb, p.cap_pad, d, ams::kBlockN / 4) ||
         !encode_bf16_map(&p.tmap_q, p.q_stage, p.q_pad, d, ams::kBlockM) ||
-        !encode_bf16_map(&p.tmap_qs[0], p.q_stage, p.q_pad, d, 16) ||
-        !encode_bf16_map(&p.tmap_qs[1], p.q_stage, p.q_pad, d, 32) ||
-        !encode_bf16_map(&p.tmap_qs[2], p.q_stage, p.q_pad, d, 64) ||
-        !encode_bf16_map(&p.tmap_qs[3], p.q_stage, p.q_pad, d, ams::kBlockM)) {
+        !encode_query_boxes(p, d)) {
       free_all(p);
       delete pool;
       return AMS_ERR_CUDA;

@@ -140,7 +140,7 @@ struct Pool {
   CUtensorMap tmap_pool2{};  // bf16 pool [cap_pad, d], box {64, 128}, SW128 (CTA-pair half tile)
   CUtensorMap tmap_pool4{};  // bf16 pool [cap_pad, d], box {64, 64}, SW128 (multicast quarter tile)
   CUtensorMap tmap_q{};      // bf16 queries [q_pad, d], box {64, 128}, SW128
-  CUtensorMap tmap_qs[4]{};  // bf16 queries [q_pad, d], box {64, 16/32/64/128}, SW128 (small-batch kernel)
+  CUtensorMap tmap_qs[8]{};  // bf16 queries [q_pad, d], box {64, 16 (i + 1)}, SW128 (small-batch kernel)
   int32_t kernel_policy = 0; // bit 0: never the small-batch kernel; bit 1: no 4-CTA multicast clusters
 
   void* nccl_comm = nullptr;  // ncclComm_t

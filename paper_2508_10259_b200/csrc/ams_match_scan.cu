@@ -542,8 +542,10 @@ __global__ void __launch_bounds__(kScanThreads, 1)
 }
 
 // Query-tile box (TMA rows) for a batch: the smallest encoded box >= NQ.
-int scan_box(int NQ) { return NQ <= 32 ? 32 : NQ <= 64 ? 64 : 128; }
-int box_index(int box) { return box == 16 ? 0 : box == 32 ? 1 : box == 64 ? 2 : 3; }
+// Query-tile box (TMA rows) = exactly the B rows a CTA's MMA reads (N for one CTA, N/2 on
+// a CTA pair; a multiple of 16 <= 128): no query rows are staged that the MMA skips.
+int scan_box(int rows) { return rows; }
+int box_index(int box) { return box / 16 - 1; }
 
 template <int KT, int JP, bool G, int CG>
 cudaError_t launch_scan_t(Pool& p, const ScanParams& prm, int box, int grid, cudaStream_t s) {
