@@ -167,3 +167,21 @@ def test_scan_kernel_gate_boundary_and_appends(ams):
             orc = oracle.match(emb, joints, q, qj, k, 0.0, gamma)
             g, plan = run(ams, pool, q, qj, k, 0.0, gamma)
             check_bf16(*g, orc, 0.0)
+
+
+@pytest.mark.parametrize("nq", [1, 7, 63, 64, 65, 255, 256])
+def test_survey_batch_and_k_grid(ams, nq):
+    """SURVEY.md 4, tier 2: k in {1, 5, 16, 32} x nq in {1, 7, 63, 64, 65, 255, 256} on a
+    pool that is not a multiple of the tile, gated and ungated, against the oracle --
+    whichever kernel the plan picks (small-batch on one CTA or a CTA pair, or the
+    128/256-query-tile kernel)."""
+    cfg = ams_gen.small_variant("c2", 3001, nq)
+    w = ams_gen.generate_host(cfg)
+    with ams.Pool(cfg.d, cfg.J, cfg.M, 256, 32) as pool:
+        pool.append(dev_t(w.emb), dev_t(w.joints))
+        for k in (1, 5, 16, 32):
+            for gamma in (cfg.gamma, INF):
+                orc = oracle.match(w.emb, w.joints, w.q_emb, w.q_joints, k, cfg.theta, gamma)
+                g, plan = run(ams, pool, w.q_emb, w.q_joints, k, cfg.theta, gamma)
+                assert plan["kernel_id"] == (4 if scan_eligible(nq, k) else 1 if nq <= 128 else 2)
+                check_bf16(*g, orc, cfg.theta)
