@@ -122,8 +122,8 @@ __global__ void __launch_bounds__(kScanThreads, 1)
                       const ScanParams prm) {
   // CG = 2 keeps the lists in global memory (L2-resident, private to each warp, touched
   // only on inserts): in registers 8 slots (112 registers) made ptxas serialise the gate
-  // filter's loads and spill; in shared memory they cost pipeline stages, and the
-  // HBM stream needs the stages (C5: 3 stages 7.4 ms vs 6.3 ms per 129-256-query call)
+  // filter's loads and spill; in shared memory they cost pipeline stages (C5: 3 stages,
+  // 7.4 ms vs 6.3 ms per 129-256-query call)
   constexpr bool SMEM_LISTS = CG == 2;   // (name kept: the lists are out of registers)
   constexpr int AROWS = kBlockN / CG;              // tile rows this CTA owns (aux ring)
   constexpr uint32_t AUXJ = AROWS * JP * 4;
