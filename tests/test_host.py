@@ -70,6 +70,10 @@ def test_null_pool_calls_are_invalid_argument(ams):
     assert ams.lib.ams_pool_append(None, None, None, 0, None, None) == 1
     assert ams.lib.ams_pool_destroy(None) == 0
     assert ams.lib.ams_get_nccl_unique_id(None) == 1
+    assert ams.lib.ams_pool_set_kernel_policy(None, 0) == 1
+    assert ams.lib.ams_pool_set_profiling(None, 1) == 1
+    assert ams.lib.ams_pool_last_plan(None, None, None, None, None) == 1
+    assert ams.lib.ams_match_gate_first(None, None, None, 1, 1, 0.5, 0.3, None, None, None, None) == 1
 
 
 @pytest.mark.parametrize("cap,world,block", [(100, 1, 0), (100, 3, 0), (1000, 8, 0), (1000, 8, 7),
