@@ -153,11 +153,11 @@ void plan_tc(const Pool& p, int nq, int KT, int& S, int& grid, int& cg, int& cl)
 
 // Plan of the small-batch kernel: one query tile, so units are row splits only; same
 // cost model as plan_tc (busiest CTA's tile count, ties -> fewer splits).
-void plan_scan(const Pool& p, int nq, int KT, int& S, int& grid) {
+void plan_scan(const Pool& p, int nq, int KT, bool gated, int& S, int& grid) {
   const int64_t n_pt = (p.local + ams::kBlockN - 1) / ams::kBlockN;
   const int cg = ams::scan_cg(nq);
   const int ctas = std::min(p.num_sms / cg, cg == 2 ? std::max(1, p.max_clusters2) : p.num_sms);   // tiles in flight
-  const int64_t per_split = (int64_t)nq * ams::scan_lists_per_split(nq) * KT;
+  const int64_t per_split = (int64_t)nq * ams::scan_lists_per_split(nq, KT, gated) * KT;
   int64_t s_cap = std::max<int64_t>(1, p.part_cap / per_split);
   s_cap = std::min<int64_t>({s_cap, std::max<int64_t>(1, n_pt), (int64_t)8 * ctas});
   int64_t best_cost = LLONG_MAX;
@@ -501,7 +501,7 @@ static ams_status_t match_impl(ams_pool_t pool, const void* q_emb, const float* 
   // The small-batch kernel (pool rows on the MMA M side) needs no query order.
   const bool use_scan = !gate_first && p.cfg.dtype == AMS_DTYPE_BF16 && p.local > 0 && (p.kernel_policy & 1) == 0 &&
                         ams::scan_stages(p, nq, a.KT) > 0 &&
-                        (int64_t)nq * ams::scan_lists_per_split(nq) * a.KT <= p.part_cap;   // >= 1 split fits
+                        (int64_t)nq * ams::scan_lists_per_split(nq, a.KT, a.gated != 0) * a.KT <= p.part_cap;   // >= 1 split fits
   const bool sorted = p.cfg.dtype == AMS_DTYPE_BF16 && a.gated && p.local > 0 && nq >= kSortMinQueries && !use_scan;
   if (sorted) AMS_CUDA_TRY(ams::launch_query_order(p, qj_src, nq, s));
   AMS_CUDA_TRY(ams::launch_query_prep(p, q_src, qj_src, nq, sorted ? p.q_perm : nullptr, s));
@@ -551,8 +551,8 @@ static ams_status_t match_impl(ams_pool_t pool, const void* q_emb, const float* 
       p.last_kernel = 0;
     } else if (use_scan) {
       int S, grid;
-      plan_scan(p, nq, a.KT, S, grid);
-      P = S * ams::scan_lists_per_split(nq);
+      plan_scan(p, nq, a.KT, a.gated != 0, S, grid);
+      P = S * ams::scan_lists_per_split(nq, a.KT, a.gated != 0);
       a.slots = (!a.gated && P >= a.k) ? 1 : 0;   // union-bound slots (launch_match_scan)
       if (e0) AMS_CUDA_TRY(cudaEventRecord(e0, s));
       AMS_CUDA_TRY(ams::launch_match_scan(p, a, S, grid, s));

@@ -193,7 +193,7 @@ int tc_max_active_clusters(int cl);   // co-resident clusters of cl CTAs (CTA-pa
 // above 128 queries, or the per-lane register lists would not fit)
 int scan_stages(const Pool& p, int nq, int KT);
 int scan_cg(int nq);                 // CTAs per tile: 1 (nq <= 128) or 2 (CTA pair)
-int scan_lists_per_split(int nq);    // partial lists per row split
+int scan_lists_per_split(int nq, int KT, bool gated);   // partial lists per row split (1: warps merged in the CTA)
 cudaError_t launch_match_scan(Pool& p, const MatchArgs& a, int32_t splits, int32_t grid, cudaStream_t s);
 // merge [nq][P][KT] local lists -> [nq][k] (fp32, global int64); writes hit if out_hit != null
 // tc_bounds: the lists come from launch_match_tc, whose per-query lower bounds (p.bound,

@@ -507,12 +507,50 @@ __global__ void __launch_bounds__(kScanThreads, 1)
         }
         __syncwarp();
       }
-      // this unit's lists -> partials [nq][P][KT] (list index = split * warps + warp)
+      // One CTA, KT <= 16, gated: the 4 warps' (mostly empty) lists of a query are merged
+      // here (warps 1-3 publish theirs through their transpose buffers, warp 0 inserts
+      // them into its own), so the split leaves one list per query instead of four for
+      // merge_partials (64-query C3 scan: 0.345 -> 0.339 ms per call).  Ungated lists are
+      // full, and warp 0's serial inserts cost more in the kernel (+50 us) than the merge
+      // kernel saves, so ungated calls keep four lists per split.
+      constexpr bool MERGE4 = GATED && CG == 1 && KT <= 16 && 2 * KT * 32 <= 32 * kTPad;
+      if constexpr (MERGE4) {
+#pragma unroll
+        for (int sl = 0; sl < NSL; ++sl) {
+          if (sl >= nsl) break;
+          float* ts = tr;                                       // [KT][32] scores
+          int32_t* ti = reinterpret_cast<int32_t*>(tr + KT * 32);   // [KT][32] rows
+          if (lg != 0) {
+#pragma unroll
+            for (int rr = 0; rr < KT; ++rr) {
+              ts[rr * 32 + lane] = top[SMEM_LISTS ? 0 : sl].s[rr];
+              ti[rr * 32 + lane] = top[SMEM_LISTS ? 0 : sl].i[rr];
+            }
+          }
+          ptx::named_bar_sync(2, 32 * kScanEpiWarps);
+          if (lg == 0) {
+            TopK<KT, int32_t>& tp = top[SMEM_LISTS ? 0 : sl];
+            for (int w = 1; w < kScanEpiWarps; ++w) {
+              const float* ws = trs + w * 32 * kTPad;
+              const int32_t* wi = reinterpret_cast<const int32_t*>(ws + KT * 32);
+              for (int rr = 0; rr < KT; ++rr) {   // sorted lists: stop at the first entry that cannot enter
+                const int32_t j = wi[rr * 32 + lane];
+                const float v = ws[rr * 32 + lane];
+                if (j < 0 || !better(v, j, tp.kth_s, tp.kth_i)) break;
+                tp.insert(v, j, KT);
+              }
+            }
+          }
+          ptx::named_bar_sync(2, 32 * kScanEpiWarps);   // transpose buffers free again
+        }
+      }
+      // this unit's lists -> partials [nq][P][KT] (list index = split * lists + list)
 #pragma unroll
       for (int sl = 0; sl < NSL; ++sl) {
         const int c = sl * 32 + lane;
-        if (sl < nsl && c < nq) {
-          const int64_t base = ((int64_t)c * prm.P + ((int64_t)u * CG + crank) * kScanEpiWarps + lg) * KT;
+        if (sl < nsl && c < nq && (!MERGE4 || lg == 0)) {
+          const int64_t base = MERGE4 ? ((int64_t)c * prm.P + u) * KT
+                                      : ((int64_t)c * prm.P + ((int64_t)u * CG + crank) * kScanEpiWarps + lg) * KT;
           if constexpr (SMEM_LISTS) {
 #pragma unroll
             for (int rr = 0; rr < KT; ++rr) {
@@ -625,7 +663,7 @@ cudaError_t launch_match_scan(Pool& p, const MatchArgs& a, int32_t S, int32_t gr
   prm.d = p.cfg.dim;
   prm.n_pt = (int32_t)((p.local + kBlockN - 1) / kBlockN);
   prm.S = S;
-  prm.P = S * kScanEpiWarps * cg;
+  prm.P = S * scan_lists_per_split(a.nq, a.KT, a.gated != 0);
   prm.stages = scan_stages(p, a.nq, a.KT);
   prm.b_bytes = (uint32_t)box * kBlockK * 2;
   prm.idesc = ptx::idesc_bf16_f32(kBlockM * cg, (uint32_t)NQ);
@@ -647,6 +685,8 @@ cudaError_t launch_match_scan(Pool& p, const MatchArgs& a, int32_t S, int32_t gr
   return e;
 }
 
-int scan_lists_per_split(int nq) { return kScanEpiWarps * scan_cg(nq); }
+int scan_lists_per_split(int nq, int KT, bool gated) {
+  return gated && scan_cg(nq) == 1 && KT <= 16 ? 1 : kScanEpiWarps * scan_cg(nq);
+}
 
 }  // namespace ams

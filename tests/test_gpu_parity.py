@@ -191,6 +191,10 @@ def test_plan_uses_cta_pairs_and_splits(ams):
         pool.match(to_dev(w.q_emb[:64]), to_dev(w.q_joints[:64]), cfg.k, cfg.theta, INF)
         plan = ams.ams_pool_last_plan(pool.handle)
         assert plan["kernel_id"] == 4 and plan["splits"] > 1 and plan["partials"] == 4 * plan["splits"]
+        pool.match(to_dev(w.q_emb[:64]), to_dev(w.q_joints[:64]), cfg.k, cfg.theta, cfg.gamma)
+        plan = ams.ams_pool_last_plan(pool.handle)
+        # gated, one CTA per tile, KT <= 16: the 4 epilogue warps' lists are merged in the CTA
+        assert plan["kernel_id"] == 4 and plan["splits"] > 1 and plan["partials"] == plan["splits"]
         ams.ams_pool_set_kernel_policy(pool.handle, 1)
         pool.match(to_dev(w.q_emb[:64]), to_dev(w.q_joints[:64]), cfg.k, cfg.theta, INF)
         plan = ams.ams_pool_last_plan(pool.handle)
