@@ -102,6 +102,12 @@ def test_p1_exhaustive_exact(dtype, gamma):
                 exp_hit = int(len(exp) > 0 and exp[0][0] >= Fraction(theta))
                 assert int(res.hit[i]) == exp_hit
                 assert res.nelig[i] == len(exp)
+                # (k+1)-th ranking key, used by the r = k gap rule (tests/parity.py):
+                # the exact (k+1)-th enumerated score, -inf when n_elig <= k
+                exp_next = float(exp[k][0]) if len(exp) > k else -INF
+                assert res.next[i] == exp_next, (i, k, gamma)
+                # and the full ranked keys (fp64 ranking key of each valid slot)
+                assert res.key[i].tolist() == exp_s
 
 
 # ----------------------------------------------------------------------------
@@ -222,9 +228,21 @@ def test_p4_textbook_knn(seed):
     S = (Qm / np.linalg.norm(Qm, axis=1, keepdims=True)) @ (E / np.linalg.norm(E, axis=1, keepdims=True)).T
     res = oracle.match(eb, np.zeros((M, 3), np.float32), qb, np.zeros((nq, 3), np.float32), k, 0.0, INF)
     for i in range(nq):
-        order = np.lexsort((np.arange(M), -S[i]))[:k]
+        full = np.lexsort((np.arange(M), -S[i]))
+        order = full[:k]
         assert np.allclose(res.key[i], S[i, order], rtol=0, atol=1e-12)
         assert res.idx[i].tolist() == order.tolist()
+        # the (k+1)-th key is the lexsorted (k+1)-th score (not the k-th)
+        assert abs(res.next[i] - S[i, full[k]]) <= 1e-12
+        assert res.next[i] <= res.key[i, k - 1]
+    # fewer eligible rows than k + 1: next is -inf
+    small = oracle.match(eb[:k], np.zeros((k, 3), np.float32), qb, np.zeros((nq, 3), np.float32), k, 0.0, INF)
+    assert np.all(np.isneginf(small.next))
+    one_more = oracle.match(eb[:k + 1], np.zeros((k + 1, 3), np.float32), qb, np.zeros((nq, 3), np.float32),
+                            k, 0.0, INF)
+    S1 = S[:, :k + 1]
+    for i in range(nq):
+        assert abs(one_more.next[i] - S1[i].min()) <= 1e-12
 
 
 # ----------------------------------------------------------------------------
