@@ -37,6 +37,12 @@
  *   - After AMS_ERR_CUDA / AMS_ERR_NCCL the pool is unusable and must be destroyed.
  *   - Multi-GPU (world > 1): one process per GPU; create / append / match / destroy are
  *     collective (every rank calls them in the same order with identical arguments).
+ *   - CUDA graphs: ams_match / ams_match_gate_first with DEVICE inputs on a pool without
+ *     the peer exchange are stream-ordered with no host synchronisation and may be
+ *     captured; the plan (kernel, splits) is frozen at capture, so re-capture after
+ *     appends.  During capture, host-resident inputs (a pageable copy) and peer-exchange
+ *     pools (a host epoch counter) return AMS_ERR_UNSUPPORTED and the pool stays usable;
+ *     the same holds for ams_pool_append with host-resident rows.
  */
 #ifndef AMS_H_
 #define AMS_H_
@@ -47,7 +53,7 @@
 extern "C" {
 #endif
 
-#define AMS_ABI_VERSION 1
+#define AMS_ABI_VERSION 2
 
 typedef struct ams_pool_s* ams_pool_t; /* opaque, library-owned */
 
@@ -171,7 +177,12 @@ ams_status_t ams_merge_topk(const float* in_score, const int64_t* in_index, int3
  * to the NCCL path.  Collective: every rank calls it once after ams_pool_create (the
  * three IPC handles per rank travel over the pool's NCCL communicator).  Requires all
  * ranks on one node with peer access; the pool's matches must be issued by every rank in
- * the same order (as with the NCCL path).  Errors: AMS_ERR_INVALID_ARGUMENT (null pool),
+ * the same order (as with the NCCL path).  The final merge waits for each peer's flag to
+ * reach the call's epoch for at most 10 s (device globaltimer); on timeout it writes
+ * padding (-1, -inf, miss), records the failure in a host-mapped error word, and the
+ * pool's next call (or ams_pool_status) returns AMS_ERR_NCCL -- a dead or desynchronised
+ * peer cannot hang the GPU.  Not capturable in a CUDA graph (the epoch is a host counter;
+ * ams_match returns AMS_ERR_UNSUPPORTED during capture).  Errors: AMS_ERR_INVALID_ARGUMENT (null pool),
  * AMS_ERR_UNSUPPORTED (pool without a communicator -- world == 1 and no nccl_id --,
  * world > 8, capacity >= 2^31, IPC unavailable),
  * AMS_ERR_OUT_OF_MEMORY, AMS_ERR_NCCL, AMS_ERR_CUDA.  Idempotent. */
@@ -183,14 +194,28 @@ ams_status_t ams_pool_enable_peer_exchange(ams_pool_t pool);
  * [rounds][G][nq][k] ranked lists (score desc, index asc; -inf / -1 padding; ids < 2^31);
  * out_score/out_index: DEVICE [rounds][G][nq][k]; out_hit [rounds][G][nq] -- virtual rank
  * g's merged result of round r, which must equal ams_merge_topk of that round's G lists
- * for every g.  All producer launches of a round are enqueued before its consumer
- * launches on `stream`, so no kernel waits on a concurrently running kernel.  Allocates
- * and frees its own buffers; synchronises `stream`.  Errors: AMS_ERR_INVALID_ARGUMENT
- * (G, nq, k (1..64) or rounds out of range, null pointers), AMS_ERR_OUT_OF_MEMORY,
- * AMS_ERR_CUDA. */
+ * for every g.  Every consumer launch is enqueued on `stream` after the producer launches
+ * it waits for, so no kernel waits on a concurrently running kernel.  flags:
+ *   AMS_SELFTEST_LATE_CONSUMER  virtual rank G-1 consumes round r-1 only after the other
+ *                               ranks produced round r (their flags are ahead of the epoch
+ *                               it waits for; G >= 2); results must be unchanged;
+ *   AMS_SELFTEST_DROP_LAST      virtual rank G-1 never produces the last round: the other
+ *                               ranks' waits time out after 20 ms, their outputs of that
+ *                               round are padding, and the call returns AMS_ERR_NCCL.
+ * Allocates and frees its own buffers; synchronises `stream`.  Errors:
+ * AMS_ERR_INVALID_ARGUMENT (G, nq, k (1..64), rounds or flags out of range, null
+ * pointers), AMS_ERR_OUT_OF_MEMORY, AMS_ERR_CUDA, AMS_ERR_NCCL (a wait timed out). */
+#define AMS_SELFTEST_LATE_CONSUMER 1
+#define AMS_SELFTEST_DROP_LAST 2
 ams_status_t ams_exchange_selftest(int32_t G, int32_t nq, int32_t k, int32_t rounds, float threshold,
                                    const float* in_score, const int64_t* in_index, float* out_score,
-                                   int64_t* out_index, uint8_t* out_hit, void* stream);
+                                   int64_t* out_index, uint8_t* out_hit, int32_t flags, void* stream);
+
+/* Sticky status of a pool without synchronising: AMS_ERR_NCCL once a peer-exchange wait
+ * timed out (visible as soon as the timed-out kernel wrote it; synchronise the stream
+ * first for a definite answer), AMS_ERR_CUDA after an earlier CUDA failure, else AMS_OK.
+ * Errors: AMS_ERR_INVALID_ARGUMENT (null pool). */
+ams_status_t ams_pool_status(ams_pool_t pool);
 
 /* ---- two-phase action hash (Algorithm 1) ----
  * Phase 1 hashes every s-byte segment of every input independently, phase 2 folds an

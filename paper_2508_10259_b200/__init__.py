@@ -17,8 +17,9 @@ import os
 from typing import Optional
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("AMS_LIBRARY") or os.path.join(_HERE, "libams.so")  # override: diagnostics only
+LIB_PATH = os.path.join(_HERE, "libams.so")
 
+ABI_VERSION = 2   # include/ams.h AMS_ABI_VERSION this binding marshals for
 AMS_OK = 0
 AMS_DTYPE_BF16 = 0
 AMS_DTYPE_FP32 = 1
@@ -28,7 +29,7 @@ STATUS = {0: "AMS_OK", 1: "AMS_ERR_INVALID_ARGUMENT", 2: "AMS_ERR_CAPACITY", 3: 
 # Every symbol include/ams.h declares (tests check the library exports all of them).
 EXPORTS = ("ams_get_nccl_unique_id", "ams_pool_create", "ams_pool_append", "ams_match", "ams_match_gate_first",
            "ams_merge_topk", "ams_pool_enable_peer_exchange", "ams_exchange_selftest",
-           "ams_pool_size",
+           "ams_pool_status", "ams_pool_size",
            "ams_pool_destroy", "ams_status_string", "ams_pool_set_profiling", "ams_pool_read_profile",
            "ams_pool_launch_count", "ams_pool_last_plan", "ams_pool_set_kernel_policy", "ams_shard_locate", "ams_shard_capacity",
            "ams_abi_version", "ams_hasher_create", "ams_hash_actions", "ams_hasher_destroy",
@@ -65,7 +66,8 @@ def _load():
         "ams_match_gate_first": [V, V, V, I32, I32, ctypes.c_float, ctypes.c_float, V, V, V, V],
         "ams_merge_topk": [V, V, I32, I32, I32, I32, ctypes.c_float, V, V, V, V],
         "ams_pool_enable_peer_exchange": [V],
-        "ams_exchange_selftest": [I32, I32, I32, I32, ctypes.c_float, V, V, V, V, V, V],
+        "ams_exchange_selftest": [I32, I32, I32, I32, ctypes.c_float, V, V, V, V, V, I32, V],
+        "ams_pool_status": [V],
         "ams_pool_size": [V, ctypes.POINTER(I64)],
         "ams_pool_destroy": [V],
         "ams_pool_set_profiling": [V, I32],
@@ -108,6 +110,8 @@ def _load():
 
 
 lib = _load()
+if lib.ams_abi_version() != ABI_VERSION:
+    raise ImportError(f"{LIB_PATH} has ABI {lib.ams_abi_version()}, this binding needs {ABI_VERSION}: rebuild it")
 
 
 def _check(st: int, what: str):
@@ -204,10 +208,20 @@ def ams_pool_enable_peer_exchange(pool: int) -> None:
     _check(lib.ams_pool_enable_peer_exchange(pool), "ams_pool_enable_peer_exchange")
 
 
+AMS_SELFTEST_LATE_CONSUMER = 1
+AMS_SELFTEST_DROP_LAST = 2
+
+
 def ams_exchange_selftest(G: int, nq: int, k: int, rounds: int, threshold: float, in_score, in_index, out_score,
-                          out_index, out_hit, stream=None) -> None:
+                          out_index, out_hit, flags: int = 0, stream=None) -> None:
     _check(lib.ams_exchange_selftest(G, nq, k, rounds, threshold, _ptr(in_score), _ptr(in_index), _ptr(out_score),
-                                     _ptr(out_index), _ptr(out_hit), _stream(stream)), "ams_exchange_selftest")
+                                     _ptr(out_index), _ptr(out_hit), int(flags), _stream(stream)),
+           "ams_exchange_selftest")
+
+
+def ams_pool_status(pool: int) -> int:
+    """Sticky status without a sync (AMS_ERR_NCCL after a peer-exchange timeout); returns the code."""
+    return int(lib.ams_pool_status(pool))
 
 
 def ams_pool_size(pool: int) -> int:

@@ -13,7 +13,6 @@ from __future__ import annotations
 import concurrent.futures as cf
 import glob
 import os
-import re
 import subprocess
 import sys
 import sysconfig
@@ -22,8 +21,6 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libams.so")
-# diagnostic variant (never loaded by the product path unless AMS_LIBRARY points at it)
-DIAG = os.environ.get("AMS_BUILD_DIAG")
 BUILD = os.path.join(ROOT, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -52,11 +49,6 @@ def _stale(out, deps):
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    global OUT, BUILD
-    if DIAG:
-        tag = re.sub(r"[^A-Za-z0-9]+", "_", DIAG).strip("_").lower()
-        OUT = os.path.join(ROOT, "diag_lib", f"libams_diag_{tag}.so")  # travels with gpurun (build/ does not)
-        BUILD = os.path.join(ROOT, "build", "diag_" + tag)
     os.makedirs(BUILD, exist_ok=True)
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
     inc, lib = nccl_dirs()
@@ -66,8 +58,6 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return OUT
     common = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
               "-I", os.path.join(ROOT, "include"), "-I", inc, "-Xptxas", "-v"]
-    if DIAG:
-        common += [f"-D{DIAG}"]
 
     def compile_one(src):
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")

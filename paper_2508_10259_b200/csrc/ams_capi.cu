@@ -44,9 +44,36 @@ namespace {
   } while (0)
 
 inline ams_status_t fail(ams_pool_s* pool, ams_status_t st) {
-  if (pool != nullptr && (st == AMS_ERR_CUDA || st == AMS_ERR_NCCL)) pool->p.broken = true;
+  if (pool != nullptr && (st == AMS_ERR_CUDA || st == AMS_ERR_NCCL) && !pool->p.broken) {
+    pool->p.broken = true;
+    pool->p.broken_st = st;
+  }
   return st;
 }
+
+// Sticky pool status: an earlier failure, or a peer-exchange wait that timed out (the
+// consumer kernel sets the host-mapped error word; no synchronisation needed to read it).
+inline ams_status_t pool_status(ams_pool_s* pool) {
+  ams::Pool& p = pool->p;
+  if (!p.broken && p.x_err_host != nullptr && *static_cast<volatile unsigned int*>(p.x_err_host) != 0)
+    fail(pool, AMS_ERR_NCCL);
+  return p.broken ? p.broken_st : AMS_OK;
+}
+
+// Is `s` being captured into a CUDA graph?  (Capture forbids the pageable host copies and
+// the host epoch counter of the peer exchange.)
+inline bool capturing(cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cs) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return cs != cudaStreamCaptureStatusNone;
+}
+
+// Host-append staging is allocated on the first host-sourced append, with a fixed byte
+// budget (not sized by the pool: device-sourced appends never need it).
+constexpr size_t kStageBytes = (size_t)64 << 20;
 
 typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                        const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
@@ -139,15 +166,6 @@ void plan_tc(const Pool& p, int nq, int KT, int& S, int& grid, int& cg, int& cl)
     }
   }
   S = best;
-#ifdef AMS_DIAG_SPLITS_ENV   // diagnostic builds only: AMS_DIAG_SPLITS=<S> forces the split count
-  if (const char* e = getenv("AMS_DIAG_SPLITS"))
-    S = (int)std::min<int64_t>({(int64_t)atoi(e), std::max<int64_t>(1, n_pt),
-                                std::max<int64_t>(1, p.part_cap / (nq_pad * ams::kEpiHalves * KT))});
-#endif
-#ifdef AMS_DIAG_SPLIT_MULT   // diagnostic builds only: shorter units (L2-reuse experiments)
-  S = (int)std::min<int64_t>({(int64_t)best * AMS_DIAG_SPLIT_MULT, std::max<int64_t>(1, n_pt),
-                              std::max<int64_t>(1, p.part_cap / (nq_pad * ams::kEpiHalves * KT))});
-#endif
   grid = (int)std::min<int64_t>((int64_t)n_qg * S, clusters) * cl;
 }
 
@@ -189,18 +207,26 @@ void free_peers(Pool& p) {
         if (p.peers.i[g]) cudaIpcCloseMemHandle(p.peers.i[g]);
         if (p.peers.flag[g]) cudaIpcCloseMemHandle(p.peers.flag[g]);
       }
-  void* own[] = {p.x_s, p.x_i, p.x_flag, p.x_done};
+  void* own[] = {p.x_s, p.x_i, p.x_flag, p.x_done, p.x_barrier};
   for (void* q : own)
     if (q) cudaFree(q);
+  // the error word outlives the peer mode only if it fired (pool_status keeps reporting it)
+  if (p.x_err_host && *static_cast<volatile unsigned int*>(p.x_err_host) == 0) {
+    cudaFreeHost(p.x_err_host);
+    p.x_err_host = nullptr;
+  }
   p.peer_mode = false;
   p.x_s = nullptr;
   p.x_i = nullptr;
   p.x_flag = nullptr;
   p.x_done = nullptr;
+  p.x_barrier = nullptr;
 }
 
 void free_all(Pool& p) {
   free_peers(p);
+  if (p.x_err_host) cudaFreeHost(p.x_err_host);
+  p.x_err_host = nullptr;
   for (int b = 0; b < 2; ++b) {
     if (p.staged[b]) cudaEventDestroy(p.staged[b]);
     if (p.consumed[b]) cudaEventDestroy(p.consumed[b]);
@@ -340,7 +366,8 @@ ams_status_t ams_pool_create(const ams_pool_config_t* cfg, ams_pool_t* out) {
            ams::kSimtThreads * p.KT_max;
   }
   p.part_cap = part;
-  p.stage_rows = std::min<int64_t>(std::max<int64_t>(c.capacity, 1), 65536);
+  p.stage_rows = std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(c.capacity, 1),
+                                                        (int64_t)(kStageBytes / ((size_t)d * es + 4 * c.joint_dim))));
   bool ok = alloc(&p.emb, (size_t)p.cap_pad * d * es) && alloc((void**)&p.inv_norm, (size_t)p.cap_pad * 4) &&
             alloc((void**)&p.joints, (size_t)p.cap_pad * p.JP * 4) &&
             alloc(&p.q_stage, (size_t)p.q_pad * d * es) && alloc((void**)&p.q_inv, (size_t)p.q_pad * 4) &&
@@ -353,9 +380,7 @@ ams_status_t ams_pool_create(const ams_pool_config_t* cfg, ams_pool_t* out) {
             alloc((void**)&p.slots, (size_t)p.q_pad * p.KT_max * 4) &&
             alloc((void**)&p.part_s, (size_t)part * 4) && alloc((void**)&p.part_i, (size_t)part * 4) &&
             alloc((void**)&p.shard_s, (size_t)c.max_queries * c.max_k * 4) &&
-            alloc((void**)&p.shard_i, (size_t)c.max_queries * c.max_k * 8) &&
-            alloc(&p.stage_emb, (size_t)p.stage_rows * d * es) &&
-            alloc((void**)&p.stage_joints, (size_t)p.stage_rows * c.joint_dim * 4);
+            alloc((void**)&p.shard_i, (size_t)c.max_queries * c.max_k * 8);
   if (ok && c.dtype == AMS_DTYPE_BF16) {
     const size_t gl = (size_t)p.num_sms * 4 * 8 * 8 * 32;   // see Pool::scan_glist_s
     ok = alloc((void**)&p.scan_glist_s, gl * 4) && alloc((void**)&p.scan_glist_i, gl * 4);
@@ -414,16 +439,36 @@ ams_status_t ams_pool_append(ams_pool_t pool, const void* emb, const float* join
   NvtxRange nvtx("ams_pool_append");
   if (pool == nullptr || n < 0) return AMS_ERR_INVALID_ARGUMENT;
   Pool& p = pool->p;
-  if (p.broken) return AMS_ERR_CUDA;
+  if (pool_status(pool) != AMS_OK) return p.broken_st;
   if (n > 0 && (emb == nullptr || joints == nullptr)) return AMS_ERR_INVALID_ARGUMENT;
   if (n > p.cfg.capacity - p.size) return AMS_ERR_CAPACITY;
-  if (first_index) *first_index = p.size;
-  if (n == 0) return AMS_OK;
+  if (n == 0) {
+    if (first_index) *first_index = p.size;
+    return AMS_OK;
+  }
   AMS_CUDA_TRY(cudaSetDevice(p.cfg.device));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const size_t es = esize(p);
   const size_t row_bytes = (size_t)p.cfg.dim * es;
   const bool dev_e = is_device_ptr(emb), dev_j = is_device_ptr(joints);
+  if ((!dev_e || !dev_j) && capturing(s)) return AMS_ERR_UNSUPPORTED;   // pageable copies cannot be captured
+  if ((!dev_e && p.stage_emb == nullptr) || (!dev_j && p.stage_joints == nullptr)) {
+    // first host-sourced append: allocate the staging buffers (stream-ordered frees are
+    // not needed: they live as long as the pool)
+    AMS_CUDA_TRY(cudaStreamSynchronize(s));
+    if (p.stage_emb == nullptr && cudaMalloc(&p.stage_emb, (size_t)p.stage_rows * row_bytes) != cudaSuccess) {
+      cudaGetLastError();
+      p.stage_emb = nullptr;
+      return AMS_ERR_OUT_OF_MEMORY;
+    }
+    if (p.stage_joints == nullptr &&
+        cudaMalloc((void**)&p.stage_joints, (size_t)p.stage_rows * p.cfg.joint_dim * 4) != cudaSuccess) {
+      cudaGetLastError();
+      p.stage_joints = nullptr;
+      return AMS_ERR_OUT_OF_MEMORY;
+    }
+  }
+  if (first_index) *first_index = p.size;
   for (int64_t off = 0; off < n;) {
     const int64_t m = (dev_e && dev_j) ? n - off : std::min<int64_t>(n - off, p.stage_rows);
     const void* e_src = static_cast<const uint8_t*>(emb) + off * row_bytes;
@@ -450,7 +495,7 @@ static ams_status_t match_impl(ams_pool_t pool, const void* q_emb, const float* 
   NvtxRange nvtx(gate_first ? "ams_match_gate_first" : "ams_match");
   if (pool == nullptr) return AMS_ERR_INVALID_ARGUMENT;
   Pool& p = pool->p;
-  if (p.broken) return AMS_ERR_CUDA;
+  if (pool_status(pool) != AMS_OK) return p.broken_st;
   if (q_emb == nullptr || q_joints == nullptr || out_index == nullptr || out_score == nullptr ||
       out_hit == nullptr)
     return AMS_ERR_INVALID_ARGUMENT;
@@ -478,6 +523,8 @@ static ams_status_t match_impl(ams_pool_t pool, const void* q_emb, const float* 
   const void* q_src = q_emb;
   const float* qj_src = q_joints;
   const bool host_q = !is_device_ptr(q_emb), host_j = !is_device_ptr(q_joints);
+  if ((host_q || host_j || (p.collective && p.peer_mode)) && capturing(s))
+    return AMS_ERR_UNSUPPORTED;   // pageable copies / the host epoch counter cannot be captured
   int b = -1;
   if (host_q || host_j) {
     b = p.stage_buf;
@@ -654,7 +701,7 @@ ams_status_t ams_merge_topk(const float* in_score, const int64_t* in_index, int3
 ams_status_t ams_pool_enable_peer_exchange(ams_pool_t pool) {
   if (pool == nullptr) return AMS_ERR_INVALID_ARGUMENT;
   Pool& p = pool->p;
-  if (p.broken) return AMS_ERR_CUDA;
+  if (pool_status(pool) != AMS_OK) return p.broken_st;
   const int G = p.cfg.world, r = p.cfg.rank;
   if (G < 1 || G > ams::kMaxPeers || p.nccl_comm == nullptr) return AMS_ERR_UNSUPPORTED;
   if (p.peer_mode) return AMS_OK;
@@ -662,14 +709,21 @@ ams_status_t ams_pool_enable_peer_exchange(ams_pool_t pool) {
   AMS_CUDA_TRY(cudaSetDevice(p.cfg.device));
   const size_t slot = (size_t)2 * G * p.cfg.max_queries * p.cfg.max_k;
   bool ok = cudaMalloc((void**)&p.x_s, slot * 4) == cudaSuccess && cudaMalloc((void**)&p.x_i, slot * 8) == cudaSuccess &&
-            cudaMalloc((void**)&p.x_flag, G * 8) == cudaSuccess && cudaMalloc((void**)&p.x_done, 16) == cudaSuccess;
+            cudaMalloc((void**)&p.x_flag, G * 8) == cudaSuccess && cudaMalloc((void**)&p.x_done, 4) == cudaSuccess &&
+            cudaMalloc((void**)&p.x_barrier, (size_t)G * 4) == cudaSuccess;
+  if (ok && p.x_err_host == nullptr)
+    ok = cudaHostAlloc((void**)&p.x_err_host, sizeof(unsigned int), cudaHostAllocMapped) == cudaSuccess;
+  unsigned int* err_dev = nullptr;
+  if (ok) ok = cudaHostGetDevicePointer((void**)&err_dev, p.x_err_host, 0) == cudaSuccess;
   if (!ok) {
     cudaGetLastError();
     free_peers(p);
     return AMS_ERR_OUT_OF_MEMORY;
   }
+  *p.x_err_host = 0;
   AMS_CUDA_TRY(cudaMemset(p.x_flag, 0, G * 8));
-  AMS_CUDA_TRY(cudaMemset(p.x_done, 0, 16));
+  AMS_CUDA_TRY(cudaMemset(p.x_done, 0, 4));
+  AMS_CUDA_TRY(cudaMemset(p.x_barrier, 0, (size_t)G * 4));
   AMS_CUDA_TRY(cudaDeviceSynchronize());
   // exchange the three IPC handles of every rank over the pool's NCCL communicator
   const size_t hb = 3 * sizeof(cudaIpcMemHandle_t);
@@ -698,6 +752,8 @@ ams_status_t ams_pool_enable_peer_exchange(ams_pool_t pool) {
   pt.rank = r;
   pt.max_q = p.cfg.max_queries;
   pt.max_k = p.cfg.max_k;
+  pt.err = err_dev;
+  pt.timeout_ns = ams::kPeerTimeoutNs;
   p.peer_mode = true;   // from here free_peers closes whatever was opened
   for (int g = 0; g < G; ++g) {
     if (g == r) {
@@ -724,10 +780,15 @@ ams_status_t ams_pool_enable_peer_exchange(ams_pool_t pool) {
   p.peers = pt;
   p.epoch = 0;
   // every rank has mapped every peer before anyone writes into a peer buffer
-  if (ncclAllGather(p.x_done + 1, p.x_done + 2, 1, ncclUint32, comm, nullptr) != ncclSuccess)
+  if (ncclAllGather(p.x_barrier + r, p.x_barrier, 1, ncclUint32, comm, nullptr) != ncclSuccess)
     return fail(pool, AMS_ERR_NCCL);
   AMS_CUDA_TRY(cudaDeviceSynchronize());
   return AMS_OK;
+}
+
+ams_status_t ams_pool_status(ams_pool_t pool) {
+  if (pool == nullptr) return AMS_ERR_INVALID_ARGUMENT;
+  return pool_status(pool);
 }
 
 ams_status_t ams_pool_size(ams_pool_t pool, int64_t* n) {

@@ -12,12 +12,19 @@
 //             last block stores `epoch` into its slot of every rank's flag array with a
 //             system-scope release.
 //   consumer  `merge_wait_kernel`: each block waits (acquire loads) until all G flags of
-//             the local array equal `epoch`, then merges the G received lists by
-//             (score desc, global index asc) into the outputs and the hit flags.
+//             the local array have reached `epoch` (>=: a faster peer may already have
+//             raised its flag for e+1), then merges the G received lists by (score desc,
+//             global index asc) into the outputs and the hit flags.  The wait is bounded
+//             (globaltimer, PeerTable::timeout_ns): on timeout the block writes padding
+//             (-1, -inf, miss), sets the pool's error word (host-mapped memory, so the
+//             host sees it without a synchronisation) and exits; the next ams_match on
+//             that pool returns AMS_ERR_NCCL.
 //
 // Receive buffers are double-buffered by epoch parity: rank g can only start producing
 // call e+2 after its consumer of call e+1 saw rank r's flag for e+1, which rank r raises
 // only after it finished consuming call e -- so slot e%2 is never overwritten while read.
+// Flags only increase, so a flag at e+1 while rank r still waits for e means peer g's
+// slot e%2 holds call e's list (g wrote e+1 into the other parity).
 // On one GPU (no peers) `ams_exchange_selftest` runs the same device code for G virtual
 // ranks: every producer launch completes before any consumer launch starts, so no kernel
 // ever waits on a concurrently running one.
@@ -44,6 +51,11 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
   unsigned long long v;
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
 
 // k rounds of the butterfly arg-max; the merged list lands in the warp's staging area
@@ -120,13 +132,32 @@ __global__ void __launch_bounds__(32 * kWarpsX)
     merge_wait_kernel(PeerTable peers, int32_t nq, int32_t k, unsigned long long epoch, float* __restrict__ out_s,
                       int64_t* __restrict__ out_i, uint8_t* __restrict__ out_hit, float threshold) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __shared__ int timed_out;
+  if (threadIdx.x == 0) timed_out = 0;
+  __syncthreads();
   if (threadIdx.x < peers.G) {
     const unsigned long long* f = peers.flag[peers.rank] + threadIdx.x;
-    while (ld_acquire_sys(f) != epoch) __nanosleep(256);
+    const unsigned long long t0 = globaltimer_ns();
+    while (ld_acquire_sys(f) < epoch) {
+      if (globaltimer_ns() - t0 > peers.timeout_ns) {
+        atomicExch(&timed_out, 1);
+        atomicOr(peers.err, 1u);   // host-mapped: visible to the host without a sync
+        break;
+      }
+      __nanosleep(256);
+    }
   }
   __syncthreads();
   const int q = blockIdx.x * kWarpsX + w;
   if (q >= nq) return;
+  if (timed_out) {   // a peer never delivered this epoch: padding, miss
+    for (int r = lane; r < k; r += 32) {
+      out_s[(int64_t)q * k + r] = -CUDART_INF_F;
+      out_i[(int64_t)q * k + r] = -1;
+    }
+    if (lane == 0) out_hit[q] = 0;
+    return;
+  }
   const int parity = (int)(epoch & 1ull);
   const float* rs = peers.s[peers.rank];
   const int64_t* ri = peers.i[peers.rank];
@@ -231,10 +262,12 @@ extern "C" {
 
 ams_status_t ams_exchange_selftest(int32_t G, int32_t nq, int32_t k, int32_t rounds, float threshold,
                                    const float* in_score, const int64_t* in_index, float* out_score,
-                                   int64_t* out_index, uint8_t* out_hit, void* stream) {
+                                   int64_t* out_index, uint8_t* out_hit, int32_t flags, void* stream) {
   using namespace ams;
   if (G < 1 || G > kMaxPeers || nq < 1 || k < 1 || k > 64 || rounds < 1 || in_score == nullptr ||
-      in_index == nullptr || out_score == nullptr || out_index == nullptr || out_hit == nullptr)
+      in_index == nullptr || out_score == nullptr || out_index == nullptr || out_hit == nullptr ||
+      (flags & ~(AMS_SELFTEST_LATE_CONSUMER | AMS_SELFTEST_DROP_LAST)) != 0 ||
+      ((flags & AMS_SELFTEST_LATE_CONSUMER) && G < 2))
     return AMS_ERR_INVALID_ARGUMENT;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int KT = pick_KT(k);
@@ -251,6 +284,16 @@ ams_status_t ams_exchange_selftest(int32_t G, int32_t nq, int32_t k, int32_t rou
   base.G = G;
   base.max_q = nq;
   base.max_k = k;
+  // the drop test must end quickly; otherwise the library's bound
+  base.timeout_ns = (flags & AMS_SELFTEST_DROP_LAST) ? 20ull * 1000 * 1000 : kPeerTimeoutNs;
+  unsigned int* err_host = nullptr;
+  if (cudaHostAlloc((void**)&err_host, sizeof(unsigned int), cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer((void**)&base.err, err_host, 0) != cudaSuccess) {
+    cudaGetLastError();
+    if (err_host) cudaFreeHost(err_host);
+    return AMS_ERR_CUDA;
+  }
+  *err_host = 0;
   std::vector<unsigned int*> done(G);
   for (int g = 0; g < G && st == AMS_OK; ++g) {
     base.s[g] = static_cast<float*>(dalloc(slot * 4));
@@ -264,32 +307,50 @@ ams_status_t ams_exchange_selftest(int32_t G, int32_t nq, int32_t k, int32_t rou
   float* ps = static_cast<float*>(dalloc((size_t)G * nq * KT * 4));
   int32_t* pi = static_cast<int32_t*>(dalloc((size_t)G * nq * KT * 4));
   if (st == AMS_OK && (!ps || !pi)) st = AMS_ERR_OUT_OF_MEMORY;
-  for (int rd = 0; rd < rounds && st == AMS_OK; ++rd) {
+  auto push = [&](int g, int rd) {
+    if (st != AMS_OK) return;
     const unsigned long long epoch = (unsigned long long)rd + 1;
-    const float* in_s = in_score + (size_t)rd * G * nq * k;
-    const int64_t* in_i = in_index + (size_t)rd * G * nq * k;
-    for (int g = 0; g < G && st == AMS_OK; ++g) {   // every virtual rank produces ...
-      if (launch_to_partials(in_s + (size_t)g * nq * k, in_i + (size_t)g * nq * k, nq, k, KT,
-                             ps + (size_t)g * nq * KT, pi + (size_t)g * nq * KT, s) != cudaSuccess)
-        st = AMS_ERR_CUDA;
-      PeerTable pt = base;
-      pt.rank = g;
-      // ids are already global (world_ids = 0: no shard map)
-      if (st == AMS_OK && launch_exchange_push(KT, ps + (size_t)g * nq * KT, pi + (size_t)g * nq * KT, nq, 1, k, pt,
-                                               epoch, done[g], 0, 0, s) != cudaSuccess)
-        st = AMS_ERR_CUDA;
-    }
-    for (int g = 0; g < G && st == AMS_OK; ++g) {   // ... before any virtual rank consumes
-      PeerTable pt = base;
-      pt.rank = g;
-      const size_t o = ((size_t)rd * G + g) * nq;
-      if (launch_exchange_wait(KT, pt, nq, k, epoch, out_score + o * k, out_index + o * k, out_hit + o, threshold,
-                               s) != cudaSuccess)
-        st = AMS_ERR_CUDA;
-    }
+    const float* in_s = in_score + ((size_t)rd * G + g) * nq * k;
+    const int64_t* in_i = in_index + ((size_t)rd * G + g) * nq * k;
+    if (launch_to_partials(in_s, in_i, nq, k, KT, ps + (size_t)g * nq * KT, pi + (size_t)g * nq * KT, s) !=
+        cudaSuccess)
+      st = AMS_ERR_CUDA;
+    PeerTable pt = base;
+    pt.rank = g;
+    // ids are already global (world_ids = 0: no shard map)
+    if (st == AMS_OK && launch_exchange_push(KT, ps + (size_t)g * nq * KT, pi + (size_t)g * nq * KT, nq, 1, k, pt,
+                                             epoch, done[g], 0, 0, s) != cudaSuccess)
+      st = AMS_ERR_CUDA;
+  };
+  auto wait = [&](int g, int rd) {
+    if (st != AMS_OK) return;
+    PeerTable pt = base;
+    pt.rank = g;
+    const size_t o = ((size_t)rd * G + g) * nq;
+    if (launch_exchange_wait(KT, pt, nq, k, (unsigned long long)rd + 1, out_score + o * k, out_index + o * k,
+                             out_hit + o, threshold, s) != cudaSuccess)
+      st = AMS_ERR_CUDA;
+  };
+  // Every consumer is enqueued after the producers it waits for (no kernel ever waits on a
+  // concurrently running one).  LATE_CONSUMER: rank G-1 consumes round rd-1 only after the
+  // other ranks already produced round rd (their flags are then ahead of the epoch it waits
+  // for -- the order a descheduled host thread produces on a real box).  DROP_LAST: rank
+  // G-1 never produces the last round; its consumers must time out, not hang.
+  const bool late = (flags & AMS_SELFTEST_LATE_CONSUMER) != 0;
+  const bool drop = (flags & AMS_SELFTEST_DROP_LAST) != 0;
+  for (int rd = 0; rd < rounds && st == AMS_OK; ++rd) {
+    const bool skip_last = drop && rd == rounds - 1;
+    for (int g = 0; g < G - 1; ++g) push(g, rd);
+    if (late && rd > 0) wait(G - 1, rd - 1);
+    if (!skip_last) push(G - 1, rd);
+    for (int g = 0; g < G - 1; ++g) wait(g, rd);
+    if (!late) wait(G - 1, rd);
   }
+  if (late) wait(G - 1, rounds - 1);
   if (cudaStreamSynchronize(s) != cudaSuccess) st = AMS_ERR_CUDA;
+  if (st == AMS_OK && *err_host != 0) st = AMS_ERR_NCCL;   // a wait timed out
   for (void* p : allocs) cudaFree(p);
+  cudaFreeHost(err_host);
   return st;
 }
 

@@ -60,7 +60,10 @@ struct PeerTable {
   unsigned long long* flag[kMaxPeers];
   int32_t G, rank;
   int32_t max_q, max_k;
+  unsigned int* err;                // device alias of a host-mapped word: bit 0 = a wait timed out
+  unsigned long long timeout_ns;    // bound on the consumer's flag wait
 };
+constexpr unsigned long long kPeerTimeoutNs = 10ull * 1000 * 1000 * 1000;   // 10 s
 
 // --------------------------------------------------------------------------- pool
 struct Pool {
@@ -76,6 +79,7 @@ struct Pool {
   int32_t max_clusters4 = 0;
   int32_t KT_max = 8;
   bool broken = false;
+  ams_status_t broken_st = AMS_OK;   // status every call returns once broken
   bool collective = false;    // world > 1, or world == 1 with an nccl_id: shard lists go
                               // through the NCCL all-gather + shard merge (or peer exchange)
 
@@ -149,7 +153,9 @@ struct Pool {
   bool peer_mode = false;
   PeerTable peers{};
   unsigned long long epoch = 0;
-  unsigned int* x_done = nullptr;
+  unsigned int* x_done = nullptr;       // [1] arrival counter of merge_push_kernel's blocks
+  unsigned int* x_barrier = nullptr;    // [world] scratch of the mapping barrier all-gather
+  unsigned int* x_err_host = nullptr;   // host-mapped error word (PeerTable::err aliases it)
   float* x_s = nullptr;                 // own receive buffers (also peers.s[rank])
   int64_t* x_i = nullptr;
   unsigned long long* x_flag = nullptr;

@@ -335,11 +335,7 @@ __global__ void __launch_bounds__(kScanThreads, 1)
         const float* jsm = reinterpret_cast<const float*>(sAux + buf * AUX);
         const float* inv_sm = reinterpret_cast<const float*>(sAux + buf * AUX + AUXJ);
 #pragma unroll 1
-#ifdef AMS_DIAG_NO_EPILOGUE   // diagnostic builds only: MMA + TMA pipeline alone
-        for (int h = 0; h < 0; ++h) {
-#else
         for (int h = 0; h < 2 / CG; ++h) {
-#endif
           const int32_t rowbase = t * kBlockN + (h + (int)crank) * 128 + lg * 32;
           const bool valid = (int64_t)rowbase + lane < prm.L;
           const int ra = h * 128 + lg * 32 + lane;   // row within this CTA's aux block

@@ -42,29 +42,6 @@
 #include "ams_topk.cuh"
 
 namespace ams {
-#ifdef AMS_DIAG_TIMELINE   // diagnostic builds only: per-unit start/end globaltimer + cluster id
-constexpr int kDiagUnits = 1 << 16;
-__device__ unsigned long long g_diag_tl[kDiagUnits * 3];
-__device__ __forceinline__ unsigned int __smid() {
-  unsigned int r;
-  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
-  return r;
-}
-#endif
-
-#ifdef AMS_DIAG_COUNT   // diagnostic builds only: [0] chunks, [1] firing sub-chunks, [2] inserts
-__device__ unsigned long long g_diag_cnt[4];
-#define AMS_COUNT(i, v)                                                                 \
-  do {                                                                                  \
-    const unsigned long long v_ = (unsigned long long)(v);                              \
-    if ((threadIdx.x & 31) == 0) atomicAdd(&g_diag_cnt[i], v_);                         \
-    __syncwarp();                                                                       \
-  } while (0)
-#else
-#define AMS_COUNT(i, v) \
-  do {                   \
-  } while (0)
-#endif
 
 namespace {
 
@@ -148,15 +125,7 @@ __device__ __forceinline__ void epi_chunk(uint32_t taddr, int64_t jbase, int nva
         uint64_t da = 0ull, db = 0ull;   // +0.0f pairs
 #pragma unroll
         for (int t = 0; t < JF; ++t) {
-#if defined(AMS_DIAG_NO_LDS)
-          const float4 p = make_float4(qj[t] + 10.f + c4, qj[t] - 10.f - c4, qj[t] + 11.f, qj[t] - 12.f);
-#else
           const float4 p = lds4(jsm + t * kBlockN + 4 * c4);
-#endif
-#if defined(AMS_DIAG_LDS_ONLY)
-          asm volatile("" ::"f"(p.x), "f"(p.y), "f"(p.z), "f"(p.w));
-          continue;
-#endif
           const uint64_t a = ptx::sub2(QQ[t], ptx::pack2(p.x, p.y));
           da = ptx::fma2(a, a, da);
           const uint64_t b = ptx::sub2(QQ[t], ptx::pack2(p.z, p.w));
@@ -164,9 +133,6 @@ __device__ __forceinline__ void epi_chunk(uint32_t taddr, int64_t jbase, int nva
         }
         mn = fminf(mn, fminf(fminf(ptx::lo2(da), ptx::hi2(da)), fminf(ptx::lo2(db), ptx::hi2(db))));
       }
-#if defined(AMS_DIAG_LDS_ONLY)
-      mn = CUDART_INF_F;
-#endif
       fire |= (mn <= g2 ? 1u : 0u) << sub;
     }
   } else {
@@ -192,8 +158,6 @@ __device__ __forceinline__ void epi_chunk(uint32_t taddr, int64_t jbase, int nva
     }
   }
   uint32_t wfire = __reduce_or_sync(0xffffffffu, fire);
-  AMS_COUNT(0, 1);
-  AMS_COUNT(1, __popc(wfire));
   // exact path (rare), sub-chunk by sub-chunk; tcgen05.ld is warp-collective and the
   // loop is warp-uniform
   while (wfire != 0u) {
@@ -221,7 +185,6 @@ __device__ __forceinline__ void epi_chunk(uint32_t taddr, int64_t jbase, int nva
           ok = ok && (ds <= g2);
         }
       }
-      AMS_COUNT(2, __popc(__ballot_sync(0xffffffffu, ok)));
       if (ok) top.insert_monotone(s, (int32_t)(jbase + cc), k);
     }
   }
@@ -367,11 +330,7 @@ __global__ void __maxnreg__(168)
         // before every CTA has issued all loads of wave w-1.  Best effort: the wait is
         // bounded (~10 ms), so a grid that is not fully co-resident (MPS, concurrent
         // kernels) still progresses -- the lockstep only ever affects speed, never results.
-#ifndef AMS_DIAG_NO_LOCKSTEP   // diagnostic builds only: measure the lockstep's cost
         if (wave > 0) {
-#else
-        if (false) {
-#endif
           const uint32_t need = wave * gridDim.x;
           for (int it = 0; it < (1 << 16) && *reinterpret_cast<volatile uint32_t*>(prm.wave_ctr) < need; ++it)
             __nanosleep(128);
@@ -392,20 +351,8 @@ __global__ void __maxnreg__(168)
           for (int kb = 0; kb < n_kb; ++kb) {
             ptx::mbar_wait(&empty[stage], phase ^ 1u);
             if (ptx::elect_one()) {
-#if defined(AMS_DIAG_NO_B_LOAD) || defined(AMS_DIAG_NO_A_LOAD)
-              // diagnostic builds only (power attribution): after the first tile, one operand is
-              // not re-staged (the MMA reads stale shared memory; results are meaningless)
-              const bool skip = tile_count > 0;
-#ifdef AMS_DIAG_NO_B_LOAD
-              const bool load_a = true, load_b = !skip;
-#else
-              const bool load_a = !skip, load_b = true;
-#endif
-              const uint32_t bytes = (load_a ? kABytes : 0u) + (load_b ? BBYTES : 0u);
-#else
               constexpr bool load_a = true, load_b = true;
               constexpr uint32_t bytes = STAGE;
-#endif
               if (CG == 1) {
                 ptx::mbar_arrive_expect_tx(&full[stage], bytes);
                 if (load_a) ptx::tma_load_2d(sA + stage * kABytes, &tmap_q, &full[stage], kb * kBlockK, qrow0, pol_q);
@@ -459,10 +406,6 @@ __global__ void __maxnreg__(168)
         const int sp = u / n_qg;
         int t_lo, t_hi;
         split_tiles(sp, prm.S, prm.n_pt, t_lo, t_hi);
-#ifdef AMS_DIAG_TIMELINE
-        unsigned long long t0;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-#endif
         for (int t = t_lo; t < t_hi; ++t, ++tile_count) {
           const int buf = tile_count & 1;
           const uint32_t use = tile_count >> 1;
@@ -498,15 +441,6 @@ __global__ void __maxnreg__(168)
           }
           __syncwarp();
         }
-#ifdef AMS_DIAG_TIMELINE
-        unsigned long long t1;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-        if (lane == 0 && u < kDiagUnits) {
-          g_diag_tl[3 * u] = t0;
-          g_diag_tl[3 * u + 1] = t1;
-          g_diag_tl[3 * u + 2] = (unsigned long long)cid | ((unsigned long long)__smid() << 32);
-        }
-#endif
       }
     }
     __syncwarp();
@@ -579,9 +513,6 @@ __global__ void __maxnreg__(168)
           const uint32_t taddr = tmem_base + ((uint32_t)(lg * 32) << 16) + (uint32_t)(buf * kBlockN + col0);
           const int64_t jbase = (int64_t)t * kBlockN + col0;
           const int nvalid = (int)max((int64_t)0, min((int64_t)kChunk, row_end - jbase));
-#ifdef AMS_DIAG_NO_EPILOGUE  // diagnostic builds only (scripts/diag_power.py): MMA + TMA alone
-          continue;
-#endif
           if (sparse && epi_chunk_sorted<KT, JP>(taddr, jbase, nvalid, inv_sm + col0, joints_sm + col0, qj, iq,
                                                  prm.g2, bound, prm.k, wlo, whi, wlo1, whi1, lane, top))
             continue;
@@ -763,20 +694,3 @@ cudaError_t launch_match_tc(Pool& p, const MatchArgs& a, int32_t S, int32_t grid
 
 }  // namespace ams
 
-#ifdef AMS_DIAG_COUNT
-extern "C" int ams_diag_counts(unsigned long long* host, int reset) {
-  int e = (int)cudaMemcpyFromSymbol(host, ams::g_diag_cnt, 4 * 8);
-  if (reset) {
-    unsigned long long z[4] = {0, 0, 0, 0};
-    cudaMemcpyToSymbol(ams::g_diag_cnt, z, sizeof z);
-  }
-  return e;
-}
-#endif
-
-#ifdef AMS_DIAG_TIMELINE
-extern "C" int ams_diag_timeline(unsigned long long* host, int n_units) {
-  if (n_units > ams::kDiagUnits) n_units = ams::kDiagUnits;
-  return (int)cudaMemcpyFromSymbol(host, ams::g_diag_tl, (size_t)n_units * 3 * 8);
-}
-#endif

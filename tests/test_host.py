@@ -46,7 +46,7 @@ def test_library_is_sm100a_only(ams):
 
 
 def test_abi_version_and_status_strings(ams):
-    assert ams.ams_abi_version() == 1
+    assert ams.ams_abi_version() == ams.ABI_VERSION == 2
     for st, name in ams.STATUS.items():
         assert ams.ams_status_string(st) == name
 
