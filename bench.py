@@ -12,11 +12,16 @@ The default workload is BASELINE.json configs[2] (C3: M=1,048,576, d=1024 bf16, 
 Q=16384, k=16, theta 0.9, gamma 0.3), the north_star compute target; the pool is
 sharded by rows over N ranks (strong scaling).  Rank 0 prints ONE JSON line.
 
-Extra keys: roofline (dominant kernel, CUDA events on the launching stream), scan
-(the north_star 64-query HBM-bound scan of the same pool), e2e (host buffers through
-the C ABI, H2D + D2H inside the timed region), cpu_baseline (the oracle on the host
-cores, a bounded query sample), clocks (nvidia-smi during the timed region),
-gpu_launches (our kernels inside the timed region).
+Extra keys: roofline (dominant kernel, CUDA events on the launching stream; traffic
+only from an ncu capture of this very library build), outputs_sha256 (bit-identity
+across N), ungated (the same batch with gate_radius = inf), scan (the north_star
+64-query HBM-bound scan of the same pool), gate_first_variant (f3), e2e (host buffers
+through the C ABI, H2D + D2H inside the timed region), peer_exchange (N > 1: the fused
+NVLink exchange of f1, checked bit-identical to the NCCL path), c4 (BASELINE configs[3]
+at every N: the 16.8M-row pool resharded over the N ranks, with its own 64-query scan
+and output hash), cpu_baseline (the oracle on the host cores, a bounded query sample,
+CPU model named), clocks (nvidia-smi during the main timed region; every leg carries its
+own window), gpu_launches (our kernels inside the timed region).
 """
 from __future__ import annotations
 
@@ -52,19 +57,9 @@ def load_peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
 
 
-def load_traffic(workload: str, which: str):
-    """dram read+write bytes per launch of the dominant kernel from the committed ncu
-    summary (profiles/ncu_summary.json), or None."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
-            s = json.load(f)
-        return s[workload][which]["dram_bytes_per_launch"]
-    except Exception:
-        return None
-
-
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons, sampled every 100 ms during the timed region."""
+    """nvidia-smi clocks/throttle reasons, sampled every 100 ms from the first timed region
+    to the end of the last leg; window(t0, t1) summarises the samples of one leg."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
@@ -72,7 +67,7 @@ class ClockSampler:
 
     def __init__(self, device_index: int):
         self.dev = device_index
-        self.rows = []
+        self.rows = []   # (wall time, fields)
         self.proc = None
         self.th = None
 
@@ -91,7 +86,33 @@ class ClockSampler:
         for line in self.proc.stdout:
             parts = [x.strip() for x in line.split(",")]
             if len(parts) >= 8:
-                self.rows.append(parts)
+                self.rows.append((time.time(), parts))
+
+    @classmethod
+    def summarise(cls, rows):
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        pw = [float(r[3]) for r in rows if r[3].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        reasons = set()
+        for r in rows:
+            for n, v in zip(cls.NAMES, r[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(rows),
+                "power_w_median": statistics.median(pw) if pw else None}
+
+    def window(self, t0: float, t1: float):
+        """Samples taken while [t0, t1] ran (plus the one sample straddling each end: a
+        sub-100-ms leg still gets a reading)."""
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = list(self.rows)
+        inside = [r for t, r in rows if t0 <= t <= t1 + 0.1]
+        if not inside:
+            after = [r for t, r in rows if t > t1]
+            inside = after[:1]
+        return self.summarise(inside)
 
     def stop(self):
         if self.proc is None:
@@ -104,17 +125,7 @@ class ClockSampler:
             self.proc.kill()
         if self.th:
             self.th.join(timeout=2)
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        pw = [float(r[3]) for r in self.rows if r[3].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        reasons = set()
-        for r in self.rows:
-            for n, v in zip(self.NAMES, r[4:8]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.rows),
-                "power_w_median": statistics.median(pw) if pw else None}
+        return self.summarise([r for _, r in self.rows])
 
 
 def parse():
@@ -132,6 +143,12 @@ def parse():
     ap.add_argument("--gate-first", action="store_true",
                     help="time ams_match_gate_first (SURVEY 8(f) f3 variant) instead of the dense ams_match")
     ap.add_argument("--no-variant", action="store_true", help="skip the gate-first side measurement")
+    ap.add_argument("--no-ungated", action="store_true", help="skip the ungated (gate_radius = inf) sub-line")
+    ap.add_argument("--no-c4", action="store_true", help="skip the configs[3] (C4) block")
+    ap.add_argument("--no-peer", action="store_true", help="skip the fused peer-exchange side measurement (N > 1)")
+    ap.add_argument("--force-collective", action="store_true",
+                    help="N = 1 only: run the multi-GPU code path (NCCL all-gather, shard merge, peer exchange) "
+                         "over a 1-rank communicator -- a dry run of what --gpus N > 1 executes")
     ap.add_argument("--kernel-policy", type=int, default=0, choices=[0, 1, 2, 3],
                     help="bit mask for A/B measurements: 1 = batches of <= 128 queries use the 128-query-tile "
                          "kernel instead of the small-batch kernel; 2 = two CTA pairs per 4-CTA cluster sharing "
@@ -385,7 +402,7 @@ def run_reference(args):
     q = q.view(torch.int16).cpu().numpy().view(np.uint16)
     qj = qj.cpu().numpy()
     cores = oracle.max_threads()
-    n_s = args.cpu_sample or max(1, cores)
+    n_s = args.cpu_sample or max(1, 4 * cores)   # several queries per core: no per-step load imbalance
     per_query_s = cfg.M * cfg.d / 1e9 / max(cores, 1)
     while n_s > 1 and n_s * per_query_s * (args.steps + args.warmup) > 240:
         n_s //= 2
@@ -401,11 +418,55 @@ def run_reference(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": config_block(cfg, args, 1, gamma),
             "cpu_baseline": {"value": value, "unit": "queries/s", "cores": cores, "kind": "oracle",
+                             "cpu_model": cpu_model(),
                              "sample": f"{n_s} queries per step of {cfg.name} against the full pool "
                                        f"({cfg.M} rows), oracle mode A (fp64 brute force, OpenMP over queries) "
                                        f"per ~1M-row chunk + oracle.merge"},
             "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def lib_sha256() -> str:
+    import hashlib
+    with open(os.path.join(ROOT, "paper_2508_10259_b200", "libams.so"), "rb") as f:
+        return hashlib.sha256(f.read()).hexdigest()
+
+
+def traffic_of(workload: str, which: str):
+    """(dram bytes per launch, source) of the dominant kernel from the committed ncu
+    summary -- only if that capture was taken of THIS library build (sha256 of
+    libams.so recorded by scripts/ncu_summary.py); otherwise (None, why)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            e = json.load(f)[workload][which]
+    except Exception:
+        return None, "no ncu --set full capture of this kernel/workload in profiles/ncu_summary.json"
+    sha = lib_sha256()
+    if e.get("lib_sha256") != sha:
+        return None, (f"profiles/ncu_summary.json capture ({e.get('round')}, {e.get('report')}) is of another "
+                      f"library build; not reused")
+    return e["dram_bytes_per_launch"], (f"ncu --set full capture {e.get('round')} ({e.get('report')}) of this "
+                                        f"library build (libams.so sha256 {sha[:16]}), per launch")
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def outputs_sha256(out_i, out_s, out_h) -> str:
+    """sha256 of (idx int64, score fp32, hit u8) bytes: bit-identity across N (pin P8 on hardware)."""
+    import hashlib
+    h = hashlib.sha256()
+    for t in (out_i, out_s, out_h):
+        h.update(t.contiguous().cpu().numpy().tobytes())
+    return h.hexdigest()
 
 
 def main():
@@ -430,6 +491,8 @@ def main():
     tdist = None
     if world > 1:
         import torch.distributed as tdist
+    stream = torch.cuda.current_stream()
+    clk = ClockSampler(torch.cuda.current_device())
 
     def barrier():
         if tdist is not None:
@@ -442,33 +505,96 @@ def main():
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
         return float(t.item())
 
+    def all_ok(ok: bool) -> bool:
+        if tdist is None:
+            return ok
+        t = torch.tensor([0 if ok else 1], dtype=torch.int32, device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        return int(t.item()) == 0
+
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+
+    def timed(fn, reps):
+        """barrier + sync, CUDA events around reps calls on `stream`, sync + barrier;
+        (max over ranks of the elapsed ms, wall window for the clock samples)."""
+        barrier()
+        torch.cuda.synchronize()
+        w0 = time.time()
+        ev0.record(stream)
+        for _ in range(reps):
+            fn()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        w1 = time.time()
+        barrier()
+        return max_over_ranks(ev0.elapsed_time(ev1)), (w0, w1)
+
+    def kernel_avg(pool):
+        k_ms, k_n = ams.ams_pool_read_profile(pool.handle)
+        return max_over_ranks(k_ms / max(k_n, 1))
+
+    def make_pool(c):
+        pool = adist.create_pool(c.d, c.J, c.M, c.Q, c.k, dtype="bf16", shard_block=0,
+                                 force_collective=args.force_collective)
+        ams.ams_pool_set_kernel_policy(pool.handle, args.kernel_policy)
+        dummy = torch.zeros(1, c.d, dtype=torch.bfloat16, device=dev)
+        dummy_j = torch.zeros(1, c.J, dtype=torch.float32, device=dev)
+
+        def append_fn(e, j, n):
+            if e is None:
+                pool.append(dummy, dummy_j, n)   # this rank owns none of these rows
+            else:
+                pool.append(e, j, n)
+
+        need = lambda lo, hi: adist.owned_range_overlaps(c.M, world, 0, rank, lo, hi)  # noqa: E731
+        q, qj, labels = ams_gen.build_device_workload(c, dev, append_fn, chunk_needed=need)
+        torch.cuda.synchronize()
+        assert pool.size == c.M
+        return pool, q, qj, labels
+
+    def scan_leg(pool, c, q, qj, g, nq=64):
+        """The north_star 64-query HBM-bound scan of pool `c` (per GPU shard)."""
+        o = (torch.empty(nq, c.k, dtype=torch.int64, device=dev), torch.empty(nq, c.k, dtype=torch.float32, device=dev),
+             torch.empty(nq, dtype=torch.uint8, device=dev))
+        qs, qjs = q[:nq].contiguous(), qj[:nq].contiguous()
+        fn = lambda: ams.ams_match(pool.handle, qs, qjs, nq, c.k, c.theta, g, *o, stream)  # noqa: E731
+        for _ in range(5):
+            fn()
+        torch.cuda.synchronize()
+        ams.ams_pool_read_profile(pool.handle)
+        ams.ams_pool_set_profiling(pool.handle, True)
+        reps = max(20, 5 * args.steps)
+        ms, win = timed(fn, reps)
+        ams.ams_pool_set_profiling(pool.handle, False)
+        s_ms = ms / reps
+        plan = ams.ams_pool_last_plan(pool.handle)
+        k_avg = kernel_avg(pool)
+        bytes_shard = (c.M / world) * (2 * c.d + 4 * c.J + 4)
+        gbs = bytes_shard / (k_avg / 1e3) / 1e9
+        kname = "match_scan" if plan["kernel_id"] == 4 else "match_tc_scan"
+        traffic, tsrc = traffic_of(c.name if c.name != "c3scan" else "c3", kname)
+        return {"queries": nq, "value": nq / (s_ms / 1e3), "unit": "queries/s", "ms_per_call": s_ms,
+                "pool_scan_gbps_per_gpu": bytes_shard / (s_ms / 1e3) / 1e9, "plan": plan,
+                "roofline": {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                             "frac": gbs / peaks["hbm_gbs"],
+                             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks["source"] == "measured"
+                             else "fallback 6650 GB/s (B200_PROFILING.md; MEASURED_PEAKS.json absent)",
+                             "traffic": traffic, "traffic_source": tsrc,
+                             "kernel": "match_scan_kernel" if plan["kernel_id"] == 4 else "match_tc_kernel",
+                             "kernel_ms_avg": k_avg, "frac_vs_datasheet_8000": gbs / 8000.0,
+                             "algorithmic_bytes_per_launch": bytes_shard},
+                "clocks": clk.window(*win)}
+
     # ------------------------------------------------------------------ pool + queries
-    pool = adist.create_pool(cfg.d, cfg.J, cfg.M, cfg.Q, cfg.k, dtype="bf16", shard_block=0)
-    ams.ams_pool_set_kernel_policy(pool.handle, args.kernel_policy)
-    dummy = torch.zeros(1, cfg.d, dtype=torch.bfloat16, device=dev)
-    dummy_j = torch.zeros(1, cfg.J, dtype=torch.float32, device=dev)
-
-    def append_fn(e, j, n):
-        if e is None:
-            pool.append(dummy, dummy_j, n)   # this rank owns none of these rows
-        else:
-            pool.append(e, j, n)
-
-    need = lambda lo, hi: adist.owned_range_overlaps(cfg.M, world, 0, rank, lo, hi)  # noqa: E731
-    want_cpu = (not args.no_cpu_baseline) and world == 1 and rank == 0
-    q, qj, labels = ams_gen.build_device_workload(cfg, dev, append_fn, chunk_needed=need)
-    torch.cuda.synchronize()
-    assert pool.size == cfg.M
-
+    pool, q, qj, labels = make_pool(cfg)
     out_i = torch.empty(cfg.Q, cfg.k, dtype=torch.int64, device=dev)
     out_s = torch.empty(cfg.Q, cfg.k, dtype=torch.float32, device=dev)
     out_h = torch.empty(cfg.Q, dtype=torch.uint8, device=dev)
-    stream = torch.cuda.current_stream()
-
     match_fn = ams.ams_match_gate_first if args.gate_first else ams.ams_match
 
-    def step(qe=q, qjj=qj, nq=cfg.Q, fn=None):
-        (fn or match_fn)(pool.handle, qe, qjj, nq, cfg.k, cfg.theta, gamma, out_i, out_s, out_h, stream)
+    def step(qe=q, qjj=qj, nq=cfg.Q, fn=None, g=gamma):
+        (fn or match_fn)(pool.handle, qe, qjj, nq, cfg.k, cfg.theta, g, out_i, out_s, out_h, stream)
 
     # ------------------------------------------------------------------ main timing
     warmups = max(args.warmup, 3)   # the timing rules require >= 3 warm-up steps
@@ -476,29 +602,17 @@ def main():
         step()
     torch.cuda.synchronize()
     ams.ams_pool_read_profile(pool.handle)            # drop warm-up events
-    clk = ClockSampler(torch.cuda.current_device())
     clk.start()
     time.sleep(0.15)
     ams.ams_pool_set_profiling(pool.handle, True)
     l0 = ams.ams_pool_launch_count(pool.handle)
-    barrier()
-    torch.cuda.synchronize()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    for _ in range(args.steps):
-        step()
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    barrier()
+    t_ms, win_main = timed(step, args.steps)
     launches = ams.ams_pool_launch_count(pool.handle) - l0
     ams.ams_pool_set_profiling(pool.handle, False)
-    clocks = clk.stop()
-    t_ms = max_over_ranks(ev0.elapsed_time(ev1))
-    kern_ms, kern_n = ams.ams_pool_read_profile(pool.handle)
-    kern_avg = max_over_ranks(kern_ms / max(kern_n, 1))
+    kern_avg = kernel_avg(pool)
     plan = ams.ams_pool_last_plan(pool.handle)
     hit_rate = float(out_h.float().mean().item())
+    out_sha = outputs_sha256(out_i, out_s, out_h)
     lab = labels.cpu().numpy()
     top1 = out_i[:, 0].cpu().numpy()
     nd = lab >= 0
@@ -509,9 +623,9 @@ def main():
     flops_launch = 2.0 * cfg.Q * m_shard * cfg.d
     bytes_step = cfg.M * (2 * cfg.d + 4 * cfg.J + 4)
     achieved_tf = flops_launch / (kern_avg / 1e3) / 1e12
+    traffic, tsrc = traffic_of(args.workload, "match_tc")
     roofline = {"bound": "tensor", "achieved": achieved_tf, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
-                "frac": achieved_tf / peaks["bf16_tflops"],
-                "traffic": load_traffic(args.workload, "match_tc"),
+                "frac": achieved_tf / peaks["bf16_tflops"], "traffic": traffic, "traffic_source": tsrc,
                 "kernel": "match_tc_kernel (tcgen05 GEMM + fused gate/top-k epilogue)",
                 "algorithmic_per_launch": {"flop": flops_launch, "bytes": bytes_step / world},
                 "kernel_ms_avg": kern_avg, "kernel_share_of_step": kern_avg / (t_ms / args.steps),
@@ -523,9 +637,10 @@ def main():
 
     if not args.gate_first and cfg.Q <= 128:   # below the ridge (~250 flop/B): HBM-bound scan
         gbs = (bytes_step / world) / (kern_avg / 1e3) / 1e9
+        kname = "match_scan" if plan.get("kernel_id") == 4 else "match_tc"
+        traffic, tsrc = traffic_of(args.workload, kname)
         roofline = {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                    "frac": gbs / peaks["hbm_gbs"],
-                    "traffic": load_traffic(args.workload, "match_scan" if plan.get("kernel_id") == 4 else "match_tc"),
+                    "frac": gbs / peaks["hbm_gbs"], "traffic": traffic, "traffic_source": tsrc,
                     "kernel": "match_scan_kernel" if plan.get("kernel_id") == 4 else "match_tc_kernel",
                     "algorithmic_per_launch": {"bytes": bytes_step / world, "flop": flops_launch},
                     "kernel_ms_avg": kern_avg, "kernel_share_of_step": kern_avg / (t_ms / args.steps),
@@ -537,47 +652,32 @@ def main():
         jbytes = m_shard * 4 * jp
         gbs = jbytes / (kern_avg / 1e3) / 1e9
         roofline = {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                    "frac": gbs / peaks["hbm_gbs"], "traffic": None,
+                    "frac": gbs / peaks["hbm_gbs"], "traffic": None, "traffic_source": "not captured",
                     "kernel": "gate_scan_kernel + score_kernel (gate-first variant)",
                     "algorithmic_per_launch": {"bytes": jbytes}, "kernel_ms_avg": kern_avg,
                     "note": "joint bytes per launch / kernel time; the scan is ALU-bound, so this is low by design"}
 
-    # ------------------------------------------------------------------ 64-query scan
-    scan = None
-    if not args.no_scan and cfg.Q >= 64:
-        nq = 64
-        qs, qjs = q[:nq].contiguous(), qj[:nq].contiguous()
-        for _ in range(5):
-            step(qs, qjs, nq)
+    # ------------------------------------------------------------------ ungated sub-line
+    ungated = None
+    if not args.no_ungated and not args.gate_first and math.isfinite(gamma) and cfg.Q > 128:
+        g_inf = float("inf")
+        step(g=g_inf)
         torch.cuda.synchronize()
         ams.ams_pool_read_profile(pool.handle)
         ams.ams_pool_set_profiling(pool.handle, True)
-        reps = max(20, 5 * args.steps)
-        barrier()
-        torch.cuda.synchronize()
-        ev0.record(stream)
-        for _ in range(reps):
-            step(qs, qjs, nq)
-        ev1.record(stream)
-        torch.cuda.synchronize()
-        barrier()
+        u_ms, win = timed(lambda: step(g=g_inf), args.steps)
         ams.ams_pool_set_profiling(pool.handle, False)
-        s_ms = max_over_ranks(ev0.elapsed_time(ev1)) / reps
-        s_plan = ams.ams_pool_last_plan(pool.handle)
-        k_ms, k_n = ams.ams_pool_read_profile(pool.handle)
-        k_avg = max_over_ranks(k_ms / max(k_n, 1))
-        gbs_kernel = (bytes_step / world) / (k_avg / 1e3) / 1e9
-        scan = {"queries": nq, "value": nq / (s_ms / 1e3), "unit": "queries/s", "ms_per_call": s_ms,
-                "pool_scan_gbps_per_gpu": (bytes_step / world) / (s_ms / 1e3) / 1e9,
-                "roofline": {"bound": "hbm", "achieved": gbs_kernel, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                             "frac": gbs_kernel / peaks["hbm_gbs"],
-                             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks["source"] == "measured"
-                             else "fallback 6650 GB/s (B200_PROFILING.md; MEASURED_PEAKS.json absent)",
-                             "traffic": load_traffic(args.workload, "match_scan" if s_plan["kernel_id"] == 4
-                                                     else "match_tc_scan"),
-                             "kernel": "match_scan_kernel" if s_plan["kernel_id"] == 4 else "match_tc_kernel",
-                             "kernel_ms_avg": k_avg, "frac_vs_datasheet_8000": gbs_kernel / 8000.0,
-                             "algorithmic_bytes_per_launch": bytes_step / world}}
+        u_k = kernel_avg(pool)
+        u_tf = flops_launch / (u_k / 1e3) / 1e12
+        ungated = {"gate_radius": "inf", "value": cfg.Q * args.steps / (u_ms / 1e3), "unit": "queries/s",
+                   "ms_per_step": u_ms / args.steps, "kernel_ms_avg": u_k, "achieved_tflops": u_tf,
+                   "frac": u_tf / peaks["bf16_tflops"], "outputs_sha256": outputs_sha256(out_i, out_s, out_h),
+                   "clocks": clk.window(*win)}
+
+    # ------------------------------------------------------------------ 64-query scan
+    scan = None
+    if not args.no_scan and cfg.Q >= 64:
+        scan = scan_leg(pool, cfg, q, qj, gamma)
 
     # ------------------------------------------------------------------ gate-first variant (f3)
     variant = None
@@ -589,16 +689,11 @@ def main():
                 step(qv, qjv, nq, ams.ams_match_gate_first)
             torch.cuda.synchronize()
             reps = max(5, args.steps)
-            barrier()
-            ev0.record(stream)
-            for _ in range(reps):
-                step(qv, qjv, nq, ams.ams_match_gate_first)
-            ev1.record(stream)
-            torch.cuda.synchronize()
-            barrier()
-            v_ms = max_over_ranks(ev0.elapsed_time(ev1)) / reps
+            v_ms, win = timed(lambda: step(qv, qjv, nq, ams.ams_match_gate_first), reps)
+            v_ms /= reps
             res[label] = {"queries": nq, "ms_per_call": v_ms, "value": nq / (v_ms / 1e3), "unit": "queries/s",
-                          "joint_bytes_gbps_per_gpu": (cfg.M / world) * 4 * (8 if cfg.J <= 8 else 16) / (v_ms / 1e3) / 1e9}
+                          "joint_bytes_gbps_per_gpu": (cfg.M / world) * 4 * (8 if cfg.J <= 8 else 16) / (v_ms / 1e3) / 1e9,
+                          "clocks": clk.window(*win)}
         variant = {"name": "ams_match_gate_first (SURVEY 8(f) f3; exact, gate evaluated first)", **res}
 
     # ------------------------------------------------------------------ e2e (host buffers)
@@ -619,21 +714,41 @@ def main():
         for _ in range(2):
             e2e_step()
         torch.cuda.synchronize()
-        barrier()
-        ev0.record(stream)
-        for _ in range(args.steps):
-            e2e_step()
-        ev1.record(stream)
-        torch.cuda.synchronize()
-        barrier()
-        e_ms = max_over_ranks(ev0.elapsed_time(ev1))
+        e_ms, win = timed(e2e_step, args.steps)
         h2d = hq.numel() * hq.element_size() + hqj.numel() * hqj.element_size()
         d2h = ho_i.numel() * 8 + ho_s.numel() * 4 + ho_h.numel()
         e2e = {"value": cfg.Q * args.steps / (e_ms / 1e3), "unit": "queries/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "path": "ams_match(host pinned q, q_joints) + D2H of idx/score/hit"}
+               "d2h_bytes_per_step": d2h, "path": "ams_match(host pinned q, q_joints) + D2H of idx/score/hit",
+               "clocks": clk.window(*win)}
+
+    # ------------------------------------------------------------------ fused peer exchange (f1), N > 1
+    peer = None
+    if (world > 1 or args.force_collective) and not args.no_peer and not args.gate_first:
+        try:
+            ams.ams_pool_enable_peer_exchange(pool.handle)
+            ok, why = True, ""
+        except Exception as e:   # collective inside the library: every rank gets the same status
+            ok, why = False, str(e)
+        if all_ok(ok):
+            try:
+                step()
+                torch.cuda.synchronize()
+                same = outputs_sha256(out_i, out_s, out_h) == out_sha
+                p_ms, win = timed(step, args.steps)
+                st = ams.ams_pool_status(pool.handle)
+                same = same and outputs_sha256(out_i, out_s, out_h) == out_sha
+                peer = {"status": "ok" if st == 0 else ams.ams_status_string(st),
+                        "value": cfg.Q * args.steps / (p_ms / 1e3), "unit": "queries/s",
+                        "ms_per_step": p_ms / args.steps, "bit_identical_to_nccl_path": bool(all_ok(same)),
+                        "clocks": clk.window(*win)}
+            except Exception as e:
+                peer = {"status": "error", "error": str(e)}
+        else:
+            peer = {"status": "unsupported", "error": why or "a peer rank could not map the exchange buffers"}
 
     # ------------------------------------------------------------------ CPU oracle baseline
     cpu = None
+    want_cpu = (not args.no_cpu_baseline) and world == 1 and rank == 0
     if want_cpu:
         qn = q.view(torch.int16).cpu().numpy().view(np.uint16)
         qjn = qj.cpu().numpy()
@@ -645,10 +760,48 @@ def main():
             # calibrated: rescale the sample to ~15 s of oracle time (contract: 10-30 s)
             n_s = int(min(cfg.Q, max(n_s + 1, round(n_s * 15.0 / max(dt, 1e-3)))))
             dt, cores = oracle_sample(cfg, dev, qn, qjn, gamma, n_s)
-        cpu = {"value": n_s / dt, "unit": "queries/s", "cores": cores, "kind": "oracle",
+        cpu = {"value": n_s / dt, "unit": "queries/s", "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
                "sample": f"first {n_s} of the {cfg.Q} {cfg.name} queries against the full {cfg.M}-row pool, "
                          f"oracle mode A (fp64 brute force, OpenMP over queries) per ~1M-row chunk + oracle.merge, "
                          f"{dt:.1f} s in the oracle"}
+    pool.close()
+    del q, qj
+
+    # ------------------------------------------------------------------ C4 (configs[3]) at every N
+    c4 = None
+    if args.workload == "c3" and not args.no_c4:
+        c4cfg = ams_gen.CONFIGS["c4"]
+        pool4, q4, qj4, _ = make_pool(c4cfg)
+        o4 = (torch.empty(c4cfg.Q, c4cfg.k, dtype=torch.int64, device=dev),
+              torch.empty(c4cfg.Q, c4cfg.k, dtype=torch.float32, device=dev),
+              torch.empty(c4cfg.Q, dtype=torch.uint8, device=dev))
+        fn4 = lambda: ams.ams_match(pool4.handle, q4, qj4, c4cfg.Q, c4cfg.k, c4cfg.theta, c4cfg.gamma, *o4,  # noqa: E731
+                                    stream)
+        for _ in range(3):
+            fn4()
+        torch.cuda.synchronize()
+        ams.ams_pool_read_profile(pool4.handle)
+        ams.ams_pool_set_profiling(pool4.handle, True)
+        reps4 = max(3, args.steps // 4)
+        c_ms, win = timed(fn4, reps4)
+        ams.ams_pool_set_profiling(pool4.handle, False)
+        k4 = kernel_avg(pool4)
+        fl4 = 2.0 * c4cfg.Q * (-(-c4cfg.M // world)) * c4cfg.d
+        tf4 = fl4 / (k4 / 1e3) / 1e12
+        c4 = {"workload": "c4 (BASELINE.json configs[3]): M=16,777,216 d=1024 bf16 J=7, Q=8192, k=32, theta 0.9, "
+                          f"gamma 0.3; rows contiguous over {world} rank(s)",
+              "value": c4cfg.Q * reps4 / (c_ms / 1e3), "unit": "queries/s", "n_gpus": world, "steps": reps4,
+              "warmup": 3, "ms_per_step": c_ms / reps4, "scaling": "strong",
+              "roofline": {"bound": "tensor", "achieved": tf4, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                           "frac": tf4 / peaks["bf16_tflops"], "kernel_ms_avg": k4,
+                           "algorithmic_per_launch": {"flop": fl4}},
+              "plan": ams.ams_pool_last_plan(pool4.handle), "outputs_sha256": outputs_sha256(*o4),
+              "clocks": clk.window(*win)}
+        if not args.no_scan:
+            c4["scan"] = scan_leg(pool4, c4cfg, q4, qj4, c4cfg.gamma)
+        pool4.close()
+    clocks_all = clk.stop()
+    clocks = clk.window(*win_main)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
@@ -656,14 +809,15 @@ def main():
                 "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
                 "config": config_block(cfg, args, world, gamma),
                 "pool_scan_gbps_per_gpu": (bytes_step / world) / (t_ms / args.steps / 1e3) / 1e9,
-                "roofline": roofline, "scan": scan, "gate_first_variant": variant, "e2e": e2e, "cpu_baseline": cpu,
-                "clocks": clocks,
+                "collective_path": bool(world > 1 or args.force_collective),
+                "roofline": roofline, "outputs_sha256": out_sha, "ungated": ungated, "scan": scan,
+                "gate_first_variant": variant, "e2e": e2e, "peer_exchange": peer, "c4": c4, "cpu_baseline": cpu,
+                "clocks": clocks, "clocks_whole_run": clocks_all,
                 "gpu_launches": launches, "plan": plan, "hit_rate": hit_rate, "path": "ams_match_gate_first"
                 if args.gate_first else "ams_match (dense tcgen05)",
                 "near_dup_top1_equals_source": label_top1,
                 "paper_context": PAPER_CONTEXT}
         print(json.dumps(line), flush=True)
-    pool.close()
     if tdist is not None:
         tdist.destroy_process_group()
 

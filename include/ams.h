@@ -155,6 +155,31 @@ ams_status_t ams_match_gate_first(ams_pool_t pool, const void* q_emb, const floa
                                   int32_t k, float threshold, float gate_radius, int64_t* out_index,
                                   float* out_score, uint8_t* out_hit, void* stream);
 
+/* Route-selecting variant of ams_match ("select by measured
+ * pass-rate"): identical arguments, semantics, outputs and errors; the pool picks the
+ * dense tensor-core path (ams_match) or the gate-first path (ams_match_gate_first) for
+ * this call from a cost model fed by an estimate of the eligible rows per query -- the
+ * exact canonical gate over a strided sample of <= 64 of the call's queries x <= 32768
+ * local rows.  The estimate is taken synchronously (stream synchronised once) on the
+ * first gated call, when the gate radius changes or the shard size changed 2x, and
+ * refreshed asynchronously every 64 calls otherwise.  Ungated calls and fp32 pools always
+ * take the dense/exact path.  Both routes are exact; scores may differ between routes in
+ * the last fp32 bits (tensor-core vs CUDA-core accumulation), within the stated
+ * tolerance.  With world > 1 each rank chooses for its own shard.  Not capturable in a
+ * CUDA graph (AMS_ERR_UNSUPPORTED during capture).  The route of the last call:
+ * ams_pool_last_route. */
+ams_status_t ams_match_auto(ams_pool_t pool, const void* q_emb, const float* q_joints, int32_t nq,
+                            int32_t k, float threshold, float gate_radius, int64_t* out_index,
+                            float* out_score, uint8_t* out_hit, void* stream);
+
+/* Route of the last ams_match_auto call on this pool: *route 0 = dense, 1 = gate-first,
+ * -1 = none yet; the estimated eligible rows per query of the local shard (-1 if none),
+ * and the cost model's estimates in ms for both routes (0 if the route was forced by an
+ * ungated call or an fp32 pool).  Any output pointer may be NULL.
+ * Errors: AMS_ERR_INVALID_ARGUMENT (null pool). */
+ams_status_t ams_pool_last_route(ams_pool_t pool, int32_t* route, double* est_eligible_per_query,
+                                 double* est_ms_dense, double* est_ms_gate_first);
+
 /* The final k-way merge (north_star "a final k-way merge kernel"; step a7 of
  * DESIGN.md): merges G ranked lists per query -- in_score/in_index are DEVICE arrays
  * [G, nq, kin] (fp32 score, int64 global index, -1 padding), each list ordered by
@@ -278,15 +303,26 @@ ams_status_t ams_vstore_release(ams_vstore_t store, const uint64_t* ids, int32_t
                                 void* stream);
 
 /* Looks up n ids (DEVICE): arena offset and length (DEVICE i64 [n]; -1 if unknown) and,
- * if out_refcount is not NULL, the reference count (0 if unknown). */
+ * if out_refcount is not NULL, the reference count (0 if unknown).  Offsets stay valid
+ * until the next ams_vstore_intern or ams_vstore_compact (either may move bytes). */
 ams_status_t ams_vstore_resolve(ams_vstore_t store, const uint64_t* ids, int32_t n, int64_t* out_offset,
                                 int64_t* out_len, int64_t* out_refcount, void* stream);
 
 /* Device pointer of the byte arena (read-only for callers). */
 ams_status_t ams_vstore_arena(ams_vstore_t store, const uint8_t** arena);
 
-/* Synchronises; live entries, their total bytes, and arena bytes used (append-only). */
+/* Synchronises; live entries, their total bytes, and the arena top (bytes in use,
+ * including holes left by removed entries that no compaction has reclaimed yet). */
 ams_status_t ams_vstore_stats(ams_vstore_t store, int64_t* n_entries, int64_t* total_bytes, int64_t* arena_used);
+
+/* Reclaims the space of removed entries ("Any action whose reference count
+ * drops to zero is removed"; SPEC.md "no leak"): packs the live entries' bytes to the
+ * front of the arena (arena top = total live bytes afterwards) and rebuilds the table
+ * without tombstones.  ams_vstore_intern runs it automatically when a batch might not fit
+ * behind the arena top or might push the table past 3/4 load.  Stream-ordered on
+ * `stream`, then synchronises it once.  Resolved offsets become stale.
+ * Errors: AMS_ERR_INVALID_ARGUMENT, AMS_ERR_CUDA. */
+ams_status_t ams_vstore_compact(ams_vstore_t store, void* stream);
 
 ams_status_t ams_vstore_destroy(ams_vstore_t store);
 

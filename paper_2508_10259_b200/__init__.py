@@ -28,13 +28,14 @@ STATUS = {0: "AMS_OK", 1: "AMS_ERR_INVALID_ARGUMENT", 2: "AMS_ERR_CAPACITY", 3: 
 
 # Every symbol include/ams.h declares (tests check the library exports all of them).
 EXPORTS = ("ams_get_nccl_unique_id", "ams_pool_create", "ams_pool_append", "ams_match", "ams_match_gate_first",
+           "ams_match_auto", "ams_pool_last_route",
            "ams_merge_topk", "ams_pool_enable_peer_exchange", "ams_exchange_selftest",
            "ams_pool_status", "ams_pool_size",
            "ams_pool_destroy", "ams_status_string", "ams_pool_set_profiling", "ams_pool_read_profile",
            "ams_pool_launch_count", "ams_pool_last_plan", "ams_pool_set_kernel_policy", "ams_shard_locate", "ams_shard_capacity",
            "ams_abi_version", "ams_hasher_create", "ams_hash_actions", "ams_hasher_destroy",
            "ams_vstore_create", "ams_vstore_intern", "ams_vstore_release", "ams_vstore_resolve",
-           "ams_vstore_arena", "ams_vstore_stats", "ams_vstore_destroy", "ams_tier_create", "ams_tier_admit",
+           "ams_vstore_arena", "ams_vstore_stats", "ams_vstore_compact", "ams_vstore_destroy", "ams_tier_create", "ams_tier_admit",
            "ams_tier_touch", "ams_tier_evict_until", "ams_tier_fetch", "ams_tier_info", "ams_tier_usage",
            "ams_tier_read", "ams_tier_destroy")
 
@@ -64,6 +65,9 @@ def _load():
         "ams_pool_append": [V, V, V, I64, ctypes.POINTER(I64), V],
         "ams_match": [V, V, V, I32, I32, ctypes.c_float, ctypes.c_float, V, V, V, V],
         "ams_match_gate_first": [V, V, V, I32, I32, ctypes.c_float, ctypes.c_float, V, V, V, V],
+        "ams_match_auto": [V, V, V, I32, I32, ctypes.c_float, ctypes.c_float, V, V, V, V],
+        "ams_pool_last_route": [V, ctypes.POINTER(I32), ctypes.POINTER(ctypes.c_double),
+                                ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)],
         "ams_merge_topk": [V, V, I32, I32, I32, I32, ctypes.c_float, V, V, V, V],
         "ams_pool_enable_peer_exchange": [V],
         "ams_exchange_selftest": [I32, I32, I32, I32, ctypes.c_float, V, V, V, V, V, I32, V],
@@ -88,6 +92,7 @@ def _load():
         "ams_vstore_arena": [V, ctypes.POINTER(V)],
         "ams_vstore_stats": [V, ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64)],
         "ams_vstore_destroy": [V],
+        "ams_vstore_compact": [V, V],
         "ams_tier_create": [I32, I64, I64, ctypes.POINTER(V)],
         "ams_tier_admit": [V, I64, I32, V, I64, ctypes.POINTER(I32), V, V, I32, ctypes.POINTER(I32), V],
         "ams_tier_touch": [V, I64],
@@ -196,6 +201,21 @@ def ams_match_gate_first(pool: int, q_emb, q_joints, nq: int, k: int, threshold:
     _check(lib.ams_match_gate_first(pool, _ptr(q_emb), _ptr(q_joints), nq, k, threshold, gate_radius,
                                     _ptr(out_index), _ptr(out_score), _ptr(out_hit), _stream(stream)),
            "ams_match_gate_first")
+
+
+def ams_match_auto(pool: int, q_emb, q_joints, nq: int, k: int, threshold: float, gate_radius: float,
+                   out_index, out_score, out_hit, stream=None) -> None:
+    _check(lib.ams_match_auto(pool, _ptr(q_emb), _ptr(q_joints), nq, k, threshold, gate_radius, _ptr(out_index),
+                              _ptr(out_score), _ptr(out_hit), _stream(stream)), "ams_match_auto")
+
+
+def ams_pool_last_route(pool: int):
+    r = ctypes.c_int32()
+    e, md, mg = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    _check(lib.ams_pool_last_route(pool, ctypes.byref(r), ctypes.byref(e), ctypes.byref(md), ctypes.byref(mg)),
+           "ams_pool_last_route")
+    return {"route": {-1: None, 0: "dense", 1: "gate_first"}[r.value], "est_eligible_per_query": e.value,
+            "est_ms_dense": md.value, "est_ms_gate_first": mg.value}
 
 
 def ams_merge_topk(in_score, in_index, G: int, nq: int, kin: int, k: int, threshold: float, out_index,
@@ -330,6 +350,10 @@ def ams_vstore_stats(store: int):
     return {"entries": a.value, "total_bytes": b.value, "arena_used": c.value}
 
 
+def ams_vstore_compact(store: int, stream=None) -> None:
+    _check(lib.ams_vstore_compact(store, _stream(stream)), "ams_vstore_compact")
+
+
 def ams_vstore_destroy(store: int) -> None:
     _check(lib.ams_vstore_destroy(store), "ams_vstore_destroy")
 
@@ -424,7 +448,7 @@ class Pool:
             out = (torch.empty(nq, k, dtype=torch.int64, device=dev),
                    torch.empty(nq, k, dtype=torch.float32, device=dev),
                    torch.empty(nq, dtype=torch.uint8, device=dev))
-        fn = ams_match_gate_first if gate_first else ams_match
+        fn = ams_match_auto if gate_first == "auto" else ams_match_gate_first if gate_first else ams_match
         fn(self.handle, q_emb, q_joints, nq, k, threshold, gate_radius, out[0], out[1], out[2], stream)
         return out
 

@@ -216,6 +216,7 @@ void free_peers(Pool& p) {
     p.x_err_host = nullptr;
   }
   p.peer_mode = false;
+  p.peers = ams::PeerTable{};
   p.x_s = nullptr;
   p.x_i = nullptr;
   p.x_flag = nullptr;
@@ -234,12 +235,16 @@ void free_all(Pool& p) {
   }
   if (p.copy_stream) cudaStreamDestroy(p.copy_stream);
   p.copy_stream = nullptr;
+  if (p.est_ready) cudaEventDestroy(p.est_ready);
+  if (p.est_host) cudaFreeHost(p.est_host);
+  p.est_ready = nullptr;
+  p.est_host = nullptr;
   void* ptrs[] = {p.scan_glist_s, p.scan_glist_i, p.emb, p.inv_norm, p.joints, p.q_stage, p.q_inv, p.q_joints,
                   p.q_joints_raw[0], p.q_joints_raw[1],
                   p.q_raw[0], p.q_raw[1], p.q_perm, p.bound, p.slots,
                   p.gf_cnt, p.gf_cand, p.snap_j, p.snap_id, p.snap_off, p.snap_aux,
                   p.part_s, p.part_i, p.shard_s, p.shard_i, p.gath_s, p.gath_i, p.stage_emb,
-                  p.stage_joints};
+                  p.stage_joints, p.est_dev};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   for (auto& e : p.ev_free) cudaEventDestroy(e);
@@ -389,6 +394,7 @@ ams_status_t ams_pool_create(const ams_pool_config_t* cfg, ams_pool_t* out) {
     p.gf_cap = std::max(256, 8 * c.max_k);
     ok = alloc((void**)&p.gf_cnt, (size_t)p.q_pad * 4) && alloc((void**)&p.gf_cand, (size_t)p.q_pad * p.gf_cap * 4);
   }
+  if (ok) ok = alloc((void**)&p.est_dev, 16);
   p.collective = c.world > 1 || c.nccl_id != nullptr;
   if (ok && p.collective)
     ok = alloc((void**)&p.gath_s, (size_t)c.world * c.max_queries * c.max_k * 4) &&
@@ -409,7 +415,9 @@ ams_status_t ams_pool_create(const ams_pool_config_t* cfg, ams_pool_t* out) {
       return AMS_ERR_CUDA;
     }
   }
-  bool sok = cudaStreamCreateWithFlags(&p.copy_stream, cudaStreamNonBlocking) == cudaSuccess;
+  bool sok = cudaStreamCreateWithFlags(&p.copy_stream, cudaStreamNonBlocking) == cudaSuccess &&
+             cudaEventCreateWithFlags(&p.est_ready, cudaEventDisableTiming) == cudaSuccess &&
+             cudaMallocHost((void**)&p.est_host, 16) == cudaSuccess;
   for (int b = 0; b < 2 && sok; ++b)
     sok = cudaEventCreateWithFlags(&p.staged[b], cudaEventDisableTiming) == cudaSuccess &&
           cudaEventCreateWithFlags(&p.consumed[b], cudaEventDisableTiming) == cudaSuccess;
@@ -489,10 +497,73 @@ ams_status_t ams_pool_append(ams_pool_t pool, const void* emb, const float* join
   return AMS_OK;
 }
 
+// ams_match_auto's route choice (host; SURVEY.md 8(f) f3 "select by measured pass-rate").
+// The expected number of eligible rows per query comes from the exact canonical gate over
+// a strided sample (<= 64 queries x <= 32768 rows, one tiny kernel): synchronously when
+// there is no estimate for this gate radius yet or the shard changed size by 2x, else
+// refreshed asynchronously every 64 calls (pinned D2H + event; adopted once complete).
+// Cost model (ms), constants from the round-1 measurements:
+//   dense      0.02 + max(2 nq L d / 1.40e15, L (2d + 4J + 4) / 6.5e12)  (sustained tensor / HBM)
+//   gate-first 0.03 + nq L / 2e13 (filter ALU) + ceil(nq/256) L 4 JP / 4e12 (joint reads per
+//              256-query block) + nq E 2 d / 2e12 (gathered rows of the E eligible per query)
+// gate-first is taken when it is cheaper and E <= bucket capacity / 2 (no overflow rescans).
+static ams_status_t auto_route(ams_pool_s* pool, const float* qj_src, int32_t nq, float g2, cudaStream_t s,
+                               bool* gate_first) {
+  Pool& p = pool->p;
+  *gate_first = false;
+  if (p.cfg.dtype != AMS_DTYPE_BF16 || std::isinf(g2) || p.local <= 0) {
+    p.last_route = 0;
+    return AMS_OK;
+  }
+  auto adopt = [&]() {
+    const double pairs = (double)p.est_rows * (double)p.est_queries;
+    const double rate = pairs > 0 ? (double)*p.est_host / pairs : 0.0;
+    p.est_elig = rate * (double)p.local;
+    p.est_valid = true;
+  };
+  if (p.est_pending) {
+    const cudaError_t q = cudaEventQuery(p.est_ready);
+    if (q == cudaSuccess) {
+      p.est_pending = false;
+      adopt();
+    } else if (q != cudaErrorNotReady) {
+      return fail(pool, AMS_ERR_CUDA);
+    } else {
+      cudaGetLastError();   // not-ready is not an error
+    }
+  }
+  const bool stale = !p.est_valid || p.est_g2 != g2 || p.local > 2 * p.est_L || 2 * p.local < p.est_L;
+  if (stale || (++p.est_calls % 64 == 0 && !p.est_pending)) {
+    int32_t rows = 0, qs = 0;
+    AMS_CUDA_TRY(ams::launch_gate_estimate(p, qj_src, nq, g2, p.est_dev, &rows, &qs, s));
+    AMS_CUDA_TRY(cudaMemcpyAsync(p.est_host, p.est_dev, 8, cudaMemcpyDeviceToHost, s));
+    p.est_rows = rows;
+    p.est_queries = qs;
+    p.est_g2 = g2;
+    p.est_L = p.local;
+    if (stale) {
+      AMS_CUDA_TRY(cudaStreamSynchronize(s));
+      p.est_pending = false;
+      adopt();
+    } else {
+      AMS_CUDA_TRY(cudaEventRecord(p.est_ready, s));
+      p.est_pending = true;
+    }
+  }
+  const double L = (double)p.local, d = p.cfg.dim, J = p.cfg.joint_dim, n = nq, E = p.est_elig;
+  const double dense = 0.02 + 1e3 * std::max(2.0 * n * L * d / 1.40e15, L * (2 * d + 4 * J + 4) / 6.5e12);
+  const double gf = 0.03 + 1e3 * (n * L / 2e13 + std::ceil(n / 256.0) * L * 4 * p.JP / 4e12 + n * E * 2 * d / 2e12);
+  p.last_est_ms[0] = dense;
+  p.last_est_ms[1] = gf;
+  *gate_first = E <= 0.5 * p.gf_cap && gf < dense;
+  p.last_route = *gate_first ? 1 : 0;
+  return AMS_OK;
+}
+
 static ams_status_t match_impl(ams_pool_t pool, const void* q_emb, const float* q_joints, int32_t nq, int32_t k,
                                float threshold, float gate_radius, int64_t* out_index, float* out_score,
-                               uint8_t* out_hit, void* stream, bool gate_first) {
-  NvtxRange nvtx(gate_first ? "ams_match_gate_first" : "ams_match");
+                               uint8_t* out_hit, void* stream, bool gate_first, bool auto_select = false) {
+  NvtxRange nvtx(auto_select ? "ams_match_auto" : gate_first ? "ams_match_gate_first" : "ams_match");
   if (pool == nullptr) return AMS_ERR_INVALID_ARGUMENT;
   Pool& p = pool->p;
   if (pool_status(pool) != AMS_OK) return p.broken_st;
@@ -523,8 +594,8 @@ static ams_status_t match_impl(ams_pool_t pool, const void* q_emb, const float* 
   const void* q_src = q_emb;
   const float* qj_src = q_joints;
   const bool host_q = !is_device_ptr(q_emb), host_j = !is_device_ptr(q_joints);
-  if ((host_q || host_j || (p.collective && p.peer_mode)) && capturing(s))
-    return AMS_ERR_UNSUPPORTED;   // pageable copies / the host epoch counter cannot be captured
+  if ((host_q || host_j || (p.collective && p.peer_mode) || auto_select) && capturing(s))
+    return AMS_ERR_UNSUPPORTED;   // pageable copies / the host epoch counter / the estimate sync cannot be captured
   int b = -1;
   if (host_q || host_j) {
     b = p.stage_buf;
@@ -541,6 +612,10 @@ static ams_status_t match_impl(ams_pool_t pool, const void* q_emb, const float* 
     }
     AMS_CUDA_TRY(cudaEventRecord(p.staged[b], p.copy_stream));
     AMS_CUDA_TRY(cudaStreamWaitEvent(s, p.staged[b], 0));
+  }
+  if (auto_select) {
+    const ams_status_t rs = auto_route(pool, qj_src, nq, a.g2, s, &gate_first);
+    if (rs != AMS_OK) return rs;
   }
   // Gated batches are staged in (joint 0, joint 1) order (the epilogue's warp-level gate
   // test then rejects most columns for all 32 queries of a warp at once).  The order is
@@ -681,6 +756,24 @@ ams_status_t ams_match_gate_first(ams_pool_t pool, const void* q_emb, const floa
                     true);
 }
 
+ams_status_t ams_match_auto(ams_pool_t pool, const void* q_emb, const float* q_joints, int32_t nq, int32_t k,
+                            float threshold, float gate_radius, int64_t* out_index, float* out_score, uint8_t* out_hit,
+                            void* stream) {
+  return match_impl(pool, q_emb, q_joints, nq, k, threshold, gate_radius, out_index, out_score, out_hit, stream,
+                    false, true);
+}
+
+ams_status_t ams_pool_last_route(ams_pool_t pool, int32_t* route, double* est_eligible_per_query,
+                                 double* est_ms_dense, double* est_ms_gate_first) {
+  if (pool == nullptr) return AMS_ERR_INVALID_ARGUMENT;
+  const Pool& p = pool->p;
+  if (route) *route = p.last_route;
+  if (est_eligible_per_query) *est_eligible_per_query = p.est_valid ? p.est_elig : -1.0;
+  if (est_ms_dense) *est_ms_dense = p.last_est_ms[0];
+  if (est_ms_gate_first) *est_ms_gate_first = p.last_est_ms[1];
+  return AMS_OK;
+}
+
 ams_status_t ams_merge_topk(const float* in_score, const int64_t* in_index, int32_t G, int32_t nq, int32_t kin,
                             int32_t k, float threshold, int64_t* out_index, float* out_score, uint8_t* out_hit,
                             void* stream) {
@@ -707,6 +800,15 @@ ams_status_t ams_pool_enable_peer_exchange(ams_pool_t pool) {
   if (p.peer_mode) return AMS_OK;
   if (p.cfg.capacity >= ((int64_t)1 << 31)) return AMS_ERR_UNSUPPORTED;   // int32 ids in the partial lists
   AMS_CUDA_TRY(cudaSetDevice(p.cfg.device));
+  ncclComm_t comm = static_cast<ncclComm_t>(p.nccl_comm);
+  // Consensus protocol: every rank takes part in both all-gathers whatever its local
+  // outcome, and every rank returns the same status (a rank that cannot allocate or map
+  // must not leave its peers waiting inside a collective).
+  //   block per rank = 3 IPC handles + int32 local status
+  const size_t hb = 3 * sizeof(cudaIpcMemHandle_t) + sizeof(int32_t);
+  std::vector<unsigned char> host((size_t)G * hb, 0);
+  unsigned char* mine = host.data() + (size_t)r * hb;
+  int32_t st_local = AMS_OK;
   const size_t slot = (size_t)2 * G * p.cfg.max_queries * p.cfg.max_k;
   bool ok = cudaMalloc((void**)&p.x_s, slot * 4) == cudaSuccess && cudaMalloc((void**)&p.x_i, slot * 8) == cudaSuccess &&
             cudaMalloc((void**)&p.x_flag, G * 8) == cudaSuccess && cudaMalloc((void**)&p.x_done, 4) == cudaSuccess &&
@@ -717,28 +819,27 @@ ams_status_t ams_pool_enable_peer_exchange(ams_pool_t pool) {
   if (ok) ok = cudaHostGetDevicePointer((void**)&err_dev, p.x_err_host, 0) == cudaSuccess;
   if (!ok) {
     cudaGetLastError();
-    free_peers(p);
-    return AMS_ERR_OUT_OF_MEMORY;
+    st_local = AMS_ERR_OUT_OF_MEMORY;
+  } else {
+    *p.x_err_host = 0;
+    if (cudaMemset(p.x_flag, 0, G * 8) != cudaSuccess || cudaMemset(p.x_done, 0, 4) != cudaSuccess ||
+        cudaMemset(p.x_barrier, 0, (size_t)G * 4) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+      cudaGetLastError();
+      st_local = AMS_ERR_CUDA;
+    }
   }
-  *p.x_err_host = 0;
-  AMS_CUDA_TRY(cudaMemset(p.x_flag, 0, G * 8));
-  AMS_CUDA_TRY(cudaMemset(p.x_done, 0, 4));
-  AMS_CUDA_TRY(cudaMemset(p.x_barrier, 0, (size_t)G * 4));
-  AMS_CUDA_TRY(cudaDeviceSynchronize());
-  // exchange the three IPC handles of every rank over the pool's NCCL communicator
-  const size_t hb = 3 * sizeof(cudaIpcMemHandle_t);
-  std::vector<unsigned char> host((size_t)G * hb);
-  cudaIpcMemHandle_t* mine = reinterpret_cast<cudaIpcMemHandle_t*>(host.data() + (size_t)r * hb);
-  if (cudaIpcGetMemHandle(&mine[0], p.x_s) != cudaSuccess || cudaIpcGetMemHandle(&mine[1], p.x_i) != cudaSuccess ||
-      cudaIpcGetMemHandle(&mine[2], p.x_flag) != cudaSuccess) {
+  cudaIpcMemHandle_t* h_mine = reinterpret_cast<cudaIpcMemHandle_t*>(mine);
+  if (st_local == AMS_OK &&
+      (cudaIpcGetMemHandle(&h_mine[0], p.x_s) != cudaSuccess || cudaIpcGetMemHandle(&h_mine[1], p.x_i) != cudaSuccess ||
+       cudaIpcGetMemHandle(&h_mine[2], p.x_flag) != cudaSuccess)) {
     cudaGetLastError();
-    free_peers(p);
-    return AMS_ERR_UNSUPPORTED;
+    st_local = AMS_ERR_UNSUPPORTED;
   }
+  memcpy(mine + 3 * sizeof(cudaIpcMemHandle_t), &st_local, sizeof st_local);
+  // all-gather 1: handles + local status
   void* dbuf = nullptr;
   AMS_CUDA_TRY(cudaMalloc(&dbuf, host.size()));
   AMS_CUDA_TRY(cudaMemcpy(static_cast<unsigned char*>(dbuf) + (size_t)r * hb, mine, hb, cudaMemcpyHostToDevice));
-  ncclComm_t comm = static_cast<ncclComm_t>(p.nccl_comm);
   if (ncclAllGather(static_cast<unsigned char*>(dbuf) + (size_t)r * hb, dbuf, hb, ncclChar, comm, nullptr) !=
       ncclSuccess) {
     cudaFree(dbuf);
@@ -746,7 +847,17 @@ ams_status_t ams_pool_enable_peer_exchange(ams_pool_t pool) {
   }
   AMS_CUDA_TRY(cudaDeviceSynchronize());
   AMS_CUDA_TRY(cudaMemcpy(host.data(), dbuf, host.size(), cudaMemcpyDeviceToHost));
-  cudaFree(dbuf);
+  int32_t st_all = AMS_OK;
+  for (int g = 0; g < G; ++g) {
+    int32_t sg;
+    memcpy(&sg, host.data() + (size_t)g * hb + 3 * sizeof(cudaIpcMemHandle_t), sizeof sg);
+    if (sg != AMS_OK && st_all == AMS_OK) st_all = sg;
+  }
+  if (st_all != AMS_OK) {
+    cudaFree(dbuf);
+    free_peers(p);
+    return static_cast<ams_status_t>(st_all == AMS_ERR_CUDA ? AMS_ERR_UNSUPPORTED : st_all);
+  }
   ams::PeerTable pt{};
   pt.G = G;
   pt.rank = r;
@@ -755,6 +866,7 @@ ams_status_t ams_pool_enable_peer_exchange(ams_pool_t pool) {
   pt.err = err_dev;
   pt.timeout_ns = ams::kPeerTimeoutNs;
   p.peer_mode = true;   // from here free_peers closes whatever was opened
+  int32_t mapped = 1;
   for (int g = 0; g < G; ++g) {
     if (g == r) {
       pt.s[g] = p.x_s;
@@ -764,25 +876,33 @@ ams_status_t ams_pool_enable_peer_exchange(ams_pool_t pool) {
     }
     const cudaIpcMemHandle_t* h = reinterpret_cast<const cudaIpcMemHandle_t*>(host.data() + (size_t)g * hb);
     void *a0 = nullptr, *a1 = nullptr, *a2 = nullptr;
-    if (cudaIpcOpenMemHandle(&a0, h[0], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
-        cudaIpcOpenMemHandle(&a1, h[1], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
-        cudaIpcOpenMemHandle(&a2, h[2], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+    if (cudaIpcOpenMemHandle(&a0, h[0], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess) pt.s[g] = static_cast<float*>(a0);
+    if (cudaIpcOpenMemHandle(&a1, h[1], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess) pt.i[g] = static_cast<int64_t*>(a1);
+    if (cudaIpcOpenMemHandle(&a2, h[2], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess)
+      pt.flag[g] = static_cast<unsigned long long*>(a2);
+    if (!pt.s[g] || !pt.i[g] || !pt.flag[g]) {
       cudaGetLastError();
-      p.peers = pt;
-      free_peers(p);
-      return AMS_ERR_UNSUPPORTED;
+      mapped = 0;
     }
-    pt.s[g] = static_cast<float*>(a0);
-    pt.i[g] = static_cast<int64_t*>(a1);
-    pt.flag[g] = static_cast<unsigned long long*>(a2);
-    p.peers = pt;
   }
   p.peers = pt;
   p.epoch = 0;
-  // every rank has mapped every peer before anyone writes into a peer buffer
-  if (ncclAllGather(p.x_barrier + r, p.x_barrier, 1, ncclUint32, comm, nullptr) != ncclSuccess)
+  // all-gather 2 (also the barrier: no rank writes into a peer before every rank has
+  // mapped every peer): every rank's mapping outcome
+  AMS_CUDA_TRY(cudaMemcpy(p.x_barrier + r, &mapped, 4, cudaMemcpyHostToDevice));
+  if (ncclAllGather(p.x_barrier + r, p.x_barrier, 1, ncclUint32, comm, nullptr) != ncclSuccess) {
+    cudaFree(dbuf);
     return fail(pool, AMS_ERR_NCCL);
+  }
   AMS_CUDA_TRY(cudaDeviceSynchronize());
+  cudaFree(dbuf);
+  std::vector<uint32_t> all(G);
+  AMS_CUDA_TRY(cudaMemcpy(all.data(), p.x_barrier, (size_t)G * 4, cudaMemcpyDeviceToHost));
+  for (int g = 0; g < G; ++g)
+    if (all[g] != 1) {
+      free_peers(p);
+      return AMS_ERR_UNSUPPORTED;
+    }
   return AMS_OK;
 }
 

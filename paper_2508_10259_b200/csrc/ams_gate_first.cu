@@ -484,7 +484,54 @@ cudaError_t launch_gf_jp(Pool& p, const MatchArgs& a, int32_t cap, float* out_s,
   return cudaGetLastError();
 }
 
+// Pass-rate estimate for ams_match_auto: exact canonical gate over a strided sample of
+// up to kEstQueries queries (raw [nq][J] joints) x up to kEstRows local rows; out[0] +=
+// eligible sampled pairs.  Thread per sampled row, loop over the sampled queries.
+__global__ void gate_estimate_kernel(const float* __restrict__ pool_joints, int32_t JP, int64_t L, int64_t row_step,
+                                     int32_t n_rows, const float* __restrict__ qj, int32_t J, int32_t q_step,
+                                     int32_t n_q, float g2, unsigned long long* __restrict__ out) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned int c = 0;
+  if (r < n_rows) {
+    const int64_t l = (int64_t)r * row_step;
+    float pj[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) pj[t] = t < J ? pool_joints[joint_offset(l, t, JP)] : 0.0f;
+    for (int i = 0; i < n_q; ++i) {
+      const float* q = qj + (int64_t)i * q_step * J;
+      float ds = 0.0f;
+#pragma unroll
+      for (int t = 0; t < 16; ++t)
+        if (t < J) {
+          const float diff = q[t] - pj[t];
+          ds = fmaf(diff, diff, ds);
+        }
+      c += ds <= g2 ? 1u : 0u;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, (unsigned long long)c);
+}
+
 }  // namespace
+
+cudaError_t launch_gate_estimate(Pool& p, const float* qj_raw, int32_t nq, float g2, unsigned long long* out,
+                                 int32_t* rows_sampled, int32_t* queries_sampled, cudaStream_t s) {
+  const int64_t L = p.local;
+  const int64_t row_step = std::max<int64_t>(1, (L + kEstRows - 1) / kEstRows);
+  const int32_t n_rows = (int32_t)((L + row_step - 1) / row_step);
+  const int32_t q_step = std::max<int32_t>(1, (nq + kEstQueries - 1) / kEstQueries);
+  const int32_t n_q = (nq + q_step - 1) / q_step;
+  *rows_sampled = n_rows;
+  *queries_sampled = n_q;
+  cudaError_t e = cudaMemsetAsync(out, 0, 8, s);
+  if (e != cudaSuccess || n_rows == 0) return e;
+  gate_estimate_kernel<<<(n_rows + 255) / 256, 256, 0, s>>>(p.joints, p.JP, L, row_step, n_rows, qj_raw,
+                                                            p.cfg.joint_dim, q_step, n_q, g2, out);
+  ++p.launches;
+  return cudaGetLastError();
+}
 
 cudaError_t launch_gate_first(Pool& p, const MatchArgs& a, float* out_s, int64_t* out_i, uint8_t* out_hit,
                               bool sorted, cudaStream_t s) {

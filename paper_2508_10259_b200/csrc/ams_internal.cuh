@@ -160,6 +160,19 @@ struct Pool {
   int64_t* x_i = nullptr;
   unsigned long long* x_flag = nullptr;
 
+  // ams_match_auto: cached estimate of eligible rows per query (refreshed asynchronously)
+  unsigned long long* est_dev = nullptr;     // [1] sampled eligible pairs
+  unsigned long long* est_host = nullptr;    // pinned copy of est_dev
+  cudaEvent_t est_ready = nullptr;           // recorded after the D2H of a refresh
+  bool est_pending = false, est_valid = false;
+  float est_g2 = 0.0f;                       // gate of the cached estimate
+  int64_t est_L = 0;                         // local rows when it was taken
+  int32_t est_rows = 0, est_queries = 0;     // sample sizes of the pending / adopted refresh
+  double est_elig = 0.0;                     // eligible rows per query (local shard)
+  int64_t est_calls = 0;
+  int32_t last_route = -1;                   // 0 dense, 1 gate-first
+  double last_est_ms[2] = {0.0, 0.0};        // cost model of the last auto call (dense, gate-first)
+
   // instrumentation
   bool profiling = false;
   std::vector<cudaEvent_t> ev_free;
@@ -225,5 +238,11 @@ cudaError_t launch_exchange_wait(int KT, const PeerTable& pt, int32_t nq, int32_
 cudaError_t launch_to_partials(const float* s, const int64_t* i, int32_t nq, int32_t k, int32_t KT, float* ps,
                                int32_t* pi, cudaStream_t st);
 int pick_KT(int k);
+// ams_match_auto's pass-rate estimate: out[0] = eligible pairs among a strided sample of
+// <= kEstQueries of the caller's raw query joints [nq][J] x <= kEstRows local rows
+constexpr int kEstQueries = 64;
+constexpr int64_t kEstRows = 32768;
+cudaError_t launch_gate_estimate(Pool& p, const float* qj_raw, int32_t nq, float g2, unsigned long long* out,
+                                 int32_t* rows_sampled, int32_t* queries_sampled, cudaStream_t s);
 
 }  // namespace ams

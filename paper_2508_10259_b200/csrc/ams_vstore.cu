@@ -13,9 +13,15 @@
 //
 // Layout: open-addressing table (power-of-two capacity, linear probing) of
 // {key = id | 2^63 (0 = empty, 1 = tombstone), refcount, arena offset, length}; bytes in
-// an append-only device arena (space of removed entries is not reused in this version).
-// Batched operations, one thread (or warp for byte copies / compares) per action, ordered
-// by kernel boundaries on the caller's stream.
+// one contiguous device arena, allocated by bumping a top pointer.  Removed entries leave
+// holes (and tombstones); `compact` reclaims both ("any action whose reference count drops
+// to zero is removed"): the live entries' bytes are packed to the front of
+// the arena in table-slot order (exclusive scan of the live lengths) through a scratch
+// buffer, and the live keys are re-inserted into a fresh table (no tombstones).  It runs
+// automatically before an intern whose bytes might not fit behind the top (host-side upper
+// bound of the top) or that might push the table past 3/4 load, and on request
+// (ams_vstore_compact).  Batched operations, one thread (or warp for byte copies /
+// compares) per action, ordered by kernel boundaries on the caller's stream.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -185,6 +191,92 @@ __global__ void resolve_kernel(Table t, const uint64_t* __restrict__ ids, int32_
   if (out_ref) out_ref[i] = s < 0 ? 0 : t.ref[s];
 }
 
+// ---- compaction ----------------------------------------------------------------------
+__device__ __forceinline__ bool live_slot(const Table& t, uint64_t s) {
+  return t.key[s] >= kTag && t.ref[s] > 0 && t.len[s] >= 0;
+}
+
+constexpr int kScanBlock = 1024;
+
+// per-slot live length -> ex[s]; per-block sums -> bsum[block]
+__global__ void __launch_bounds__(kScanBlock) compact_scan_kernel(Table t, long long* __restrict__ ex,
+                                                                   long long* __restrict__ bsum) {
+  __shared__ long long sh[kScanBlock];
+  const uint64_t s = (uint64_t)blockIdx.x * kScanBlock + threadIdx.x;
+  const long long v = (s <= t.mask && live_slot(t, s)) ? t.len[s] : 0;
+  sh[threadIdx.x] = v;
+  __syncthreads();
+  for (int o = 1; o < kScanBlock; o <<= 1) {   // Hillis-Steele inclusive scan
+    const long long a = threadIdx.x >= o ? sh[threadIdx.x - o] : 0;
+    __syncthreads();
+    sh[threadIdx.x] += a;
+    __syncthreads();
+  }
+  if (s <= t.mask) ex[s] = sh[threadIdx.x] - v;
+  if (threadIdx.x == kScanBlock - 1) bsum[blockIdx.x] = sh[threadIdx.x];
+}
+
+// one block: exclusive scan of the block sums in place; bsum[nb] = total live bytes
+__global__ void __launch_bounds__(kScanBlock) compact_bsum_kernel(long long* __restrict__ bsum, int nb) {
+  __shared__ long long carry;
+  __shared__ long long sh[kScanBlock];
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < nb; base += kScanBlock) {
+    const int i = base + threadIdx.x;
+    const long long v = i < nb ? bsum[i] : 0;
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int o = 1; o < kScanBlock; o <<= 1) {
+      const long long a = threadIdx.x >= o ? sh[threadIdx.x - o] : 0;
+      __syncthreads();
+      sh[threadIdx.x] += a;
+      __syncthreads();
+    }
+    if (i < nb) bsum[i] = carry + sh[threadIdx.x] - v;
+    __syncthreads();
+    if (threadIdx.x == kScanBlock - 1) carry += sh[threadIdx.x];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) bsum[nb] = carry;
+}
+
+// warp per slot: live bytes -> scratch at their packed offset; the entry is re-inserted
+// into the fresh table `nt` with its new offset
+__global__ void compact_move_kernel(Table t, Table nt, const long long* __restrict__ ex,
+                                    const long long* __restrict__ bsum, const uint8_t* __restrict__ arena,
+                                    uint8_t* __restrict__ scratch, unsigned long long* __restrict__ n_live) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t s = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (s > t.mask || !live_slot(t, s)) return;
+  const long long off = ex[s] + bsum[s / kScanBlock];
+  const long long len = t.len[s];
+  const uint8_t* src = arena + t.off[s];
+  for (long long b = lane; b < len; b += 32) scratch[off + b] = src[b];
+  if (lane == 0) {
+    bool created = false;
+    const uint64_t id = (uint64_t)t.key[s] & ~kTag;
+    const int64_t ns = find_or_insert(nt, id, &created);   // fresh table, no tombstones: one slot per live key
+    if (ns < 0) return;
+    nt.ref[ns] = t.ref[s];
+    nt.off[ns] = off;
+    nt.len[ns] = len;
+    atomicAdd(n_live, 1ull);
+  }
+}
+
+// scratch -> arena (bytes [0, total)); the new top
+__global__ void compact_copy_back_kernel(const uint8_t* __restrict__ scratch, uint8_t* __restrict__ arena,
+                                         const long long* __restrict__ total_p, unsigned long long* __restrict__ top) {
+  const long long total = *total_p;
+  const long long n16 = total / 16;
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = tid; i < (uint64_t)n16; i += stride)
+    reinterpret_cast<uint4*>(arena)[i] = reinterpret_cast<const uint4*>(scratch)[i];
+  for (uint64_t i = (uint64_t)n16 * 16 + tid; i < (uint64_t)total; i += stride) arena[i] = scratch[i];
+  if (tid == 0) *top = (unsigned long long)total;
+}
+
 __global__ void stats_kernel(Table t, unsigned long long* __restrict__ out) {   // out[0] entries, out[1] bytes
   for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s <= t.mask; s += (uint64_t)gridDim.x * blockDim.x) {
     const unsigned long long k = t.key[s];
@@ -202,6 +294,13 @@ struct ams_vstore_s {
   int32_t device = 0;
   int64_t cap_batch = 0, cap_bytes_batch = 0, arena_cap = 0;
   ams::vs::Table t{};
+  ams::vs::Table t2{};            // spare table: compaction re-inserts the live keys here, then swaps
+  long long* scan_ex = nullptr;   // [table capacity] packed offsets (compaction)
+  long long* scan_bs = nullptr;   // [table capacity / 1024 + 1] block sums, then the total
+  // host-side upper bounds since the last compaction (no synchronisation on the fast path):
+  int64_t top_bound = 0;          // arena top <= this (every interned byte counted)
+  int64_t slots_bound = 0;        // occupied table slots (live + tombstones) <= this
+  int64_t compactions = 0;
   uint8_t* arena = nullptr;
   unsigned long long* arena_top = nullptr;
   unsigned long long* stats = nullptr;
@@ -219,8 +318,8 @@ struct ams_vstore_s {
 namespace {
 void vstore_free(ams_vstore_s* s) {
   if (!s) return;
-  void* ptrs[] = {s->t.key, s->t.ref, s->t.off, s->t.len, s->arena, s->arena_top, s->stats, s->ids, s->slot_of,
-                  s->d_offsets, s->stage};
+  void* ptrs[] = {s->t.key, s->t.ref, s->t.off, s->t.len, s->t2.key, s->t2.ref, s->t2.off, s->t2.len, s->scan_ex,
+                  s->scan_bs, s->arena, s->arena_top, s->stats, s->ids, s->slot_of, s->d_offsets, s->stage};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (s->h_pinned) cudaFreeHost(s->h_pinned);
@@ -228,6 +327,41 @@ void vstore_free(ams_vstore_s* s) {
   if (s->hasher) ams_hasher_destroy(s->hasher);
   delete s;
 }
+// Stream-ordered compaction (see the header comment); synchronises once at the end to
+// re-seed the host-side bounds with the exact top and live count.
+ams_status_t compact(ams_vstore_s* s, cudaStream_t st) {
+  using namespace ams::vs;
+  const uint64_t cap = s->t.mask + 1;
+  const int nb = (int)((cap + kScanBlock - 1) / kScanBlock);
+  uint8_t* scratch = nullptr;
+  bool ok = cudaMallocAsync((void**)&scratch, (size_t)std::max<int64_t>(s->arena_cap, 16), st) == cudaSuccess &&
+            cudaMemsetAsync(s->t2.key, 0, cap * 8, st) == cudaSuccess &&
+            cudaMemsetAsync(s->t2.ref, 0, cap * 4, st) == cudaSuccess &&
+            cudaMemsetAsync(s->stats, 0, 16, st) == cudaSuccess;
+  if (ok) {
+    compact_scan_kernel<<<nb, kScanBlock, 0, st>>>(s->t, s->scan_ex, s->scan_bs);
+    compact_bsum_kernel<<<1, kScanBlock, 0, st>>>(s->scan_bs, nb);
+    compact_move_kernel<<<(unsigned)((cap + 7) / 8), 256, 0, st>>>(s->t, s->t2, s->scan_ex, s->scan_bs, s->arena,
+                                                                  scratch, s->stats);
+    compact_copy_back_kernel<<<148 * 4, 256, 0, st>>>(scratch, s->arena, s->scan_bs + nb, s->arena_top);
+    ok = cudaGetLastError() == cudaSuccess && cudaFreeAsync(scratch, st) == cudaSuccess;
+  }
+  unsigned long long top = 0, live = 0;
+  ok = ok && cudaMemcpyAsync(&top, s->arena_top, 8, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
+       cudaMemcpyAsync(&live, s->stats, 8, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
+       cudaStreamSynchronize(st) == cudaSuccess;
+  if (!ok) {
+    cudaGetLastError();
+    s->broken = true;
+    return AMS_ERR_CUDA;
+  }
+  std::swap(s->t, s->t2);
+  s->top_bound = (int64_t)top;
+  s->slots_bound = (int64_t)live;
+  ++s->compactions;
+  return AMS_OK;
+}
+
 bool is_dev(const void* p) {
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -260,8 +394,13 @@ ams_status_t ams_vstore_create(int32_t device, int64_t max_actions, int64_t aren
   uint64_t cap = 1024;
   while (cap < (uint64_t)max_actions * 2) cap <<= 1;
   s->t.mask = cap - 1;
+  s->t2.mask = cap - 1;
   bool ok = cudaMalloc(&s->t.key, cap * 8) == cudaSuccess && cudaMalloc(&s->t.ref, cap * 4) == cudaSuccess &&
             cudaMalloc(&s->t.off, cap * 8) == cudaSuccess && cudaMalloc(&s->t.len, cap * 8) == cudaSuccess &&
+            cudaMalloc(&s->t2.key, cap * 8) == cudaSuccess && cudaMalloc(&s->t2.ref, cap * 4) == cudaSuccess &&
+            cudaMalloc(&s->t2.off, cap * 8) == cudaSuccess && cudaMalloc(&s->t2.len, cap * 8) == cudaSuccess &&
+            cudaMalloc(&s->scan_ex, cap * 8) == cudaSuccess &&
+            cudaMalloc(&s->scan_bs, (cap / 1024 + 2) * 8) == cudaSuccess &&
             cudaMalloc(&s->arena, std::max<int64_t>(arena_bytes, 16)) == cudaSuccess &&
             cudaMalloc(&s->arena_top, 8) == cudaSuccess && cudaMalloc(&s->stats, 16) == cudaSuccess &&
             cudaMalloc(&s->ids, (size_t)max_batch * 8) == cudaSuccess &&
@@ -306,6 +445,15 @@ ams_status_t ams_vstore_intern(ams_vstore_t s, const uint8_t* data, const int64_
     const ams_status_t hs = ams_hash_actions(s->hasher, data, offsets, n, out_ids, stream);
     if (hs != AMS_OK) return hs;
   }
+  // reclaim removed entries first if this batch might not fit behind the arena top or
+  // might push the table past 3/4 load (host-side upper bounds; exact after compaction)
+  const int64_t slot_cap = (int64_t)(s->t.mask + 1);
+  if (s->top_bound + total > s->arena_cap || s->slots_bound + n > slot_cap / 4 * 3) {
+    const ams_status_t cs = compact(s, st);
+    if (cs != AMS_OK) return cs;
+  }
+  s->top_bound += total;
+  s->slots_bound += n;
   // device copies of the bytes (rebased) and offsets
   if (s->pending && cudaEventSynchronize(s->done) != cudaSuccess) return AMS_ERR_CUDA;
   for (int32_t i = 0; i <= n; ++i) s->h_pinned[i] = offsets[i] - offsets[0];
@@ -357,6 +505,13 @@ ams_status_t ams_vstore_resolve(ams_vstore_t s, const uint64_t* ids, int32_t n, 
     return AMS_ERR_CUDA;
   }
   return AMS_OK;
+}
+
+ams_status_t ams_vstore_compact(ams_vstore_t s, void* stream) {
+  if (s == nullptr) return AMS_ERR_INVALID_ARGUMENT;
+  if (s->broken) return AMS_ERR_CUDA;
+  if (cudaSetDevice(s->device) != cudaSuccess) return AMS_ERR_CUDA;
+  return compact(s, static_cast<cudaStream_t>(stream));
 }
 
 ams_status_t ams_vstore_arena(ams_vstore_t s, const uint8_t** arena) {

@@ -26,13 +26,17 @@ def bootstrap_nccl_id(group=None) -> Optional[bytes]:
 
 
 def create_pool(dim, joint_dim, capacity, max_queries, max_k, dtype="bf16", shard_block=0, group=None,
-                device: Optional[int] = None) -> Pool:
-    """Collective: every rank of the torch.distributed group creates its shard."""
+                device: Optional[int] = None, force_collective: bool = False) -> Pool:
+    """Collective: every rank of the torch.distributed group creates its shard.
+    force_collective (world 1 only): build a 1-rank NCCL communicator so the world > 1 code
+    path (shard merge, all-gather, final merge, peer exchange) runs on one GPU."""
     import torch
     import torch.distributed as dist
     rank, world = (dist.get_rank(group), dist.get_world_size(group)) if dist.is_initialized() else (0, 1)
     dev = torch.cuda.current_device() if device is None else device
     nid = bootstrap_nccl_id(group)
+    if nid is None and force_collective:
+        nid = ams_get_nccl_unique_id()
     return Pool(dim, joint_dim, capacity, max_queries, max_k, dtype=dtype, device=dev, rank=rank, world=world,
                 nccl_id=nid, shard_block=shard_block)
 

@@ -13,7 +13,8 @@ def test_bench_help_lists_the_contract_flags():
     out = subprocess.run([sys.executable, "bench.py", "--help"], cwd=ROOT, capture_output=True, text=True,
                          timeout=120)
     assert out.returncode == 0
-    for flag in ("--gpus", "--steps", "--warmup", "--impl", "--workload", "--kernel-policy"):
+    for flag in ("--gpus", "--steps", "--warmup", "--impl", "--workload", "--kernel-policy", "--no-c4",
+                 "--force-collective", "--no-peer", "--no-ungated"):
         assert flag in out.stdout
 
 

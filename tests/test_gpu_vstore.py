@@ -127,3 +127,62 @@ def test_collision_and_unknown_and_full(ams):
     assert status3.tolist() == [FULL]
     assert ams.ams_vstore_stats(st)["entries"] == 1
     ams.ams_vstore_destroy(st)
+
+
+def _check_against_oracle(ams, st, orc, ids_all, tag):
+    off, ln, rc = gpu_resolve(ams, st, ids_all)
+    for i, o, l, r in zip(ids_all, off, ln, rc):
+        assert r == orc.refcount(i), (tag, i)
+        b = orc.resolve(i)
+        assert (l == -1) == (b is None), (tag, i)
+        if b is not None:
+            assert l == len(b) and arena_slice(ams, st, o, l) == b, (tag, i)
+
+
+@pytest.mark.parametrize("device_data", [False, True])
+def test_churn_reclaims_arena_and_table(ams, device_data):
+    """PAPER.md:583 "Any action whose reference count drops to zero is removed": 100 rounds
+    of interns and releases through an arena (and table) far smaller than the bytes (and
+    keys) interned over time.  Removed entries' space is reclaimed by compaction, so the
+    arena top stays bounded; every live entry keeps its refcount and bytes, op by op
+    against the oracle store (oracle/vstore.py)."""
+    rng = np.random.Generator(np.random.PCG64(77 + device_data))
+    arena = 256 << 10
+    st = ams.ams_vstore_create(0, 512, arena, 64, 1 << 20)   # table: 1024 slots
+    orc = VirtualActionStore()
+    live = []
+    interned_bytes = interned_keys = 0
+    for step in range(100):
+        fresh = [rng.integers(0, 256, rng.integers(0, 2000), dtype=np.uint8).tobytes()
+                 for _ in range(rng.integers(1, 40))]
+        again = [orc.resolve(i) for i in rng.choice(live, min(len(live), 8), replace=False)] if live else []
+        batch = fresh + again
+        ids, status = gpu_intern(ams, st, batch, device_data=device_data)
+        assert (status != FULL).all(), step
+        for a, i in zip(batch, ids):
+            oi, _ = orc.intern(a)
+            assert int(i) == oi
+        interned_bytes += sum(len(a) for a in fresh)
+        interned_keys += len(fresh)
+        live += [int(i) for i in ids]
+        rng.shuffle(live)
+        keep = max(0, len(live) - rng.integers(len(live) // 2, len(live) + 1))
+        rel, live = live[keep:], live[:keep]   # release most references: the live set stays small
+        if rel:
+            t = torch.from_numpy(np.array(rel, np.uint64).view(np.int64)).cuda()
+            rem = torch.empty(len(rel), dtype=torch.int64, device="cuda")
+            ams.ams_vstore_release(st, t, len(rel), rem)
+            torch.cuda.synchronize()
+            for i in rel:
+                orc.release(i)
+        stats = ams.ams_vstore_stats(st)
+        assert stats["entries"] == len(orc.entries) and stats["total_bytes"] == orc.total_bytes, step
+        assert stats["arena_used"] <= arena, step
+        if step % 10 == 9:
+            _check_against_oracle(ams, st, orc, sorted(set(live) | set(rel)), step)
+    assert interned_bytes > 4 * arena and interned_keys > 2 * 1024   # the churn did overflow both
+    ams.ams_vstore_compact(st)
+    stats = ams.ams_vstore_stats(st)
+    assert stats["arena_used"] == orc.total_bytes == stats["total_bytes"]   # no holes after compaction
+    _check_against_oracle(ams, st, orc, sorted(set(live)), "final")
+    ams.ams_vstore_destroy(st)
