@@ -70,6 +70,8 @@ class ClockSampler:
         self.rows = []   # (wall time, fields)
         self.proc = None
         self.th = None
+        self.pending = []
+        self.stopped = False
 
     def start(self):
         try:
@@ -102,17 +104,24 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(rows),
                 "power_w_median": statistics.median(pw) if pw else None}
 
+    def _window_rows(self, t0: float, t1: float):
+        inside = [r for t, r in self.rows if t0 <= t <= t1 + 0.1]
+        if not inside:   # a leg shorter than the sampling period: the first sample after it
+            inside = [r for t, r in self.rows if t > t1][:1]
+        return inside
+
     def window(self, t0: float, t1: float):
-        """Samples taken while [t0, t1] ran (plus the one sample straddling each end: a
-        sub-100-ms leg still gets a reading)."""
+        """Summary of the samples taken while [t0, t1] ran (at least the first sample after
+        it, so a sub-100-ms leg still gets a reading).  Filled in when the sampler stops
+        (the returned dict is updated in place), so late samples are not missed."""
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        rows = list(self.rows)
-        inside = [r for t, r in rows if t0 <= t <= t1 + 0.1]
-        if not inside:
-            after = [r for t, r in rows if t > t1]
-            inside = after[:1]
-        return self.summarise(inside)
+        out = {"window_s": round(t1 - t0, 4)}
+        if self.stopped:
+            out.update(self.summarise(self._window_rows(t0, t1)))
+        else:
+            self.pending.append((t0, t1, out))
+        return out
 
     def stop(self):
         if self.proc is None:
@@ -125,6 +134,10 @@ class ClockSampler:
             self.proc.kill()
         if self.th:
             self.th.join(timeout=2)
+        self.stopped = True
+        for t0, t1, out in self.pending:
+            out.update(self.summarise(self._window_rows(t0, t1)))
+        self.pending = []
         return self.summarise([r for _, r in self.rows])
 
 
@@ -562,9 +575,10 @@ def main():
         for _ in range(5):
             fn()
         torch.cuda.synchronize()
+        w_ms, _ = timed(fn, 5)
         ams.ams_pool_read_profile(pool.handle)
         ams.ams_pool_set_profiling(pool.handle, True)
-        reps = max(20, 5 * args.steps)
+        reps = max(20, 5 * args.steps, int(500.0 / max(w_ms / 5, 1e-3)))   # >= ~0.5 s: several clock samples
         ms, win = timed(fn, reps)
         ams.ams_pool_set_profiling(pool.handle, False)
         s_ms = ms / reps
@@ -696,6 +710,27 @@ def main():
                           "clocks": clk.window(*win)}
         variant = {"name": "ams_match_gate_first (SURVEY 8(f) f3; exact, gate evaluated first)", **res}
 
+    # ------------------------------------------------------------------ route selection (f3 auto)
+    auto = None
+    if not args.no_variant and not args.gate_first:
+        res = {}
+        for label, nq in (("full_batch", cfg.Q), ("scan_64", min(64, cfg.Q))):
+            qv, qjv = q[:nq].contiguous(), qj[:nq].contiguous()
+            for _ in range(3):
+                step(qv, qjv, nq, ams.ams_match_auto)
+            torch.cuda.synchronize()
+            reps = max(5, args.steps)
+            a_ms, win = timed(lambda: step(qv, qjv, nq, ams.ams_match_auto), reps)
+            r = ams.ams_pool_last_route(pool.handle)
+            m_loc = cfg.M / world
+            res[label] = {"queries": nq, "ms_per_call": a_ms / reps, "value": nq / (a_ms / reps / 1e3),
+                          "unit": "queries/s", "route": r["route"],
+                          "est_eligible_rows_per_query": r["est_eligible_per_query"],
+                          "est_pass_rate": (r["est_eligible_per_query"] / m_loc) if r["est_eligible_per_query"] >= 0
+                          else None, "cost_model_ms": {"dense": r["est_ms_dense"], "gate_first": r["est_ms_gate_first"]},
+                          "clocks": clk.window(*win)}
+        auto = {"name": "ams_match_auto (SURVEY 8(f) f3: route by sampled pass-rate + cost model)", **res}
+
     # ------------------------------------------------------------------ e2e (host buffers)
     e2e = None
     if not args.no_e2e:
@@ -811,7 +846,7 @@ def main():
                 "pool_scan_gbps_per_gpu": (bytes_step / world) / (t_ms / args.steps / 1e3) / 1e9,
                 "collective_path": bool(world > 1 or args.force_collective),
                 "roofline": roofline, "outputs_sha256": out_sha, "ungated": ungated, "scan": scan,
-                "gate_first_variant": variant, "e2e": e2e, "peer_exchange": peer, "c4": c4, "cpu_baseline": cpu,
+                "gate_first_variant": variant, "auto_route": auto, "e2e": e2e, "peer_exchange": peer, "c4": c4, "cpu_baseline": cpu,
                 "clocks": clocks, "clocks_whole_run": clocks_all,
                 "gpu_launches": launches, "plan": plan, "hit_rate": hit_rate, "path": "ams_match_gate_first"
                 if args.gate_first else "ams_match (dense tcgen05)",

@@ -24,8 +24,8 @@ def T(a):
 
 
 @pytest.mark.parametrize("name,M,Q,gamma,route", [
-    ("c3", 30011, 300, 0.3, "gate_first"),    # R14 gate: ~0-1 eligible rows per query
-    ("c3", 30011, 64, 0.3, "gate_first"),
+    ("c3", 120011, 300, 0.3, "gate_first"),   # R14 gate: ~0-1 eligible rows per query
+    ("c3", 120011, 64, 0.3, "gate_first"),
     ("c2", 40000, 257, 3.5, "dense"),         # J = 7, gamma 3.5: ~8 % of rows eligible -> buckets overflow
     ("c2", 40000, 64, INF, "dense"),          # ungated: always dense
 ])
@@ -50,7 +50,7 @@ def test_auto_route_and_parity(ams, name, M, Q, gamma, route):
 
 
 def test_auto_estimate_refreshes_on_gamma_change(ams):
-    cfg = ams_gen.small_variant("c2", 40000, 128)
+    cfg = ams_gen.small_variant("c2", 120011, 128)
     w = ams_gen.generate_host(cfg)
     with ams.Pool(cfg.d, cfg.J, cfg.M, cfg.Q, cfg.k) as pool:
         pool.append(T(w.emb), T(w.joints))
@@ -64,7 +64,7 @@ def test_auto_estimate_refreshes_on_gamma_change(ams):
 
 def test_auto_many_calls_async_refresh(ams):
     """> 64 calls: the asynchronous refresh path runs and keeps choosing correctly."""
-    cfg = ams_gen.small_variant("c3", 20000, 96)
+    cfg = ams_gen.small_variant("c3", 120011, 96)
     w = ams_gen.generate_host(cfg)
     orc = oracle.match(w.emb, w.joints, w.q_emb, w.q_joints, cfg.k, cfg.theta, cfg.gamma, mode="B")
     with ams.Pool(cfg.d, cfg.J, cfg.M, cfg.Q, cfg.k) as pool:
