@@ -269,6 +269,14 @@ ams_status_t ams_hasher_create(int32_t device, int64_t max_inputs, int64_t max_b
 ams_status_t ams_hash_actions(ams_hasher_t hasher, const uint8_t* data, const int64_t* offsets,
                               int32_t n_inputs, uint64_t* out_hash, void* stream);
 
+/* Segments of the last ams_hash_actions call, and how many of them phase 1 hashed on the
+ * tensor cores: full segments starting 16-B aligned, when s is a multiple of 128 and
+ * <= 8192 -- each segment hash is then an exact u8 x u8 -> s32 contraction of its bytes
+ * with the 8-bit limbs of the weights B^(s-1-k) mod M (tcgen05.mma kind::i8), folded mod
+ * M.  All other segments use the CUDA-core path; the results are identical.
+ * Errors: AMS_ERR_INVALID_ARGUMENT (null hasher). */
+ams_status_t ams_hasher_last_stats(ams_hasher_t hasher, int64_t* segments, int64_t* tc_segments);
+
 /* Synchronises the device and frees the hasher.  NULL is a no-op. */
 ams_status_t ams_hasher_destroy(ams_hasher_t hasher);
 

@@ -33,7 +33,7 @@ EXPORTS = ("ams_get_nccl_unique_id", "ams_pool_create", "ams_pool_append", "ams_
            "ams_pool_status", "ams_pool_size",
            "ams_pool_destroy", "ams_status_string", "ams_pool_set_profiling", "ams_pool_read_profile",
            "ams_pool_launch_count", "ams_pool_last_plan", "ams_pool_set_kernel_policy", "ams_shard_locate", "ams_shard_capacity",
-           "ams_abi_version", "ams_hasher_create", "ams_hash_actions", "ams_hasher_destroy",
+           "ams_abi_version", "ams_hasher_create", "ams_hash_actions", "ams_hasher_last_stats", "ams_hasher_destroy",
            "ams_vstore_create", "ams_vstore_intern", "ams_vstore_release", "ams_vstore_resolve",
            "ams_vstore_arena", "ams_vstore_stats", "ams_vstore_compact", "ams_vstore_destroy", "ams_tier_create", "ams_tier_admit",
            "ams_tier_touch", "ams_tier_evict_until", "ams_tier_fetch", "ams_tier_info", "ams_tier_usage",
@@ -85,6 +85,7 @@ def _load():
         "ams_hasher_create": [I32, I64, I64, I64, ctypes.POINTER(V)],
         "ams_hash_actions": [V, V, V, I32, V, V],
         "ams_hasher_destroy": [V],
+        "ams_hasher_last_stats": [V, ctypes.POINTER(I64), ctypes.POINTER(I64)],
         "ams_vstore_create": [I32, I64, I64, I32, I64, ctypes.POINTER(V)],
         "ams_vstore_intern": [V, V, V, I32, V, V, V, V],
         "ams_vstore_release": [V, V, I32, V, V],
@@ -309,6 +310,12 @@ def ams_hash_actions(hasher: int, data, offsets, n_inputs: int, out_hash, stream
     off = np.ascontiguousarray(offsets, dtype=np.int64)
     _check(lib.ams_hash_actions(hasher, _ptr(data), off.ctypes.data, n_inputs, _ptr(out_hash), _stream(stream)),
            "ams_hash_actions")
+
+
+def ams_hasher_last_stats(hasher: int):
+    a, b = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib.ams_hasher_last_stats(hasher, ctypes.byref(a), ctypes.byref(b)), "ams_hasher_last_stats")
+    return {"segments": a.value, "tc_segments": b.value}
 
 
 def ams_hasher_destroy(hasher: int) -> None:

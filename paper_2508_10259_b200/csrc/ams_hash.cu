@@ -17,6 +17,19 @@
 // hashes the same way (steps of B^32).  All arithmetic is exact modular arithmetic on
 // 64-bit limbs (Mersenne reduction), so the result is bit-identical to the sequential
 // definition for every input.
+//
+// Tensor-core phase 1 (full, 16-B aligned segments; s a multiple of 128, s <= 8192).  A
+// segment's hash is a dot product: h = sum_k b_k w_k mod M with w_k = B^(s-1-k) mod M
+// (Horner expanded).  Split every w_k into eight 8-bit limbs w_k = sum_n w_kn 2^(8n):
+// h = sum_n 2^(8n) S_n mod M, S_n = sum_k b_k w_kn -- an exact u8 x u8 -> s32 contraction
+// (S_n <= 8192 * 255 * 255 < 2^31) of the [segments x s] byte matrix with the constant
+// [s x 8] limb matrix: tcgen05.mma kind::i8, M = 128 segments, N = 8 limbs, K = 32 per
+// instruction, accumulators in TMEM.  The segment bytes are streamed from HBM once; the
+// limb matrix stays in shared memory; the epilogue folds the 8 limb sums mod M.  Segments
+// start at arbitrary 16-B aligned offsets (CSR inputs), so they are staged with 16-byte
+// cp.async into the 128-B-swizzled K-major layout rather than by a tensor map.  Every
+// other segment (partial, unaligned) keeps the CUDA-core path above; both write the
+// same per-segment hash array, so phase 2 is unchanged.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -26,6 +39,7 @@
 #include <vector>
 
 #include "../../include/ams.h"
+#include "ams_ptx.cuh"
 
 namespace ams {
 namespace hash {
@@ -87,9 +101,198 @@ struct Tables {
   uint64_t pow1[16];       // B^t, t < 16
 };
 
+// Segments the tensor-core kernel hashes (identical test in both phase-1 kernels).
+__device__ __forceinline__ bool tc_segment(const uint8_t* data, int64_t start, int64_t len, int64_t s, int tc_on) {
+  return tc_on != 0 && len == s && ((reinterpret_cast<uintptr_t>(data + start) & 15u) == 0);
+}
+
+// owning input of segment g: last i with seg_base[i] <= g (empty inputs share a base)
+__device__ __forceinline__ int owner_of(const int64_t* __restrict__ seg_base, int32_t n_inputs, int64_t g) {
+  int lo = 0, hi = n_inputs - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (seg_base[mid] <= g) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+constexpr int kTcRows = 128;                     // segments per tile (MMA M)
+constexpr int kTcLimbs = 8;                      // MMA N
+constexpr int kTcStages = 8;                     // 16 KB A stages
+constexpr int kTcLag = 6;                        // cp.async groups in flight per producer thread
+constexpr int kTcProducerWarps = 4;
+constexpr int kTcEpiWarps = 4;
+constexpr int kTcThreads = 32 * (kTcProducerWarps + 1 + kTcEpiWarps);   // 288
+constexpr uint32_t kTcStageBytes = kTcRows * 128;                       // 16 KB
+constexpr int kTcMaxKb = 64;                                            // s <= 8192
+__host__ __device__ constexpr uint32_t tc_smem_bytes(int n_kb) {
+  return 1024 + (uint32_t)n_kb * 1024 + kTcStages * kTcStageBytes + 256;
+}
+
+// wgt: [n_kb][8 limbs][128 B] in the 128-B swizzled K-major layout (host-built)
+__global__ void __launch_bounds__(kTcThreads, 1)
+    phase1_tc_kernel(const uint8_t* __restrict__ data, const int64_t* __restrict__ offsets,
+                     const int64_t* __restrict__ seg_base, int32_t n_inputs, int64_t n_segs, int64_t s,
+                     const uint8_t* __restrict__ wgt, uint64_t* __restrict__ seg_hash) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+  const int n_kb = (int)(s / 128);
+  uint8_t* sB = smem;                                   // n_kb KB
+  uint8_t* sA = smem + n_kb * 1024;                     // kTcStages x 16 KB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sA + kTcStages * kTcStageBytes);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kTcStages;
+  uint64_t* tfull = bars + 2 * kTcStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int kMmaWarp = kTcProducerWarps;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kTcStages; ++i) {
+      ptx::mbar_init(&full[i], 32 * kTcProducerWarps);
+      ptx::mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&tfull[i], 1);
+      ptx::mbar_init(&tempty[i], kTcEpiWarps);
+    }
+    ptx::fence_mbar_init();
+  }
+  // the constant limb matrix -> shared memory (already in the swizzled layout)
+  for (int i = threadIdx.x; i < n_kb * 64; i += kTcThreads)
+    reinterpret_cast<uint4*>(sB)[i] = __ldg(reinterpret_cast<const uint4*>(wgt) + i);
+  ptx::fence_proxy_async_smem();
+  if (warp == kMmaWarp) {
+    ptx::tmem_alloc<1>(tmem_holder, 32);
+    ptx::tmem_relinquish<1>();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  const int64_t n_tiles = (n_segs + kTcRows - 1) / kTcRows;
+
+  if (warp < kTcProducerWarps) {
+    // ------------------------------------------------------------ cp.async producers
+    // warp pw stages rows 32 pw .. 32 pw + 31; instruction i covers rows 32 pw + 4 i +
+    // lane / 8, 16-byte chunk lane % 8 of the K-block (4 full 128-B rows per instruction)
+    const int pw = warp;
+    const int chunk = lane & 7;
+    uint32_t dst_off[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int r = 32 * pw + 4 * i + (lane >> 3);
+      dst_off[i] = (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((chunk ^ (r & 7)) << 4));
+    }
+    const uint32_t sA_u = ptx::smem_u32(sA);
+    uint32_t it = 0;   // stage sequence number
+    for (int64_t T = blockIdx.x; T < n_tiles; T += gridDim.x) {
+      const int64_t g = T * kTcRows + 32 * pw + lane;
+      const uint8_t* rp = nullptr;
+      int el = 0;
+      if (g < n_segs) {
+        const int i = owner_of(seg_base, n_inputs, g);
+        const int64_t start = offsets[i] + (g - seg_base[i]) * s;
+        const int64_t len = min(s, offsets[i + 1] - start);
+        el = tc_segment(data, start, len, s, 1) ? 1 : 0;
+        rp = data + start;
+      }
+      const uint8_t* src[8];
+      int ok = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int sl = 4 * i + (lane >> 3);
+        src[i] = reinterpret_cast<const uint8_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(rp), sl)) +
+                 16 * chunk;
+        ok |= __shfl_sync(0xffffffffu, el, sl) << i;
+      }
+      for (int kb = 0; kb < n_kb; ++kb, ++it) {
+        const uint32_t slot = it % kTcStages;
+        ptx::mbar_wait(&empty[slot], ((it / kTcStages) & 1u) ^ 1u);
+        const uint32_t base = sA_u + slot * kTcStageBytes;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if ((ok >> i) & 1) ptx::cp_async16(base + dst_off[i], src[i] + 128 * kb);
+        ptx::cp_async_commit();
+        if (it >= kTcLag) {   // stage it - kTcLag has landed: publish it to the MMA
+          ptx::cp_async_wait<kTcLag>();
+          ptx::fence_proxy_async_smem();
+          ptx::mbar_arrive(&full[(it - kTcLag) % kTcStages]);
+        }
+      }
+    }
+    ptx::cp_async_wait<0>();
+    ptx::fence_proxy_async_smem();
+    for (uint32_t j = it > (uint32_t)kTcLag ? it - kTcLag : 0; j < it; ++j) ptx::mbar_arrive(&full[j % kTcStages]);
+  } else if (warp == kMmaWarp) {
+    // ------------------------------------------------------------ MMA issuer
+    const uint32_t idesc = ptx::idesc_u8_s32(kTcRows, kTcLimbs);
+    const uint64_t da0 = ptx::sdesc_k_sw128(ptx::smem_u32(sA));
+    const uint64_t db0 = ptx::sdesc_k_sw128(ptx::smem_u32(sB));
+    uint32_t it = 0, tcount = 0;
+    for (int64_t T = blockIdx.x; T < n_tiles; T += gridDim.x, ++tcount) {
+      const uint32_t buf = tcount & 1u;
+      ptx::mbar_wait(&tempty[buf], ((tcount >> 1) & 1u) ^ 1u);
+      ptx::tc_fence_after();
+      const uint32_t d = tmem_base + buf * kTcLimbs;
+      for (int kb = 0; kb < n_kb; ++kb, ++it) {
+        const uint32_t slot = it % kTcStages;
+        ptx::mbar_wait(&full[slot], (it / kTcStages) & 1u);
+        ptx::tc_fence_after();
+        if (ptx::elect_one()) {
+          const uint64_t da = da0 + (uint64_t)(slot * (kTcStageBytes >> 4));
+          const uint64_t db = db0 + (uint64_t)(kb * (1024 >> 4));
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)   // K = 32 bytes per instruction: +32 B = +2 in the descriptor
+            ptx::umma_i8(d, da + 2 * kk, db + 2 * kk, idesc, (kb | kk) != 0 ? 1u : 0u);
+          ptx::umma_commit<1>(&empty[slot]);
+        }
+        __syncwarp();
+      }
+      if (ptx::elect_one()) ptx::umma_commit<1>(&tfull[buf]);
+      __syncwarp();
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue: fold the limbs
+    const int ew = warp & 3;   // a warp may read TMEM lanes 32 (warp % 4) .. + 31
+    uint32_t tcount = 0;
+    for (int64_t T = blockIdx.x; T < n_tiles; T += gridDim.x, ++tcount) {
+      const uint32_t buf = tcount & 1u;
+      ptx::mbar_wait(&tfull[buf], (tcount >> 1) & 1u);
+      ptx::tc_fence_after();
+      uint32_t v[8];
+      ptx::tmem_ld8(tmem_base + ((uint32_t)(32 * ew) << 16) + buf * kTcLimbs, v);
+      ptx::tmem_wait_ld();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&tempty[buf]);
+      const int64_t g = T * kTcRows + 32 * ew + lane;
+      if (g < n_segs) {
+        const int i = owner_of(seg_base, n_inputs, g);
+        const int64_t start = offsets[i] + (g - seg_base[i]) * s;
+        const int64_t len = min(s, offsets[i + 1] - start);
+        if (tc_segment(data, start, len, s, 1)) {
+          // sum_n S_n 2^(8n) < 2^31 * 2^57: exact in 128 bits, then 2^64 = 2^3 (mod M)
+          unsigned __int128 x = 0;
+#pragma unroll
+          for (int n = 7; n >= 0; --n) x = (x << 8) + (unsigned __int128)v[n];
+          const uint64_t lo = (uint64_t)x, hi = (uint64_t)(x >> 64);
+          seg_hash[g] = canon(red((lo & kM) + (lo >> 61) + (hi << 3)));
+        }
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == kMmaWarp) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<1>(tmem_base, 32);
+  }
+}
+
 __global__ void phase1_kernel(const uint8_t* __restrict__ data, const int64_t* __restrict__ offsets,
                               const int64_t* __restrict__ seg_base, int32_t n_inputs, int64_t n_segs, int64_t s,
-                              Tables tb, uint64_t* __restrict__ seg_hash) {
+                              Tables tb, uint64_t* __restrict__ seg_hash, int tc_on) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   // each warp takes a contiguous run of segments: one binary search for the owning
@@ -111,6 +314,7 @@ __global__ void phase1_kernel(const uint8_t* __restrict__ data, const int64_t* _
     const int64_t j = g - seg_base[lo];
     const int64_t start = offsets[lo] + j * s;
     const int64_t len = min(s, offsets[lo + 1] - start);
+    if (tc_segment(data, start, len, s, tc_on)) continue;   // hashed by phase1_tc_kernel
     const uint8_t* p = data + start;
     const int head = (int)min(len, (int64_t)((16 - ((uintptr_t)p & 15)) & 15));
     const int64_t P = (len - head) >> 4;
@@ -187,15 +391,21 @@ __global__ void phase2_kernel(const int64_t* __restrict__ seg_base, int32_t n_in
 
 struct ams_hasher_s {
   int32_t device = 0;
+  int32_t num_sms = 148;
   int64_t max_inputs = 0, max_bytes = 0, s = 4096, max_segs = 0;
+  uint8_t* d_wgt = nullptr;       // tensor-core limb matrix [s/128][8][128] (null: no TC path)
+  int64_t last_segs = 0, last_tc_segs = 0;
   uint8_t* d_stage = nullptr;
   int64_t* d_offsets = nullptr;
   int64_t* d_seg_base = nullptr;
   uint64_t* d_seg_hash = nullptr;
   uint64_t* d_pow16 = nullptr;
-  int64_t* h_pinned = nullptr;   // [2 * (max_inputs + 1)]: offsets, seg_base
-  cudaEvent_t done = nullptr;
-  bool pending = false;
+  // host staging of the offsets / segment bases, double-buffered so a call never waits
+  // for the previous one on the host: slot b = [2 * (max_inputs + 1)] (offsets, seg_base)
+  int64_t* h_pinned = nullptr;   // [2 slots][2 * (max_inputs + 1)]
+  cudaEvent_t done[2] = {nullptr, nullptr};
+  bool pending[2] = {false, false};
+  int32_t slot = 0;
   bool broken = false;
   ams::hash::Tables tb{};
 };
@@ -208,8 +418,10 @@ void hasher_free(ams_hasher_s* h) {
   cudaFree(h->d_seg_base);
   cudaFree(h->d_seg_hash);
   cudaFree(h->d_pow16);
+  cudaFree(h->d_wgt);
   if (h->h_pinned) cudaFreeHost(h->h_pinned);
-  if (h->done) cudaEventDestroy(h->done);
+  for (auto& e : h->done)
+    if (e) cudaEventDestroy(e);
   delete h;
 }
 bool dev_ptr(const void* p) {
@@ -249,8 +461,9 @@ ams_status_t ams_hasher_create(int32_t device, int64_t max_inputs, int64_t max_b
             cudaMalloc(&h->d_seg_base, (max_inputs + 1) * sizeof(int64_t)) == cudaSuccess &&
             cudaMalloc(&h->d_seg_hash, h->max_segs * sizeof(uint64_t)) == cudaSuccess &&
             cudaMalloc(&h->d_pow16, npow * sizeof(uint64_t)) == cudaSuccess &&
-            cudaMallocHost(&h->h_pinned, 2 * (max_inputs + 1) * sizeof(int64_t)) == cudaSuccess &&
-            cudaEventCreateWithFlags(&h->done, cudaEventDisableTiming) == cudaSuccess;
+            cudaMallocHost(&h->h_pinned, 4 * (max_inputs + 1) * sizeof(int64_t)) == cudaSuccess &&
+            cudaEventCreateWithFlags(&h->done[0], cudaEventDisableTiming) == cudaSuccess &&
+            cudaEventCreateWithFlags(&h->done[1], cudaEventDisableTiming) == cudaSuccess;
   if (!ok) {
     cudaGetLastError();
     hasher_free(h);
@@ -275,6 +488,30 @@ ams_status_t ams_hasher_create(int32_t device, int64_t max_inputs, int64_t max_b
     return AMS_ERR_CUDA;
   }
   h->tb.pow16 = h->d_pow16;
+  if (segment_size % 128 == 0 && segment_size / 128 <= kTcMaxKb) {
+    // limb matrix of the tensor-core path: byte k of a segment has weight B^(s-1-k) mod M;
+    // limb n of it sits at K-block k/128, row n, 16-B chunk ((k%128)/16) ^ n (128-B swizzle)
+    const int64_t n_kb = segment_size / 128;
+    std::vector<uint8_t> w((size_t)n_kb * 1024, 0);
+    uint64_t wk = 1;   // B^(s-1-k), k from s-1 down
+    for (int64_t k = segment_size - 1; k >= 0; --k) {
+      const int64_t kb = k / 128, j = k % 128;
+      for (int n = 0; n < 8; ++n)
+        w[(size_t)kb * 1024 + n * 128 + (((j >> 4) ^ n) << 4) + (j & 15)] = (uint8_t)((wk >> (8 * n)) & 0xFF);
+      wk = mulmod_host(wk, kB);
+    }
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+    h->num_sms = nsm;
+    if (cudaMalloc(&h->d_wgt, w.size()) != cudaSuccess ||
+        cudaMemcpy(h->d_wgt, w.data(), w.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaFuncSetAttribute(phase1_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)tc_smem_bytes((int)n_kb)) != cudaSuccess) {
+      cudaGetLastError();
+      hasher_free(h);
+      return AMS_ERR_CUDA;
+    }
+  }
   {  // fast-path weights E[jj][u] = B^(2(7-u)) * B^(512 jj) mod M
     uint32_t elo[8][8], ehi[8][8];
     uint64_t bj = 1;   // B^(512 jj)
@@ -299,6 +536,7 @@ ams_status_t ams_hasher_create(int32_t device, int64_t max_inputs, int64_t max_b
 
 ams_status_t ams_hash_actions(ams_hasher_t h, const uint8_t* data, const int64_t* offsets, int32_t n_inputs,
                               uint64_t* out_hash, void* stream) {
+  using namespace ams::hash;
   if (h == nullptr || offsets == nullptr || out_hash == nullptr || n_inputs < 1 || n_inputs > h->max_inputs)
     return AMS_ERR_INVALID_ARGUMENT;
   if (h->broken) return AMS_ERR_CUDA;
@@ -308,14 +546,21 @@ ams_status_t ams_hash_actions(ams_hasher_t h, const uint8_t* data, const int64_t
   if (total > h->max_bytes) return AMS_ERR_CAPACITY;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (cudaSetDevice(h->device) != cudaSuccess) return AMS_ERR_CUDA;
-  // the pinned staging buffer is reused: wait until the previous call consumed it
-  if (h->pending && cudaEventSynchronize(h->done) != cudaSuccess) {
+  // pinned slot b was last read by the call before the previous one (normally long done);
+  // the device buffers are ordered after the previous call on the device, not the host
+  const int b = h->slot;
+  if (h->pending[b] && cudaEventSynchronize(h->done[b]) != cudaSuccess) {
     h->broken = true;
     return AMS_ERR_CUDA;
   }
-  int64_t* off = h->h_pinned;
-  int64_t* base = h->h_pinned + (h->max_inputs + 1);
-  int64_t nseg = 0;
+  h->pending[b] = false;
+  if (h->pending[b ^ 1] && cudaStreamWaitEvent(s, h->done[b ^ 1], 0) != cudaSuccess) {
+    h->broken = true;
+    return AMS_ERR_CUDA;
+  }
+  int64_t* off = h->h_pinned + (size_t)b * 2 * (h->max_inputs + 1);
+  int64_t* base = off + (h->max_inputs + 1);
+  int64_t nseg = 0, ntc = 0;
   for (int32_t i = 0; i <= n_inputs; ++i) {
     off[i] = device_data ? offsets[i] : offsets[i] - offsets[0];
     if (i > 0 && offsets[i] < offsets[i - 1]) return AMS_ERR_INVALID_ARGUMENT;
@@ -326,20 +571,31 @@ ams_status_t ams_hash_actions(ams_hasher_t h, const uint8_t* data, const int64_t
   }
   base[n_inputs] = nseg;
   if (nseg > h->max_segs) return AMS_ERR_CAPACITY;
-  const uint8_t* src = data;
+  const uint8_t* src = (total > 0 && !device_data) ? h->d_stage : data;
+  if (h->d_wgt != nullptr)   // full 16-B aligned segments go to the tensor-core kernel
+    for (int32_t i = 0; i < n_inputs; ++i)
+      if (((reinterpret_cast<uintptr_t>(src) + (uintptr_t)off[i]) & 15u) == 0)
+        ntc += (offsets[i + 1] - offsets[i]) / h->s;
+  h->last_segs = nseg;
+  h->last_tc_segs = ntc;
   bool ok = cudaMemcpyAsync(h->d_offsets, off, (n_inputs + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s) ==
                 cudaSuccess &&
             cudaMemcpyAsync(h->d_seg_base, base, (n_inputs + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s) ==
                 cudaSuccess;
-  if (ok && total > 0 && !device_data) {
+  if (ok && total > 0 && !device_data)
     ok = cudaMemcpyAsync(h->d_stage, data + offsets[0], total, cudaMemcpyDefault, s) == cudaSuccess;
-    src = h->d_stage;
+  if (ok && ntc > 0) {
+    const int64_t tiles = (nseg + kTcRows - 1) / kTcRows;
+    ams::hash::phase1_tc_kernel<<<(unsigned)std::min<int64_t>(tiles, h->num_sms), kTcThreads,
+                                  tc_smem_bytes((int)(h->s / 128)), s>>>(src, h->d_offsets, h->d_seg_base, n_inputs,
+                                                                         nseg, h->s, h->d_wgt, h->d_seg_hash);
+    ok = cudaGetLastError() == cudaSuccess;
   }
-  if (ok && nseg > 0) {
+  if (ok && nseg > ntc) {
     const int wpb = 8;
     const int64_t blocks = std::min<int64_t>((nseg + wpb - 1) / wpb, 148 * 16);
     ams::hash::phase1_kernel<<<(unsigned)blocks, wpb * 32, 0, s>>>(src, h->d_offsets, h->d_seg_base, n_inputs, nseg,
-                                                                   h->s, h->tb, h->d_seg_hash);
+                                                                   h->s, h->tb, h->d_seg_hash, ntc > 0 ? 1 : 0);
     ok = cudaGetLastError() == cudaSuccess;
   }
   if (ok) {
@@ -348,12 +604,20 @@ ams_status_t ams_hash_actions(ams_hasher_t h, const uint8_t* data, const int64_t
         h->d_seg_base, n_inputs, h->d_seg_hash, h->tb, out_hash);
     ok = cudaGetLastError() == cudaSuccess;
   }
-  ok = ok && cudaEventRecord(h->done, s) == cudaSuccess;
+  ok = ok && cudaEventRecord(h->done[b], s) == cudaSuccess;
   if (!ok) {
     h->broken = true;
     return AMS_ERR_CUDA;
   }
-  h->pending = true;
+  h->pending[b] = true;
+  h->slot = b ^ 1;
+  return AMS_OK;
+}
+
+ams_status_t ams_hasher_last_stats(ams_hasher_t h, int64_t* segments, int64_t* tc_segments) {
+  if (h == nullptr) return AMS_ERR_INVALID_ARGUMENT;
+  if (segments) *segments = h->last_segs;
+  if (tc_segments) *tc_segments = h->last_tc_segs;
   return AMS_OK;
 }
 

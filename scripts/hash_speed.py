@@ -1,3 +1,4 @@
+"""Hash throughput (ams_hash_actions) on 64 x 16 MB blobs, 1M 57-byte actions, and a mix."""
 import os, sys, time, json
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch
@@ -18,5 +19,6 @@ for label, lens in [("blobs_16MB", np.full(64, 16 << 20)), ("actions_57B", np.fu
     for _ in range(reps): ams.ams_hash_actions(h, data, offs, n, out)
     e1.record(); torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
-    print(json.dumps({"case": label, "bytes": int(offs[-1]), "inputs": n, "ms": ms, "GBps": offs[-1] / ms / 1e6}))
+    print(json.dumps({"case": label, "bytes": int(offs[-1]), "inputs": n, "ms": ms, "GBps": offs[-1] / ms / 1e6,
+                      **ams.ams_hasher_last_stats(h)}))
     ams.ams_hasher_destroy(h)

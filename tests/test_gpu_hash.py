@@ -77,3 +77,62 @@ def test_hash_errors(ams):
         ams.ams_hash_actions(h, data, np.zeros(6, np.int64), 5, out)            # n_inputs > max_inputs
     assert e.value.status == 1
     ams.ams_hasher_destroy(h)
+
+
+def _gpu_hash_stats(ams, data, offs, s, device_data):
+    n = len(offs) - 1
+    h = ams.ams_hasher_create(0, n, max(int(offs[-1]), 1), s)
+    out = torch.empty(n, dtype=torch.int64, device="cuda")
+    src = torch.from_numpy(data).cuda() if device_data else data
+    ams.ams_hash_actions(h, src, offs, n, out)
+    torch.cuda.synchronize()
+    st = ams.ams_hasher_last_stats(h)
+    ams.ams_hasher_destroy(h)
+    return out.cpu().numpy().view(np.uint64), st
+
+
+@pytest.mark.parametrize("s", [128, 4096, 8192])
+@pytest.mark.parametrize("fill", ["random", "ff"])
+def test_hash_tensor_core_path_exact(ams, s, fill):
+    """Full 16-B aligned segments take the tcgen05 kind::i8 path (u8 bytes x 8-bit limbs of
+    B^(s-1-k) mod M, s32 accumulate, fold mod M); bit-exact against the sequential oracle,
+    including all-0xFF bytes (the largest limb sums) and inputs with partial last segments."""
+    rng = np.random.Generator(np.random.PCG64(s + (fill == "ff")))
+    lens = np.array([16 * int(x) for x in rng.integers(0, 6 * s // 16, 40)] + [s, 2 * s, 3 * s + 16, 0, 16], np.int64)
+    offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)   # every input 16-B aligned
+    data = (np.full(int(offs[-1]) + 16, 255, np.uint8) if fill == "ff"
+            else rng.integers(0, 256, int(offs[-1]) + 16, dtype=np.uint8))
+    exp = oracle.hash_actions(data, offs, s=s)
+    for device_data in (False, True):
+        got, st = _gpu_hash_stats(ams, data, offs, s, device_data)
+        assert np.array_equal(got, exp), device_data
+        assert st["tc_segments"] == int(np.sum(lens // s)) > 0
+        assert st["segments"] == int(np.sum((lens + s - 1) // s))
+
+
+def test_hash_tensor_core_mixed_alignment(ams):
+    """Aligned and unaligned inputs in one batch: each segment is hashed by exactly one of
+    the two phase-1 kernels (tensor-core for full aligned segments, CUDA cores otherwise)."""
+    rng = np.random.Generator(np.random.PCG64(9))
+    lens = rng.integers(0, 5 * 4096, 200)
+    offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    data = rng.integers(0, 256, int(offs[-1]) + 1, dtype=np.uint8)
+    exp = oracle.hash_actions(data, offs)
+    got, st = _gpu_hash_stats(ams, data, offs, 4096, True)
+    assert np.array_equal(got, exp)
+    aligned = (offs[:-1] % 16) == 0
+    assert st["tc_segments"] == int(np.sum((lens // 4096)[aligned])) > 0
+    assert st["tc_segments"] < st["segments"]
+
+
+def test_hash_tensor_core_many_tiles(ams):
+    """More 128-segment tiles than SMs (the persistent loop wraps, TMEM double buffer and
+    every shared-memory stage reused many times): 48 x 4 MB aligned inputs."""
+    rng = np.random.Generator(np.random.PCG64(3))
+    lens = np.full(48, 4 << 20, np.int64)
+    offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    data = rng.integers(0, 256, int(offs[-1]), dtype=np.uint8)
+    exp = oracle.hash_actions(data, offs)
+    got, st = _gpu_hash_stats(ams, data, offs, 4096, True)
+    assert np.array_equal(got, exp)
+    assert st["tc_segments"] == st["segments"] == 48 * 1024

@@ -147,14 +147,14 @@ def test_churn_reclaims_arena_and_table(ams, device_data):
     arena top stays bounded; every live entry keeps its refcount and bytes, op by op
     against the oracle store (oracle/vstore.py)."""
     rng = np.random.Generator(np.random.PCG64(77 + device_data))
-    arena = 256 << 10
-    st = ams.ams_vstore_create(0, 512, arena, 64, 1 << 20)   # table: 1024 slots
+    arena = 1 << 20
+    st = ams.ams_vstore_create(0, 512, arena, 128, 1 << 20)   # table: 1024 slots
     orc = VirtualActionStore()
     live = []
     interned_bytes = interned_keys = 0
     for step in range(100):
-        fresh = [rng.integers(0, 256, rng.integers(0, 2000), dtype=np.uint8).tobytes()
-                 for _ in range(rng.integers(1, 40))]
+        fresh = [rng.integers(0, 256, rng.integers(0, 4000), dtype=np.uint8).tobytes()
+                 for _ in range(rng.integers(1, 60))]
         again = [orc.resolve(i) for i in rng.choice(live, min(len(live), 8), replace=False)] if live else []
         batch = fresh + again
         ids, status = gpu_intern(ams, st, batch, device_data=device_data)
