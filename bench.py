@@ -162,10 +162,10 @@ def parse():
     ap.add_argument("--force-collective", action="store_true",
                     help="N = 1 only: run the multi-GPU code path (NCCL all-gather, shard merge, peer exchange) "
                          "over a 1-rank communicator -- a dry run of what --gpus N > 1 executes")
-    ap.add_argument("--kernel-policy", type=int, default=0, choices=[0, 1, 2, 3],
+    ap.add_argument("--kernel-policy", type=int, default=0, choices=list(range(8)),
                     help="bit mask for A/B measurements: 1 = batches of <= 128 queries use the 128-query-tile "
                          "kernel instead of the small-batch kernel; 2 = two CTA pairs per 4-CTA cluster sharing "
-                         "multicast pool rows (opt-in)")
+                         "multicast pool rows (opt-in); 4 = narrow small-batch CTA pairs (one tile per stage)")
     return ap.parse_args()
 
 

@@ -172,7 +172,8 @@ void plan_tc(const Pool& p, int nq, int KT, int& S, int& grid, int& cg, int& cl)
 // Plan of the small-batch kernel: one query tile, so units are row splits only; same
 // cost model as plan_tc (busiest CTA's tile count, ties -> fewer splits).
 void plan_scan(const Pool& p, int nq, int KT, bool gated, int& S, int& grid) {
-  const int64_t n_pt = (p.local + ams::kBlockN - 1) / ams::kBlockN;
+  const int w = ams::scan_w(p, nq, KT);   // splits are counted in super-tiles of w tiles
+  const int64_t n_pt = ((p.local + ams::kBlockN - 1) / ams::kBlockN + w - 1) / w;
   const int cg = ams::scan_cg(nq);
   const int ctas = std::min(p.num_sms / cg, cg == 2 ? std::max(1, p.max_clusters2) : p.num_sms);   // tiles in flight
   const int64_t per_split = (int64_t)nq * ams::scan_lists_per_split(nq, KT, gated) * KT;
@@ -964,7 +965,7 @@ ams_status_t ams_pool_launch_count(ams_pool_t pool, int64_t* launches) {
 }
 
 ams_status_t ams_pool_set_kernel_policy(ams_pool_t pool, int32_t policy) {
-  if (pool == nullptr || policy < 0 || policy > 3) return AMS_ERR_INVALID_ARGUMENT;
+  if (pool == nullptr || policy < 0 || policy > 7) return AMS_ERR_INVALID_ARGUMENT;
   pool->p.kernel_policy = policy;
   return AMS_OK;
 }

@@ -145,7 +145,8 @@ struct Pool {
   CUtensorMap tmap_pool4{};  // bf16 pool [cap_pad, d], box {64, 64}, SW128 (multicast quarter tile)
   CUtensorMap tmap_q{};      // bf16 queries [q_pad, d], box {64, 128}, SW128
   CUtensorMap tmap_qs[8]{};  // bf16 queries [q_pad, d], box {64, 16 (i + 1)}, SW128 (small-batch kernel)
-  int32_t kernel_policy = 0; // bit 0: never the small-batch kernel; bit 1: no 4-CTA multicast clusters
+  int32_t kernel_policy = 0; // bit 0: never the small-batch kernel; bit 1: 4-CTA multicast clusters;
+                             // bit 2: narrow (one tile per stage) small-batch CTA pairs
 
   void* nccl_comm = nullptr;  // ncclComm_t
 
@@ -212,6 +213,7 @@ int tc_max_active_clusters(int cl);   // co-resident clusters of cl CTAs (CTA-pa
 // above 128 queries, or the per-lane register lists would not fit)
 int scan_stages(const Pool& p, int nq, int KT);
 int scan_cg(int nq);                 // CTAs per tile: 1 (nq <= 128) or 2 (CTA pair)
+int scan_w(const Pool& p, int nq, int KT);   // tiles per pipeline stage (2: wide CTA pair)
 int scan_lists_per_split(int nq, int KT, bool gated);   // partial lists per row split (1: warps merged in the CTA)
 cudaError_t launch_match_scan(Pool& p, const MatchArgs& a, int32_t splits, int32_t grid, cudaStream_t s);
 // merge [nq][P][KT] local lists -> [nq][k] (fp32, global int64); writes hit if out_hit != null

@@ -20,6 +20,15 @@
 // bf16 per pipeline stage (one 128-B swizzle atom).  TMEM: two accumulator buffers of
 // 2*NQ columns; half h of buffer b at columns b*2NQ + h*NQ, lane = pool row (mod 128).
 //
+// CTA pairs (129-256 queries) are "wide" (W = 2): a pipeline stage carries the pair's
+// 128-row halves of TWO consecutive tiles per CTA (two cta_group::2 MMAs, M = 256 each)
+// against one stage of N/2 query rows per CTA, so every query byte staged from L2 serves
+// 512 pool rows instead of 256.  The L2 -> SM operand traffic of a call drops from
+// pool x (1 + N/256) to pool x (1 + N/512) -- at N = 224 from 1.88x to 1.44x the pool --
+// which is what bounded the narrow pair (LTS throughput, ~9.5 TB/s at the capped clock).
+// The price is TMEM: 2 halves x N columns fill it, so the accumulator is single-
+// buffered; the TMA ring keeps streaming the next super-tile while the epilogue drains.
+//
 // Warp roles (192 threads, 1 CTA/SM): warps 0..3 epilogue (warp w reads TMEM lanes
 // 32w.. = pool rows 32w+lane and 128+32w+lane of each tile), warp 4 TMA producer
 // (pool + query tiles into a STAGES ring, per-tile joints/inv_norm into a 2-deep aux
@@ -79,19 +88,21 @@ struct ScanParams {
 
 // shared-memory layout (byte offsets from the 1024-aligned base), host and device
 struct ScanLayout {
-  uint32_t a, b, aux, tr, qj, iq, thr, ls, li, bars, total;
+  uint32_t a, b, aux, tr, qj, iq, thr, em, ls, li, bars, total;
 };
 
 // cg = 2: a CTA stages 128 of the pair's 256 pool rows per stage
-__host__ __device__ inline ScanLayout scan_layout(int stages, uint32_t b_bytes, int JP, int NQ, int cg, int KT) {
+__host__ __device__ inline ScanLayout scan_layout(int stages, uint32_t b_bytes, int JP, int NQ, int cg, int KT,
+                                                  int W) {
   ScanLayout l{};
+  const uint32_t rows = (uint32_t)(kBlockN / cg * W);   // pool rows per CTA and stage
   uint32_t o = 0;
   l.a = o;
-  o += (uint32_t)stages * (kScanABytes / (uint32_t)cg);
+  o += (uint32_t)stages * rows * kBlockK * 2;
   l.b = o;
   o += (uint32_t)stages * b_bytes;
   l.aux = o;
-  o += 2u * (uint32_t)((kBlockN / cg) * JP * 4 + (kBlockN / cg) * 4);   // joints + inv of this CTA's rows
+  o += 2u * (rows * JP * 4 + rows * 4);   // joints + inv of this CTA's rows
   l.tr = o;
   o += (uint32_t)(kScanEpiWarps * 32 * kTPad * 4 + 64);   // + keep 16-B alignment below
   l.qj = o;
@@ -100,6 +111,8 @@ __host__ __device__ inline ScanLayout scan_layout(int stages, uint32_t b_bytes, 
   o += (uint32_t)(NQ * 4);
   l.thr = o;
   o += (uint32_t)(kScanEpiWarps * NQ * 4);
+  l.em = o;   // gate masks [warps][halves][NQ / 32 slots][32 lanes]
+  o += (uint32_t)(kScanEpiWarps * (cg == 1 ? 2 : W) * NQ * 4);
   l.ls = l.li = o;   // (lists: registers for cg = 1, global memory for cg = 2)
   l.bars = o;
   o += 256;
@@ -107,16 +120,19 @@ __host__ __device__ inline ScanLayout scan_layout(int stages, uint32_t b_bytes, 
   return l;
 }
 
-__device__ __forceinline__ void scan_split(int sp, int S, int n_pt, int& t_lo, int& t_hi) {
-  t_lo = (int)((int64_t)sp * n_pt / S);
-  t_hi = (int)((int64_t)(sp + 1) * n_pt / S);
+// split sp of S over the pool's tiles, in whole super-tiles of W tiles (the last may be
+// short: its missing tiles are past the pool and load / score nothing)
+__device__ __forceinline__ void scan_split(int sp, int S, int n_pt, int W, int& t_lo, int& t_hi) {
+  const int n_st = (n_pt + W - 1) / W;
+  t_lo = W * (int)((int64_t)sp * n_st / S);
+  t_hi = min(n_pt, W * (int)((int64_t)(sp + 1) * n_st / S));
 }
 
 // CG = 1: one CTA per 256-row tile (two M = 128 MMAs), nq <= 128.  CG = 2: a CTA pair
 // per 256-row tile (one tcgen05.mma.cta_group::2 with M = 256: each CTA stages 128 pool
 // rows and half of the N query rows), 128 < nq <= 256; each CTA's epilogue owns its 128
 // rows against all N queries.
-template <int KT, int JP, bool GATED, int CG>
+template <int KT, int JP, bool GATED, int CG, int W>
 __global__ void __launch_bounds__(kScanThreads, 1)
     match_scan_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_pool,
                       const ScanParams prm) {
@@ -125,10 +141,13 @@ __global__ void __launch_bounds__(kScanThreads, 1)
   // filter's loads and spill; in shared memory they cost pipeline stages (C5: 3 stages,
   // 7.4 ms vs 6.3 ms per 129-256-query call)
   constexpr bool SMEM_LISTS = CG == 2;   // (name kept: the lists are out of registers)
-  constexpr int AROWS = kBlockN / CG;              // tile rows this CTA owns (aux ring)
+  static_assert(W == 1 || CG == 2, "wide stages are a CTA-pair mode");
+  constexpr int HALVES = CG == 1 ? 2 : W;          // 128-row MMA halves per CTA and stage
+  constexpr int NBUF = W == 1 ? 2 : 1;             // TMEM accumulator buffers (2 * HALVES * NQ <= 512)
+  constexpr int AROWS = 128 * HALVES;              // super-tile rows this CTA owns (aux ring)
   constexpr uint32_t AUXJ = AROWS * JP * 4;
   constexpr uint32_t AUX = AUXJ + AROWS * 4;
-  constexpr uint32_t ABYTES = kScanABytes / CG;   // pool rows staged per CTA and stage
+  constexpr uint32_t ABYTES = kScanHalfBytes * HALVES;   // pool rows staged per CTA and stage
   constexpr int NQMAX = 128 * CG;
   constexpr int NSL0 = kScanListRegs / (32 * KT);
   constexpr int NSL = NSL0 < NQMAX / 32 ? NSL0 : NQMAX / 32;   // 32-query slots per lane
@@ -136,7 +155,7 @@ __global__ void __launch_bounds__(kScanThreads, 1)
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   const int NQ = prm.NQ;
   const int STAGES = prm.stages;
-  const ScanLayout lay = scan_layout(STAGES, prm.b_bytes, JP, NQ, CG, KT);
+  const ScanLayout lay = scan_layout(STAGES, prm.b_bytes, JP, NQ, CG, KT, W);
   uint8_t* sA = smem + lay.a;
   uint8_t* sB = smem + lay.b;
   uint8_t* sAux = smem + lay.aux;
@@ -144,6 +163,7 @@ __global__ void __launch_bounds__(kScanThreads, 1)
   float* qjs = reinterpret_cast<float*>(smem + lay.qj);   // [JP][NQ]
   float* iqs = reinterpret_cast<float*>(smem + lay.iq);   // [NQ]
   float* thr = reinterpret_cast<float*>(smem + lay.thr);  // [warps][NQ]
+  uint32_t* ems = reinterpret_cast<uint32_t*>(smem + lay.em);   // [warps][HALVES][NQ/32][32]
   float* lsm = prm.glist_s + (int64_t)blockIdx.x * kScanEpiWarps * NSL * KT * 32;   // SMEM_LISTS
   int32_t* lim = prm.glist_i + (int64_t)blockIdx.x * kScanEpiWarps * NSL * KT * 32;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + lay.bars);
@@ -197,23 +217,30 @@ __global__ void __launch_bounds__(kScanThreads, 1)
     uint32_t phase = 0, tile_count = 0;
     for (int u = cid; u < prm.S; u += ncl) {
       int t_lo, t_hi;
-      scan_split(u, prm.S, prm.n_pt, t_lo, t_hi);
-      for (int t = t_lo; t < t_hi; ++t, ++tile_count) {
+      scan_split(u, prm.S, prm.n_pt, W, t_lo, t_hi);
+      for (int t = t_lo; t < t_hi; t += W, ++tile_count) {
         const int buf = tile_count & 1;
         const uint32_t use = tile_count >> 1;
         ptx::mbar_wait(&aempty[buf], (use & 1u) ^ 1u);
         if (ptx::elect_one()) {
           uint8_t* aux = sAux + buf * AUX;
-          ptx::mbar_arrive_expect_tx(&afull[buf], AUX);
           if (CG == 1) {
+            ptx::mbar_arrive_expect_tx(&afull[buf], AUX);
             ptx::bulk_load(aux, prm.pool_joints + (int64_t)t * kBlockN * JP, AUXJ, &afull[buf]);
-          } else {   // this CTA's 128 columns of each joint row of the [JP][256] tile block
+            ptx::bulk_load(aux + AUXJ, prm.pool_inv + (int64_t)t * kBlockN, AROWS * 4, &afull[buf]);
+          } else {   // this CTA's 128 columns of each joint row of the [JP][256] block of tile t + h
+            const int hv = min(W, prm.n_pt - t);   // a super-tile past the last tile loads nothing for it
+            ptx::mbar_arrive_expect_tx(&afull[buf], (uint32_t)hv * 128u * (JP + 1) * 4u);
+            for (int h = 0; h < hv; ++h) {
 #pragma unroll
-            for (int tj = 0; tj < JP; ++tj)
-              ptx::bulk_load(aux + tj * AROWS * 4, prm.pool_joints + ((int64_t)t * JP + tj) * kBlockN + crank * AROWS,
-                             AROWS * 4, &afull[buf]);
+              for (int tj = 0; tj < JP; ++tj)
+                ptx::bulk_load(aux + (tj * AROWS + h * 128) * 4,
+                               prm.pool_joints + ((int64_t)(t + h) * JP + tj) * kBlockN + crank * 128, 128 * 4,
+                               &afull[buf]);
+              ptx::bulk_load(aux + AUXJ + h * 128 * 4, prm.pool_inv + (int64_t)(t + h) * kBlockN + crank * 128, 128 * 4,
+                             &afull[buf]);
+            }
           }
-          ptx::bulk_load(aux + AUXJ, prm.pool_inv + (int64_t)t * kBlockN + crank * AROWS, AROWS * 4, &afull[buf]);
         }
         __syncwarp();
         for (int kb = 0; kb < n_kb; ++kb) {
@@ -226,8 +253,10 @@ __global__ void __launch_bounds__(kScanThreads, 1)
             } else {
               if (crank == 0) ptx::mbar_arrive_expect_tx(&full[stage], CG * tx);
               const uint32_t fb = full_leader0 + (uint32_t)(stage * sizeof(uint64_t));
-              ptx::tma_load_2d_pair(sA + stage * ABYTES, &tmap_pool, fb, kb * kBlockK, t * kBlockN + (int)crank * 128,
-                                    pol_pool);
+#pragma unroll
+              for (int h = 0; h < W; ++h)   // rows past the pool's storage are zero-filled by the TMA
+                ptx::tma_load_2d_pair(sA + stage * ABYTES + h * kScanHalfBytes, &tmap_pool, fb, kb * kBlockK,
+                                      (t + h) * kBlockN + (int)crank * 128, pol_pool);
               ptx::tma_load_2d_pair(sB + stage * prm.b_bytes, &tmap_q, fb, kb * kBlockK, qrow0, pol_q);
             }
           }
@@ -247,13 +276,13 @@ __global__ void __launch_bounds__(kScanThreads, 1)
     uint32_t phase = 0, tile_count = 0;
     for (int u = cid; u < prm.S && crank == 0; u += ncl) {
       int t_lo, t_hi;
-      scan_split(u, prm.S, prm.n_pt, t_lo, t_hi);
-      for (int t = t_lo; t < t_hi; ++t, ++tile_count) {
-        const int buf = tile_count & 1;
-        const uint32_t use = tile_count >> 1;
+      scan_split(u, prm.S, prm.n_pt, W, t_lo, t_hi);
+      for (int t = t_lo; t < t_hi; t += W, ++tile_count) {
+        const int buf = NBUF == 2 ? (int)(tile_count & 1) : 0;
+        const uint32_t use = NBUF == 2 ? tile_count >> 1 : tile_count;
         ptx::mbar_wait(&tempty[buf], (use & 1u) ^ 1u);
         ptx::tc_fence_after();
-        const uint32_t d0 = tmem_base + (uint32_t)(buf * (2 / CG) * NQ);
+        const uint32_t d0 = tmem_base + (uint32_t)(buf * HALVES * NQ);
         for (int kb = 0; kb < n_kb; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
@@ -261,7 +290,7 @@ __global__ void __launch_bounds__(kScanThreads, 1)
             const uint64_t da = da0 + (uint64_t)((uint32_t)stage * (ABYTES >> 4));
             const uint64_t db = db0 + (uint64_t)((uint32_t)stage * (prm.b_bytes >> 4));
 #pragma unroll
-            for (int h = 0; h < 2 / CG; ++h)
+            for (int h = 0; h < HALVES; ++h)
 #pragma unroll
               for (int kk = 0; kk < kBlockK / 16; ++kk)
                 ptx::umma_f16<CG>(d0 + (uint32_t)(h * NQ), da + (uint64_t)(h * (kScanHalfBytes >> 4) + 2 * kk),
@@ -295,7 +324,7 @@ __global__ void __launch_bounds__(kScanThreads, 1)
     uint32_t tile_count = 0;
     for (int u = cid; u < prm.S; u += ncl) {
       int t_lo, t_hi;
-      scan_split(u, prm.S, prm.n_pt, t_lo, t_hi);
+      scan_split(u, prm.S, prm.n_pt, W, t_lo, t_hi);
       // lane q owns query sl*32 + q of every slot sl: its list and its shared bound
       TopK<KT, int32_t> top[SMEM_LISTS ? 1 : NSL];
       float kth_s[NSL], best_s[NSL];   // SMEM_LISTS: each list's KT-th and best score
@@ -326,37 +355,38 @@ __global__ void __launch_bounds__(kScanThreads, 1)
         if (sl < nsl) mythr[c] = act ? bnd[sl] : CUDART_INF_F;
       }
       __syncwarp();
-      for (int t = t_lo; t < t_hi; ++t, ++tile_count) {
-        const int buf = tile_count & 1;
+      for (int t = t_lo; t < t_hi; t += W, ++tile_count) {
+        const int buf = tile_count & 1;   // aux ring slot
         const uint32_t use = tile_count >> 1;
+        const int tb = NBUF == 2 ? buf : 0;   // TMEM accumulator buffer
+        const uint32_t tuse = NBUF == 2 ? use : tile_count;
         ptx::mbar_wait(&afull[buf], use & 1u);
-        ptx::mbar_wait(&tfull[buf], use & 1u);
-        ptx::tc_fence_after();
         const float* jsm = reinterpret_cast<const float*>(sAux + buf * AUX);
         const float* inv_sm = reinterpret_cast<const float*>(sAux + buf * AUX + AUXJ);
+        // Phase A (gated): the joint gate needs no score, so it runs as soon as the tile's
+        // joints have landed -- while the MMA is still accumulating the tile -- and leaves
+        // per (row half, 32-query slot) masks of the pairs that pass the exact canonical
+        // gate.  Phase B holds the accumulators only for blocks with a passing pair (with
+        // single-buffered TMEM in the wide pair mode this is what keeps the MMA fed).
+        uint32_t* emw = ems + lg * HALVES * NQ;   // this warp's masks, [h][sl][lane]
+        if (GATED) {
 #pragma unroll 1
-        for (int h = 0; h < 2 / CG; ++h) {
-          const int32_t rowbase = t * kBlockN + (h + (int)crank) * 128 + lg * 32;
-          const bool valid = (int64_t)rowbase + lane < prm.L;
-          const int ra = h * 128 + lg * 32 + lane;   // row within this CTA's aux block
-          float pj[JP];
+          for (int h = 0; h < HALVES; ++h) {
+            const int32_t rowbase = CG == 1 ? t * kBlockN + h * 128 + lg * 32
+                                            : (t + h) * kBlockN + (int)crank * 128 + lg * 32;
+            const bool valid = (int64_t)rowbase + lane < prm.L;
+            const int ra = h * 128 + lg * 32 + lane;   // row within this CTA's aux block
+            float pj[JP];
 #pragma unroll
-          for (int tj = 0; tj < JP; ++tj) pj[tj] = jsm[tj * AROWS + ra];
-          const float ie = inv_sm[ra];
-          const uint64_t IE2 = ptx::pack2(ie, ie);
+            for (int tj = 0; tj < JP; ++tj) pj[tj] = jsm[tj * AROWS + ra];
+            uint64_t PP[4];
 #pragma unroll
-          for (int sl = 0; sl < NSL; ++sl) {
-            if (sl >= nsl) break;
-            const int c0 = sl * 32;
-            const uint32_t taddr =
-                tmem_base + ((uint32_t)(lg * 32) << 16) + (uint32_t)(buf * (2 / CG) * NQ + h * NQ + c0);
-            uint32_t elig = valid ? 0xFFFFFFFFu : 0u;   // pairs (this row, query c0 + c) that may enter
-            if (GATED) {
+            for (int tj = 0; tj < 4; ++tj) PP[tj] = ptx::pack2(pj[tj], pj[tj]);   // JP >= 4
+#pragma unroll 1
+            for (int sl = 0; sl < nsl; ++sl) {
+              const int c0 = sl * 32;
               // partial canonical distance over joints 0..3 for the 32 queries, two at a time
               uint32_t fire = 0;
-              uint64_t PP[4];
-#pragma unroll
-              for (int tj = 0; tj < 4; ++tj) PP[tj] = ptx::pack2(pj[tj], pj[tj]);   // JP >= 4
 #pragma unroll
               for (int g = 0; g < 32; g += 4) {
                 uint64_t da = 0ull, db = 0ull;
@@ -373,23 +403,44 @@ __global__ void __launch_bounds__(kScanThreads, 1)
                 fire |= (ptx::lo2(db) <= prm.g2 ? 1u : 0u) << (g + 2);
                 fire |= (ptx::hi2(db) <= prm.g2 ? 1u : 0u) << (g + 3);
               }
-              fire &= elig;
-              if (__reduce_or_sync(0xffffffffu, fire) == 0u) continue;   // the common case
-              // exact canonical gate for the surviving pairs of this lane
-              elig = 0u;
-              while (fire != 0u) {
-                const int c = __ffs(fire) - 1;
-                fire &= fire - 1u;
-                float ds = 0.0f;
+              if (!valid) fire = 0u;
+              uint32_t elig = 0u;
+              if (__reduce_or_sync(0xffffffffu, fire) != 0u) {   // rare: exact canonical gate of the survivors
+                while (fire != 0u) {
+                  const int c = __ffs(fire) - 1;
+                  fire &= fire - 1u;
+                  float ds = 0.0f;
 #pragma unroll
-                for (int tj = 0; tj < JP; ++tj) {
-                  const float df = __fsub_rn(qjs[tj * NQ + c0 + c], pj[tj]);
-                  ds = __fmaf_rn(df, df, ds);
+                  for (int tj = 0; tj < JP; ++tj) {
+                    const float df = __fsub_rn(qjs[tj * NQ + c0 + c], pj[tj]);
+                    ds = __fmaf_rn(df, df, ds);
+                  }
+                  if (ds <= prm.g2) elig |= 1u << c;
                 }
-                if (ds <= prm.g2) elig |= 1u << c;
               }
-              if (__reduce_or_sync(0xffffffffu, elig) == 0u) continue;
+              emw[(h * (NQ / 32) + sl) * 32 + lane] = elig;
             }
+          }
+        }
+        ptx::mbar_wait(&tfull[tb], tuse & 1u);
+        ptx::tc_fence_after();
+#pragma unroll 1
+        for (int h = 0; h < HALVES; ++h) {
+          const int32_t rowbase = CG == 1 ? t * kBlockN + h * 128 + lg * 32
+                                          : (t + h) * kBlockN + (int)crank * 128 + lg * 32;
+          const int ra = h * 128 + lg * 32 + lane;
+          const bool valid = (int64_t)rowbase + lane < prm.L;
+          const float ie = inv_sm[ra];
+          const uint64_t IE2 = ptx::pack2(ie, ie);
+#pragma unroll
+          for (int sl = 0; sl < NSL; ++sl) {
+            if (sl >= nsl) break;
+            const int c0 = sl * 32;
+            const uint32_t taddr =
+                tmem_base + ((uint32_t)(lg * 32) << 16) + (uint32_t)(tb * HALVES * NQ + h * NQ + c0);
+            // pairs (this row, query c0 + c) that may enter
+            const uint32_t elig = GATED ? emw[(h * (NQ / 32) + sl) * 32 + lane] : (valid ? 0xFFFFFFFFu : 0u);
+            if (GATED && __reduce_or_sync(0xffffffffu, elig) == 0u) continue;   // the common case
             // exact scores of the block (kept in v), then the threshold test
             uint32_t v[32];
             __syncwarp();
@@ -455,9 +506,9 @@ __global__ void __launch_bounds__(kScanThreads, 1)
         __syncwarp();
         if (lane == 0) {
           if (CG == 1)
-            ptx::mbar_arrive(&tempty[buf]);
+            ptx::mbar_arrive(&tempty[tb]);
           else
-            ptx::mbar_arrive_cluster(tempty_leader0 + (uint32_t)(buf * sizeof(uint64_t)));
+            ptx::mbar_arrive_cluster(tempty_leader0 + (uint32_t)(tb * sizeof(uint64_t)));
           ptx::mbar_arrive(&aempty[buf]);
         }
         // share the admission bound with the other CTAs (publish improvements only).
@@ -465,8 +516,8 @@ __global__ void __launch_bounds__(kScanThreads, 1)
         // thresholds move fast early and slowly later, and each refresh is a chain of
         // L2 round trips that one epilogue warp per sub-partition cannot hide (ncu: the
         // per-tile refresh was the top stall of the ungated scan).
-        const int done = t - t_lo + 1;
-        const bool refresh = (done & (done - 1)) == 0 || t + 1 == t_hi;
+        const int done = (t - t_lo) / W + 1;
+        const bool refresh = (done & (done - 1)) == 0 || t + W >= t_hi;
 #pragma unroll
         for (int sl = 0; sl < NSL; ++sl) {
           const int c = sl * 32 + lane;
@@ -585,10 +636,10 @@ __global__ void __launch_bounds__(kScanThreads, 1)
 int scan_box(int rows) { return rows; }
 int box_index(int box) { return box / 16 - 1; }
 
-template <int KT, int JP, bool G, int CG>
+template <int KT, int JP, bool G, int CG, int W>
 cudaError_t launch_scan_t(Pool& p, const ScanParams& prm, int box, int grid, cudaStream_t s) {
-  auto kern = match_scan_kernel<KT, JP, G, CG>;
-  const size_t smem = scan_layout(prm.stages, prm.b_bytes, JP, prm.NQ, CG, KT).total;
+  auto kern = match_scan_kernel<KT, JP, G, CG, W>;
+  const size_t smem = scan_layout(prm.stages, prm.b_bytes, JP, prm.NQ, CG, KT, W).total;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
@@ -606,23 +657,24 @@ cudaError_t launch_scan_t(Pool& p, const ScanParams& prm, int box, int grid, cud
   return cudaLaunchKernelEx(&cfg, kern, p.tmap_qs[box_index(box)], CG == 1 ? p.tmap_pool : p.tmap_pool2, prm);
 }
 
-template <int KT, bool G, int CG>
+template <int KT, bool G, int CG, int W>
 cudaError_t launch_scan_kt(Pool& p, const ScanParams& prm, int box, int grid, cudaStream_t s) {
   switch (p.JP) {
-    case 4: return launch_scan_t<KT, 4, G, CG>(p, prm, box, grid, s);
-    case 8: return launch_scan_t<KT, 8, G, CG>(p, prm, box, grid, s);
-    default: return launch_scan_t<KT, 16, G, CG>(p, prm, box, grid, s);
+    case 4: return launch_scan_t<KT, 4, G, CG, W>(p, prm, box, grid, s);
+    case 8: return launch_scan_t<KT, 8, G, CG, W>(p, prm, box, grid, s);
+    default: return launch_scan_t<KT, 16, G, CG, W>(p, prm, box, grid, s);
   }
 }
 
 template <bool G>
-cudaError_t launch_scan_g(Pool& p, const MatchArgs& a, const ScanParams& prm, int box, int grid, int cg,
+cudaError_t launch_scan_g(Pool& p, const MatchArgs& a, const ScanParams& prm, int box, int grid, int cg, int w,
                           cudaStream_t s) {
-  if (cg == 2) return launch_scan_kt<8, G, 2>(p, prm, box, grid, s);   // eligibility: KT = 8 only
+  if (cg == 2)   // eligibility: KT = 8 only
+    return w == 2 ? launch_scan_kt<8, G, 2, 2>(p, prm, box, grid, s) : launch_scan_kt<8, G, 2, 1>(p, prm, box, grid, s);
   switch (a.KT) {
-    case 8: return launch_scan_kt<8, G, 1>(p, prm, box, grid, s);
-    case 16: return launch_scan_kt<16, G, 1>(p, prm, box, grid, s);
-    default: return launch_scan_kt<32, G, 1>(p, prm, box, grid, s);
+    case 8: return launch_scan_kt<8, G, 1, 1>(p, prm, box, grid, s);
+    case 16: return launch_scan_kt<16, G, 1, 1>(p, prm, box, grid, s);
+    default: return launch_scan_kt<32, G, 1, 1>(p, prm, box, grid, s);
   }
 }
 
@@ -630,14 +682,24 @@ cudaError_t launch_scan_g(Pool& p, const MatchArgs& a, const ScanParams& prm, in
 
 int scan_cg(int nq) { return nq > kBlockM ? 2 : 1; }
 
+// tiles per pipeline stage: 2 on CTA pairs (the wide mode) unless policy bit 2 asks for
+// the narrow pair (A/B measurements) or the wide stages do not fit shared memory
+int scan_w(const Pool& p, int nq, int KT) {
+  if (scan_cg(nq) != 2 || (p.kernel_policy & 4) != 0) return 1;
+  const int NQ = (nq + 31) / 32 * 32;
+  const uint32_t b_bytes = (uint32_t)scan_box(NQ / 2) * kBlockK * 2;
+  return scan_layout(3, b_bytes, p.JP, NQ, 2, KT, 2).total <= kSmemLimit ? 2 : 1;
+}
+
 int scan_stages(const Pool& p, int nq, int KT) {
   const int cg = scan_cg(nq);
   if (nq < 1 || nq > kBlockM * cg || KT > 32 || (cg == 2 && KT != 8)) return 0;
   const int NQ = (nq + 31) / 32 * 32;
   if (NQ * KT > kScanListRegs) return 0;   // register lists: (NQ / 32) x KT entries per lane
   const uint32_t b_bytes = (uint32_t)scan_box(NQ / cg) * kBlockK * 2;
+  const int w = scan_w(p, nq, KT);
   for (int st = 6; st >= 3; --st)
-    if (scan_layout(st, b_bytes, p.JP, NQ, cg, KT).total <= kSmemLimit) return st;
+    if (scan_layout(st, b_bytes, p.JP, NQ, cg, KT, w).total <= kSmemLimit) return st;
   return 0;
 }
 
@@ -676,7 +738,9 @@ cudaError_t launch_match_scan(Pool& p, const MatchArgs& a, int32_t S, int32_t gr
     e = cudaMemsetAsync(p.slots, 0, (size_t)a.nq * a.KT * sizeof(uint32_t), s);
     if (e != cudaSuccess) return e;
   }
-  e = a.gated ? launch_scan_g<true>(p, a, prm, box, grid, cg, s) : launch_scan_g<false>(p, a, prm, box, grid, cg, s);
+  const int w = scan_w(p, a.nq, a.KT);
+  e = a.gated ? launch_scan_g<true>(p, a, prm, box, grid, cg, w, s)
+              : launch_scan_g<false>(p, a, prm, box, grid, cg, w, s);
   ++p.launches;
   return e;
 }

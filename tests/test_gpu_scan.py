@@ -185,3 +185,42 @@ def test_survey_batch_and_k_grid(ams, nq):
                 g, plan = run(ams, pool, w.q_emb, w.q_joints, k, cfg.theta, gamma)
                 assert plan["kernel_id"] == (4 if scan_eligible(nq, k) else 1 if nq <= 128 else 2)
                 check_bf16(*g, orc, cfg.theta)
+
+
+@pytest.mark.parametrize("M", [1, 255, 256, 257, 511, 513, 767, 769, 5000, 20011])
+@pytest.mark.parametrize("nq", [129, 200, 256])
+def test_wide_pair_matches_narrow_pair_and_oracle(ams, M, nq):
+    """CTA pairs, 129-256 queries: the wide mode (two 256-row tiles per pipeline stage,
+    single-buffered accumulators) against the oracle and byte-for-byte against the narrow
+    mode (policy bit 2) -- same MMA shape and K order per element, so the same bits.  Pools
+    with an odd tile count leave the last super-tile half past the pool (no loads, no
+    scores); tiny pools give empty splits."""
+    cfg = ams_gen.small_variant("c3", M, nq)
+    w = ams_gen.generate_host(cfg)
+    with ams.Pool(cfg.d, cfg.J, cfg.M, 256, 8) as pool:
+        pool.append(dev_t(w.emb), dev_t(w.joints))
+        for k in (1, 8):
+            for gamma in (0.3, 2.5, INF):
+                orc = oracle.match(w.emb, w.joints, w.q_emb, w.q_joints, k, cfg.theta, gamma)
+                a, pa = run(ams, pool, w.q_emb, w.q_joints, k, cfg.theta, gamma, policy=0)
+                b, pb = run(ams, pool, w.q_emb, w.q_joints, k, cfg.theta, gamma, policy=4)
+                assert pa["kernel_id"] == 4 and pb["kernel_id"] == 4
+                check_bf16(*a, orc, cfg.theta)
+                for x, y in zip(a, b):
+                    assert x.tobytes() == y.tobytes()
+
+
+def test_wide_pair_appends_between_calls(ams):
+    """Appends move L past super-tile boundaries between calls (the split plan and the
+    half-empty last super-tile change every call)."""
+    cfg = ams_gen.small_variant("c5", 3000, 180)
+    w = ams_gen.generate_host(cfg)
+    with ams.Pool(cfg.d, cfg.J, cfg.M, 256, 8) as pool:
+        done = 0
+        for step in (300, 212, 256, 1000, 1232):
+            pool.append(dev_t(w.emb[done:done + step]), dev_t(w.joints[done:done + step]))
+            done += step
+            orc = oracle.match(w.emb[:done], w.joints[:done], w.q_emb, w.q_joints, 8, cfg.theta, INF)
+            a, pa = run(ams, pool, w.q_emb, w.q_joints, 8, cfg.theta, INF)
+            assert pa["kernel_id"] == 4
+            check_bf16(*a, orc, cfg.theta)
