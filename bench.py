@@ -165,7 +165,7 @@ def parse():
     ap.add_argument("--kernel-policy", type=int, default=0, choices=list(range(8)),
                     help="bit mask for A/B measurements: 1 = batches of <= 128 queries use the 128-query-tile "
                          "kernel instead of the small-batch kernel; 2 = two CTA pairs per 4-CTA cluster sharing "
-                         "multicast pool rows (opt-in); 4 = narrow small-batch CTA pairs (one tile per stage)")
+                         "multicast pool rows (opt-in); 4 = wide small-batch CTA pairs (two tiles per stage, opt-in)")
     return ap.parse_args()
 
 

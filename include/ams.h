@@ -429,9 +429,10 @@ ams_status_t ams_pool_launch_count(ams_pool_t pool, int64_t* launches);
  *     4-CTA cluster sharing multicast pool rows (plan id 5) instead of one pair per
  *     cluster (plan id 2).  Opt-in: only the co-resident 4-CTA clusters are launched
  *     (33 = 132 SMs on a B200), which costs more than the multicast saves;
- *   bit 2 set: the small-batch kernel on CTA pairs (129-256 queries, k <= 8) stages one
- *     256-row tile per pipeline stage ("narrow", round 1) instead of two ("wide": every
- *     staged query byte serves twice the pool rows, single-buffered accumulators).
+ *   bit 2 set: the small-batch kernel on CTA pairs (129-256 queries, k <= 8) stages two
+ *     256-row tiles per pipeline stage ("wide": every staged query byte serves twice the
+ *     pool rows, single-buffered accumulators) instead of one ("narrow", the default:
+ *     measured faster).
  * Host-only; takes effect at the next ams_match.  AMS_ERR_INVALID_ARGUMENT for a NULL
  * pool or a policy outside [0, 7]. */
 ams_status_t ams_pool_set_kernel_policy(ams_pool_t pool, int32_t policy);

@@ -20,7 +20,7 @@
 // bf16 per pipeline stage (one 128-B swizzle atom).  TMEM: two accumulator buffers of
 // 2*NQ columns; half h of buffer b at columns b*2NQ + h*NQ, lane = pool row (mod 128).
 //
-// CTA pairs (129-256 queries) are "wide" (W = 2): a pipeline stage carries the pair's
+// CTA pairs (129-256 queries) can run "wide" (W = 2, opt-in): a pipeline stage carries the pair's
 // 128-row halves of TWO consecutive tiles per CTA (two cta_group::2 MMAs, M = 256 each)
 // against one stage of N/2 query rows per CTA, so every query byte staged from L2 serves
 // 512 pool rows instead of 256.  The L2 -> SM operand traffic of a call drops from
@@ -682,10 +682,13 @@ cudaError_t launch_scan_g(Pool& p, const MatchArgs& a, const ScanParams& prm, in
 
 int scan_cg(int nq) { return nq > kBlockM ? 2 : 1; }
 
-// tiles per pipeline stage: 2 on CTA pairs (the wide mode) unless policy bit 2 asks for
-// the narrow pair (A/B measurements) or the wide stages do not fit shared memory
+// tiles per pipeline stage: 2 on CTA pairs only when policy bit 2 asks for the wide mode
+// (opt-in: it cuts the L2 -> SM bytes by 18 % on a 200-query C3 call, but that call is at
+// the ridge -- tensor pipe 64-70 % and DRAM 62 % busy in both modes -- so the narrow
+// pair's double-buffered accumulators win, 0.465 vs 0.491 ms) and if the
+// wide stages fit shared memory
 int scan_w(const Pool& p, int nq, int KT) {
-  if (scan_cg(nq) != 2 || (p.kernel_policy & 4) != 0) return 1;
+  if (scan_cg(nq) != 2 || (p.kernel_policy & 4) == 0) return 1;
   const int NQ = (nq + 31) / 32 * 32;
   const uint32_t b_bytes = (uint32_t)scan_box(NQ / 2) * kBlockK * 2;
   return scan_layout(3, b_bytes, p.JP, NQ, 2, KT, 2).total <= kSmemLimit ? 2 : 1;

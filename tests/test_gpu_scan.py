@@ -190,9 +190,9 @@ def test_survey_batch_and_k_grid(ams, nq):
 @pytest.mark.parametrize("M", [1, 255, 256, 257, 511, 513, 767, 769, 5000, 20011])
 @pytest.mark.parametrize("nq", [129, 200, 256])
 def test_wide_pair_matches_narrow_pair_and_oracle(ams, M, nq):
-    """CTA pairs, 129-256 queries: the wide mode (two 256-row tiles per pipeline stage,
-    single-buffered accumulators) against the oracle and byte-for-byte against the narrow
-    mode (policy bit 2) -- same MMA shape and K order per element, so the same bits.  Pools
+    """CTA pairs, 129-256 queries: the wide mode (policy bit 2: two 256-row tiles per
+    pipeline stage, single-buffered accumulators) against the oracle and byte-for-byte
+    against the narrow default -- same MMA shape and K order per element, so the same bits.  Pools
     with an odd tile count leave the last super-tile half past the pool (no loads, no
     scores); tiny pools give empty splits."""
     cfg = ams_gen.small_variant("c3", M, nq)
@@ -202,8 +202,8 @@ def test_wide_pair_matches_narrow_pair_and_oracle(ams, M, nq):
         for k in (1, 8):
             for gamma in (0.3, 2.5, INF):
                 orc = oracle.match(w.emb, w.joints, w.q_emb, w.q_joints, k, cfg.theta, gamma)
-                a, pa = run(ams, pool, w.q_emb, w.q_joints, k, cfg.theta, gamma, policy=0)
-                b, pb = run(ams, pool, w.q_emb, w.q_joints, k, cfg.theta, gamma, policy=4)
+                a, pa = run(ams, pool, w.q_emb, w.q_joints, k, cfg.theta, gamma, policy=4)
+                b, pb = run(ams, pool, w.q_emb, w.q_joints, k, cfg.theta, gamma, policy=0)
                 assert pa["kernel_id"] == 4 and pb["kernel_id"] == 4
                 check_bf16(*a, orc, cfg.theta)
                 for x, y in zip(a, b):
@@ -221,6 +221,7 @@ def test_wide_pair_appends_between_calls(ams):
             pool.append(dev_t(w.emb[done:done + step]), dev_t(w.joints[done:done + step]))
             done += step
             orc = oracle.match(w.emb[:done], w.joints[:done], w.q_emb, w.q_joints, 8, cfg.theta, INF)
-            a, pa = run(ams, pool, w.q_emb, w.q_joints, 8, cfg.theta, INF)
-            assert pa["kernel_id"] == 4
-            check_bf16(*a, orc, cfg.theta)
+            for pol in (0, 4):
+                a, pa = run(ams, pool, w.q_emb, w.q_joints, 8, cfg.theta, INF, policy=pol)
+                assert pa["kernel_id"] == 4
+                check_bf16(*a, orc, cfg.theta)
