@@ -106,3 +106,26 @@ def test_c3_deterministic(ams, c3):
     b = [t.cpu().numpy() for t in pool.match(q, qj, cfg.k, cfg.theta, INF)]
     for x, y in zip(a, b):
         assert x.tobytes() == y.tobytes()
+
+
+def test_c3_full_size_wide_gate_lists_fill(ams, c3):
+    """gamma = 4.0 on C3's 14-DoF pool: ~200 eligible rows per query (gamma = 3.5 measured
+    a median of ~30, 74 % of queries >= 16), so nearly every gated top-16 list fills and the gated top-k machinery (sorted batch, warp-box filter, exact gate,
+    register lists, shared bounds, merge) is checked beyond the top-1 -- on the full
+    16,384-query call (CTA pairs) and the 64-query scan (small-batch kernel)."""
+    cfg, pool, q, qj, labels, host_e, host_j = c3
+    gamma = 4.0
+    qn = q.view(torch.int16).cpu().numpy().view(np.uint16)
+    qjn = qj.cpu().numpy()
+    gi, gs, gh = (t.cpu().numpy() for t in pool.match(q, qj, cfg.k, cfg.theta, gamma))
+    assert ams.ams_pool_last_plan(pool.handle)["kernel_id"] == 2
+    sel = np.arange(5, cfg.Q, cfg.Q // 512)[:512]
+    orc = oracle.match(host_e, host_j, qn[sel], qjn[sel], cfg.k, cfg.theta, gamma, mode="B")
+    assert (orc.nelig >= cfg.k).mean() > 0.8          # the lists really fill
+    stats = check_bf16(gi[sel], gs[sel], gh[sel], orc, cfg.theta)
+    assert stats["rank_checks"] > 0
+    si, ss, sh = (t.cpu().numpy() for t in pool.match(q[:64].contiguous(), qj[:64].contiguous(), cfg.k,
+                                                       cfg.theta, gamma))
+    assert ams.ams_pool_last_plan(pool.handle)["kernel_id"] == 4
+    orc64 = oracle.match(host_e, host_j, qn[:64], qjn[:64], cfg.k, cfg.theta, gamma, mode="B")
+    check_bf16(si, ss, sh, orc64, cfg.theta)

@@ -84,7 +84,7 @@ def test_largest_configs_sampled(ams, name):
     qn = q.view(torch.int16).cpu().numpy().view(np.uint16)
     qjn = qj.cpu().numpy()
     sel_g = np.arange(0, cfg.Q, max(1, cfg.Q // 64))[:64]
-    sel_u = np.arange(3, cfg.Q, max(1, cfg.Q // 8))[:8]
+    sel_u = np.arange(3, cfg.Q, max(1, cfg.Q // 32))[:32]
     og, ou = streamed_oracle(cfg, dev, qn, qjn, [(sel_g, cfg.gamma, "B"), (sel_u, INF, "A")])
     check_bf16(gi[sel_g], gs[sel_g], gh[sel_g], og, cfg.theta)
     check_bf16(ui[sel_u], us[sel_u], uh[sel_u], ou, cfg.theta)
