@@ -106,10 +106,11 @@ bool encode_bf16_map(CUtensorMap* m, void* base, int64_t rows, int32_t d, uint32
   return r == CUDA_SUCCESS;
 }
 
-// small-batch kernel: query tiles of exactly 16, 32, ..., 128 rows (box i = 16 (i + 1))
+// small-batch kernel: query tiles of exactly 8, 16, ..., 128 rows (box i = 8 (i + 1)): the
+// MMA's N (queries rounded up to 16) on one CTA, or its half on a CTA pair
 bool encode_query_boxes(ams::Pool& p, int32_t d) {
-  for (int i = 0; i < 8; ++i)
-    if (!encode_bf16_map(&p.tmap_qs[i], p.q_stage, p.q_pad, d, (uint32_t)(16 * (i + 1)))) return false;
+  for (int i = 0; i < 16; ++i)
+    if (!encode_bf16_map(&p.tmap_qs[i], p.q_stage, p.q_pad, d, (uint32_t)(8 * (i + 1)))) return false;
   return true;
 }
 

@@ -144,7 +144,7 @@ struct Pool {
   CUtensorMap tmap_pool2{};  // bf16 pool [cap_pad, d], box {64, 128}, SW128 (CTA-pair half tile)
   CUtensorMap tmap_pool4{};  // bf16 pool [cap_pad, d], box {64, 64}, SW128 (multicast quarter tile)
   CUtensorMap tmap_q{};      // bf16 queries [q_pad, d], box {64, 128}, SW128
-  CUtensorMap tmap_qs[8]{};  // bf16 queries [q_pad, d], box {64, 16 (i + 1)}, SW128 (small-batch kernel)
+  CUtensorMap tmap_qs[16]{}; // bf16 queries [q_pad, d], box {64, 8 (i + 1)}, SW128 (small-batch kernel)
   int32_t kernel_policy = 0; // bit 0: never the small-batch kernel; bit 1: 4-CTA multicast clusters;
                              // bit 2: wide (two tiles per stage) small-batch CTA pairs
 

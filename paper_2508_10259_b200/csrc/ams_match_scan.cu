@@ -80,7 +80,8 @@ struct ScanParams {
   float* glist_s;            // CG = 2: per (CTA, epilogue warp) lists [slot][KT][32 lanes]
   int32_t* glist_i;
   int64_t L;                 // local rows
-  int32_t nq, NQ, d, n_pt, S, P, stages, k;
+  int32_t nq, NQ, NM, d, n_pt, S, P, stages, k;   // NQ = round_up(nq, 32): epilogue slots / TMEM
+                                                  // layout; NM = round_up(nq, 16): the MMA's N
   uint32_t b_bytes;          // query stage bytes (box rows x 128 B)
   uint32_t idesc;            // kind::f16, M = 128, N = NQ
   float g2;
@@ -212,7 +213,7 @@ __global__ void __launch_bounds__(kScanThreads, 1)
     const uint64_t pol_pool = ptx::policy_evict_first();   // every pool byte is read once
     const uint32_t tx = ABYTES + prm.b_bytes;
     const uint32_t full_leader0 = CG == 2 ? ptx::mapa(ptx::smem_u32(&full[0]), 0) : 0u;
-    const int qrow0 = (int)crank * (NQ / CG);   // this CTA's query rows (the B half)
+    const int qrow0 = (int)crank * (prm.NM / CG);   // this CTA's query rows (the B half)
     int stage = 0;
     uint32_t phase = 0, tile_count = 0;
     for (int u = cid; u < prm.S; u += ncl) {
@@ -634,7 +635,11 @@ __global__ void __launch_bounds__(kScanThreads, 1)
 // Query-tile box (TMA rows) = exactly the B rows a CTA's MMA reads (N for one CTA, N/2 on
 // a CTA pair; a multiple of 16 <= 128): no query rows are staged that the MMA skips.
 int scan_box(int rows) { return rows; }
-int box_index(int box) { return box / 16 - 1; }
+int box_index(int box) { return box / 8 - 1; }
+// MMA N: queries rounded up to 16 (the instruction's granularity), not to the epilogue's
+// 32-query slots -- TMEM columns [NM, NQ) of a half are never written and belong to
+// inactive queries only
+int scan_nm(int nq) { return (nq + 15) / 16 * 16; }
 
 template <int KT, int JP, bool G, int CG, int W>
 cudaError_t launch_scan_t(Pool& p, const ScanParams& prm, int box, int grid, cudaStream_t s) {
@@ -690,7 +695,7 @@ int scan_cg(int nq) { return nq > kBlockM ? 2 : 1; }
 int scan_w(const Pool& p, int nq, int KT) {
   if (scan_cg(nq) != 2 || (p.kernel_policy & 4) == 0) return 1;
   const int NQ = (nq + 31) / 32 * 32;
-  const uint32_t b_bytes = (uint32_t)scan_box(NQ / 2) * kBlockK * 2;
+  const uint32_t b_bytes = (uint32_t)scan_box(scan_nm(nq) / 2) * kBlockK * 2;
   return scan_layout(3, b_bytes, p.JP, NQ, 2, KT, 2).total <= kSmemLimit ? 2 : 1;
 }
 
@@ -699,7 +704,7 @@ int scan_stages(const Pool& p, int nq, int KT) {
   if (nq < 1 || nq > kBlockM * cg || KT > 32 || (cg == 2 && KT != 8)) return 0;
   const int NQ = (nq + 31) / 32 * 32;
   if (NQ * KT > kScanListRegs) return 0;   // register lists: (NQ / 32) x KT entries per lane
-  const uint32_t b_bytes = (uint32_t)scan_box(NQ / cg) * kBlockK * 2;
+  const uint32_t b_bytes = (uint32_t)scan_box(scan_nm(nq) / cg) * kBlockK * 2;
   const int w = scan_w(p, nq, KT);
   for (int st = 6; st >= 3; --st)
     if (scan_layout(st, b_bytes, p.JP, NQ, cg, KT, w).total <= kSmemLimit) return st;
@@ -710,7 +715,8 @@ cudaError_t launch_match_scan(Pool& p, const MatchArgs& a, int32_t S, int32_t gr
   ScanParams prm{};
   const int cg = scan_cg(a.nq);
   const int NQ = (a.nq + 31) / 32 * 32;
-  const int box = scan_box(NQ / cg);
+  const int NM = scan_nm(a.nq);
+  const int box = scan_box(NM / cg);
   prm.inv_q = p.q_inv;
   prm.q_joints = p.q_joints;
   prm.pool_inv = p.inv_norm;
@@ -721,13 +727,14 @@ cudaError_t launch_match_scan(Pool& p, const MatchArgs& a, int32_t S, int32_t gr
   prm.L = p.local;
   prm.nq = a.nq;
   prm.NQ = NQ;
+  prm.NM = NM;
   prm.d = p.cfg.dim;
   prm.n_pt = (int32_t)((p.local + kBlockN - 1) / kBlockN);
   prm.S = S;
   prm.P = S * scan_lists_per_split(a.nq, a.KT, a.gated != 0);
   prm.stages = scan_stages(p, a.nq, a.KT);
   prm.b_bytes = (uint32_t)box * kBlockK * 2;
-  prm.idesc = ptx::idesc_bf16_f32(kBlockM * cg, (uint32_t)NQ);
+  prm.idesc = ptx::idesc_bf16_f32(kBlockM * cg, (uint32_t)NM);
   prm.g2 = a.g2;
   prm.k = a.k;
   if (prm.stages == 0 || grid % cg != 0) return cudaErrorInvalidValue;
