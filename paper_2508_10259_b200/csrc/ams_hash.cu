@@ -561,21 +561,31 @@ ams_status_t ams_hash_actions(ams_hasher_t h, const uint8_t* data, const int64_t
   int64_t* off = h->h_pinned + (size_t)b * 2 * (h->max_inputs + 1);
   int64_t* base = off + (h->max_inputs + 1);
   int64_t nseg = 0, ntc = 0;
-  for (int32_t i = 0; i <= n_inputs; ++i) {
-    off[i] = device_data ? offsets[i] : offsets[i] - offsets[0];
-    if (i > 0 && offsets[i] < offsets[i - 1]) return AMS_ERR_INVALID_ARGUMENT;
-  }
+  const uint8_t* src = (total > 0 && !device_data) ? h->d_stage : data;
+  // one pass: rebased offsets, monotonicity, segment bases and the tensor-core segment
+  // count (shifts for a power-of-two s: this loop is the per-call cost of hashing many
+  // tiny actions)
+  const int64_t s_len = h->s;
+  const bool pow2 = (s_len & (s_len - 1)) == 0;
+  const int sh = pow2 ? __builtin_ctzll((unsigned long long)s_len) : 0;
+  const int64_t o0 = device_data ? 0 : offsets[0];
+  const uintptr_t src_addr = reinterpret_cast<uintptr_t>(src);
+  const bool tc = h->d_wgt != nullptr;   // full 16-B aligned segments go to the tensor-core kernel
+  int64_t prev = offsets[0];
   for (int32_t i = 0; i < n_inputs; ++i) {
+    const int64_t o = prev, o1 = offsets[i + 1];
+    if (o1 < o) return AMS_ERR_INVALID_ARGUMENT;
+    const int64_t len = o1 - o;
+    off[i] = o - o0;
     base[i] = nseg;
-    nseg += (offsets[i + 1] - offsets[i] + h->s - 1) / h->s;
+    const int64_t full = pow2 ? (len >> sh) : len / s_len;
+    nseg += full + ((len - full * s_len) != 0 ? 1 : 0);
+    if (tc && ((src_addr + (uintptr_t)(o - o0)) & 15u) == 0) ntc += full;
+    prev = o1;
   }
+  off[n_inputs] = offsets[n_inputs] - o0;
   base[n_inputs] = nseg;
   if (nseg > h->max_segs) return AMS_ERR_CAPACITY;
-  const uint8_t* src = (total > 0 && !device_data) ? h->d_stage : data;
-  if (h->d_wgt != nullptr)   // full 16-B aligned segments go to the tensor-core kernel
-    for (int32_t i = 0; i < n_inputs; ++i)
-      if (((reinterpret_cast<uintptr_t>(src) + (uintptr_t)off[i]) & 15u) == 0)
-        ntc += (offsets[i + 1] - offsets[i]) / h->s;
   h->last_segs = nseg;
   h->last_tc_segs = ntc;
   bool ok = cudaMemcpyAsync(h->d_offsets, off, (n_inputs + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s) ==
