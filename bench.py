@@ -19,7 +19,7 @@ across N), ungated (the same batch with gate_radius = inf), scan (the north_star
 through the C ABI, H2D + D2H inside the timed region), peer_exchange (N > 1: the fused
 NVLink exchange of f1, checked bit-identical to the NCCL path), c4 (BASELINE configs[3]
 at every N: the 16.8M-row pool resharded over the N ranks, with its own 64-query scan
-and output hash), cpu_baseline (the oracle on the host cores, a bounded query sample,
+and output hash), c2 (configs[1]), c5 (configs[4] streaming, 20 steps), cpu_baseline (the oracle on the host cores, a bounded query sample,
 CPU model named), clocks (nvidia-smi during the main timed region; every leg carries its
 own window), gpu_launches (our kernels inside the timed region).
 """
@@ -158,6 +158,8 @@ def parse():
     ap.add_argument("--no-variant", action="store_true", help="skip the gate-first side measurement")
     ap.add_argument("--no-ungated", action="store_true", help="skip the ungated (gate_radius = inf) sub-line")
     ap.add_argument("--no-c4", action="store_true", help="skip the configs[3] (C4) block")
+    ap.add_argument("--no-c2", action="store_true", help="skip the configs[1] (C2) block")
+    ap.add_argument("--no-c5", action="store_true", help="skip the configs[4] (C5 streaming, 20 steps) block")
     ap.add_argument("--no-peer", action="store_true", help="skip the fused peer-exchange side measurement (N > 1)")
     ap.add_argument("--force-collective", action="store_true",
                     help="N = 1 only: run the multi-GPU code path (NCCL all-gather, shard merge, peer exchange) "
@@ -245,22 +247,32 @@ def auto_sample(cfg, cores):
 
 
 def run_stream(args):
+    """C5 (configs[4]) streaming record-and-replay as the bench line (--workload c5)."""
+    rank, world, local = dist_setup(args)
+    line = stream_measure(args, args.steps, max(args.warmup, 3), rank, world, local)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as tdist
+        tdist.destroy_process_group()
+
+
+def stream_measure(args, T, W, rank, world, local):
     """C5 (configs[4]) streaming record-and-replay.  A step = one simulated 20 ms robot
     step: ams_pool_append of 256 new contexts, then the step's 256 queries (50 %
     near-duplicates of rows appended <= 50 steps ago or of initial rows, 50 % mixture)
     in seeded batches of 1..256 (log-uniform).  Every ams_match is timed with CUDA
-    events on the launching stream; value = queries/s over the timed steps."""
+    events on the launching stream; value = queries/s over the timed steps.  Returns the
+    line (rank 0) or None."""
     import numpy as np
     import torch
     import ams_gen
     import paper_2508_10259_b200 as ams
     from paper_2508_10259_b200 import dist as adist
 
-    rank, world, local = dist_setup(args)
     cfg = ams_gen.CONFIGS["c5"]
     dev = torch.device("cuda", local)
     peaks = load_peaks()
-    T, W = args.steps, max(args.warmup, 3)
     per_step = 256
     cap = cfg.M + per_step * (T + W)
     block = 256
@@ -365,6 +377,7 @@ def run_stream(args):
     else:
         p50, p99 = float(np.percentile(lat, 50)), float(np.percentile(lat, 99))
     m_now = pool.size
+    line = None
     shard_rows = -(-m_now // world)
     bytes_call = shard_rows * (2 * cfg.d + 4 * cfg.J + 4)
     if args.gate_first:   # the gate-first scan reads the (padded) joints only
@@ -390,11 +403,8 @@ def run_stream(args):
                              "note": "whole ams_match call (prep + scan kernel + merge) at the median batch"},
                 "clocks": clocks, "gpu_launches": launches, "e2e": None, "cpu_baseline": None,
                 "path": "ams_match_gate_first" if args.gate_first else "ams_match (dense tcgen05)"}
-        print(json.dumps(line), flush=True)
     pool.close()
-    if world > 1:
-        import torch.distributed as tdist
-        tdist.destroy_process_group()
+    return line
 
 
 def run_reference(args):
@@ -835,6 +845,55 @@ def main():
         if not args.no_scan:
             c4["scan"] = scan_leg(pool4, c4cfg, q4, qj4, c4cfg.gamma)
         pool4.close()
+    # ------------------------------------------------------------------ C2 (configs[1]) at every N
+    c2 = None
+    if args.workload == "c3" and not args.no_c2:
+        c2cfg = ams_gen.CONFIGS["c2"]
+        w2 = ams_gen.generate_host(c2cfg)
+        pool2 = adist.create_pool(c2cfg.d, c2cfg.J, c2cfg.M, c2cfg.Q, c2cfg.k, dtype="bf16", shard_block=0,
+                                  force_collective=args.force_collective)
+        pool2.append(w2.emb, w2.joints, c2cfg.M)
+        q2 = torch.from_numpy(w2.q_emb).to(dev).view(torch.bfloat16)
+        qj2 = torch.from_numpy(w2.q_joints).to(dev)
+        o2 = (torch.empty(c2cfg.Q, c2cfg.k, dtype=torch.int64, device=dev),
+              torch.empty(c2cfg.Q, c2cfg.k, dtype=torch.float32, device=dev),
+              torch.empty(c2cfg.Q, dtype=torch.uint8, device=dev))
+        fn2 = lambda: ams.ams_match(pool2.handle, q2, qj2, c2cfg.Q, c2cfg.k, c2cfg.theta, c2cfg.gamma, *o2,  # noqa: E731
+                                    stream)
+        for _ in range(5):
+            fn2()
+        torch.cuda.synchronize()
+        ams.ams_pool_read_profile(pool2.handle)
+        ams.ams_pool_set_profiling(pool2.handle, True)
+        reps2 = max(50, 5 * args.steps)
+        c_ms, win = timed(fn2, reps2)
+        ams.ams_pool_set_profiling(pool2.handle, False)
+        k2 = kernel_avg(pool2)
+        fl2 = 2.0 * c2cfg.Q * (-(-c2cfg.M // world)) * c2cfg.d
+        nd2 = w2.labels >= 0
+        c2 = {"workload": "c2 (BASELINE.json configs[1]): M=100,000 d=768 bf16 J=7, Q=4096, k=10, theta 0.92, "
+                          f"gamma 0.3; rows contiguous over {world} rank(s)",
+              "value": c2cfg.Q * reps2 / (c_ms / 1e3), "unit": "queries/s", "steps": reps2, "warmup": 5,
+              "ms_per_step": c_ms / reps2,
+              "roofline": {"bound": "tensor", "achieved": fl2 / (k2 / 1e3) / 1e12, "peak": peaks["bf16_tflops"],
+                           "unit": "TFLOP/s", "frac": fl2 / (k2 / 1e3) / 1e12 / peaks["bf16_tflops"],
+                           "kernel_ms_avg": k2},
+              "hits_equal_near_duplicates": bool(np.array_equal(o2[2].cpu().numpy().astype(bool), nd2)),
+              "outputs_sha256": outputs_sha256(*o2), "clocks": clk.window(*win)}
+        pool2.close()
+
+    # ------------------------------------------------------------------ C5 (configs[4]) streaming
+    c5 = None
+    if args.workload == "c3" and not args.no_c5:
+        w0 = time.time()
+        c5l = stream_measure(args, 20, 3, rank, world, local)
+        if c5l is not None:
+            c5 = {k: c5l[k] for k in ("value", "unit", "ms_per_step", "latency_ms", "step_ms",
+                                      "pool_scan_gbps_per_gpu_p50", "roofline", "clocks", "gpu_launches")}
+            c5["workload"] = c5l["config"]["workload"] + f", {c5l['steps']} timed steps after {c5l['warmup']} warm-up"
+            c5["shard"] = c5l["config"]["shard"]
+            c5["wall_s"] = round(time.time() - w0, 1)
+
     clocks_all = clk.stop()
     clocks = clk.window(*win_main)
 
@@ -846,7 +905,8 @@ def main():
                 "pool_scan_gbps_per_gpu": (bytes_step / world) / (t_ms / args.steps / 1e3) / 1e9,
                 "collective_path": bool(world > 1 or args.force_collective),
                 "roofline": roofline, "outputs_sha256": out_sha, "ungated": ungated, "scan": scan,
-                "gate_first_variant": variant, "auto_route": auto, "e2e": e2e, "peer_exchange": peer, "c4": c4, "cpu_baseline": cpu,
+                "gate_first_variant": variant, "auto_route": auto, "e2e": e2e, "peer_exchange": peer, "c4": c4,
+                "c2": c2, "c5": c5, "cpu_baseline": cpu,
                 "clocks": clocks, "clocks_whole_run": clocks_all,
                 "gpu_launches": launches, "plan": plan, "hit_rate": hit_rate, "path": "ams_match_gate_first"
                 if args.gate_first else "ams_match (dense tcgen05)",

@@ -1,0 +1,16 @@
+# round 2 profile refresh: default bench line, launch list of the bench command, ncu --set full
+# of the dominant kernels (C3 batch K2, C3 64-query scan K2s, hash TC, C4 batch K2) with the
+# library's sha256 recorded next to the reports (bench.py reuses the traffic only for that build)
+set -x
+sha256sum paper_2508_10259_b200/libams.so > gpurun_out/prof_libsha.txt
+timeout 1200 python bench.py > gpurun_out/r02_bench_final.json 2> gpurun_out/r02_bench_final.err; echo "bench rc=$?"
+timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches_r02_c3.csv \
+   python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-c4 > gpurun_out/ncu_launch.log 2>&1; echo "launch rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:match_tc_kernel -c 1 \
+   -o gpurun_out/ncu_r02_c3_match_tc -f python scripts/one_call.py c3 --nq 16384 --k 16 --calls 1 > gpurun_out/ncu_k2.log 2>&1; echo "k2 rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:match_scan_kernel --launch-skip 3 -c 1 \
+   -o gpurun_out/ncu_r02_c3_match_scan -f python scripts/one_call.py c3 --nq 64 --k 16 > gpurun_out/ncu_k2s.log 2>&1; echo "k2s rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:match_scan_kernel --launch-skip 3 -c 1 \
+   -o gpurun_out/ncu_r02_c3_200q_k8_pair -f python scripts/one_call.py c3 --nq 200 --k 8 > gpurun_out/ncu_pair.log 2>&1; echo "pair rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:phase1_tc_kernel -c 1 \
+   -o gpurun_out/ncu_r02_hash_phase1_tc -f python scripts/hash_speed.py > gpurun_out/ncu_hash2.log 2>&1; echo "hash rc=$?"

@@ -74,6 +74,13 @@ def test_null_pool_calls_are_invalid_argument(ams):
     assert ams.lib.ams_pool_set_profiling(None, 1) == 1
     assert ams.lib.ams_pool_last_plan(None, None, None, None, None) == 1
     assert ams.lib.ams_match_gate_first(None, None, None, 1, 1, 0.5, 0.3, None, None, None, None) == 1
+    assert ams.lib.ams_match_auto(None, None, None, 1, 1, 0.5, 0.3, None, None, None, None) == 1
+    assert ams.lib.ams_pool_last_route(None, None, None, None, None) == 1
+    assert ams.lib.ams_pool_status(None) == 1
+    assert ams.lib.ams_pool_enable_peer_exchange(None) == 1
+    assert ams.lib.ams_vstore_compact(None, None) == 1
+    assert ams.lib.ams_hasher_last_stats(None, None, None) == 1
+    assert ams.lib.ams_pool_set_kernel_policy(None, 4) == 1
 
 
 @pytest.mark.parametrize("cap,world,block", [(100, 1, 0), (100, 3, 0), (1000, 8, 0), (1000, 8, 7),
