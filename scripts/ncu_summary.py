@@ -101,7 +101,9 @@ def main():
         for r in rows:
             if r.get("Metric Name") != "gpu__time_duration.sum":
                 continue
-            name = r["Kernel Name"].split("(")[0].split("<")[0].replace("void ", "")
+            name = r["Kernel Name"].replace("(anonymous namespace)::", "").replace("<unnamed>::", "")
+            name = name.split("(")[0].split("<")[0]
+            name = name.replace("void ", "")
             x = float(r["Metric Value"].replace(",", "")) * UNIT_SCALE.get(r["Metric Unit"], 1.0)
             tot[name] += x
             cnt[name] += 1
