@@ -257,13 +257,14 @@ def run_stream(args):
         tdist.destroy_process_group()
 
 
-def stream_measure(args, T, W, rank, world, local):
+def stream_measure(args, T, W, rank, world, local, route=None):
     """C5 (configs[4]) streaming record-and-replay.  A step = one simulated 20 ms robot
     step: ams_pool_append of 256 new contexts, then the step's 256 queries (50 %
     near-duplicates of rows appended <= 50 steps ago or of initial rows, 50 % mixture)
     in seeded batches of 1..256 (log-uniform).  Every ams_match is timed with CUDA
     events on the launching stream; value = queries/s over the timed steps.  Returns the
-    line (rank 0) or None."""
+    line (rank 0) or None.  route: "dense" | "gate_first" | "auto" (default: --gate-first or
+    dense)."""
     import numpy as np
     import torch
     import ams_gen
@@ -273,6 +274,8 @@ def stream_measure(args, T, W, rank, world, local):
     cfg = ams_gen.CONFIGS["c5"]
     dev = torch.device("cuda", local)
     peaks = load_peaks()
+    route = route or ("gate_first" if args.gate_first else "dense")
+    match_fn = {"dense": ams.ams_match, "gate_first": ams.ams_match_gate_first, "auto": ams.ams_match_auto}[route]
     per_step = 256
     cap = cfg.M + per_step * (T + W)
     block = 256
@@ -328,7 +331,7 @@ def stream_measure(args, T, W, rank, world, local):
         for b in sizes:
             if timed:
                 evs[ev_i][0].record(stream)
-            (ams.ams_match_gate_first if args.gate_first else ams.ams_match)(
+            match_fn(
                 pool.handle, q[off:off + b], qj[off:off + b], b, cfg.k, cfg.theta, cfg.gamma, out_i, out_s, out_h,
                 stream)
             if timed:
@@ -380,7 +383,7 @@ def stream_measure(args, T, W, rank, world, local):
     line = None
     shard_rows = -(-m_now // world)
     bytes_call = shard_rows * (2 * cfg.d + 4 * cfg.J + 4)
-    if args.gate_first:   # the gate-first scan reads the (padded) joints only
+    if route == "gate_first":   # the gate-first scan reads the (padded) joints only
         bytes_call = shard_rows * 4 * (4 if cfg.J <= 4 else 8 if cfg.J <= 8 else 16)
     value = per_step * T / (total / 1e3)
     if rank == 0:
@@ -402,7 +405,10 @@ def stream_measure(args, T, W, rank, world, local):
                              "frac": gbs / peaks["hbm_gbs"], "traffic": None,
                              "note": "whole ams_match call (prep + scan kernel + merge) at the median batch"},
                 "clocks": clocks, "gpu_launches": launches, "e2e": None, "cpu_baseline": None,
-                "path": "ams_match_gate_first" if args.gate_first else "ams_match (dense tcgen05)"}
+                "path": {"dense": "ams_match (dense tcgen05)", "gate_first": "ams_match_gate_first",
+                         "auto": "ams_match_auto (route per call by sampled pass-rate)"}[route]}
+        if route == "auto":
+            line["route_last_call"] = ams.ams_pool_last_route(pool.handle)
     pool.close()
     return line
 
@@ -893,6 +899,10 @@ def main():
             c5["workload"] = c5l["config"]["workload"] + f", {c5l['steps']} timed steps after {c5l['warmup']} warm-up"
             c5["shard"] = c5l["config"]["shard"]
             c5["wall_s"] = round(time.time() - w0, 1)
+        # the same loop through ams_match_auto (f3 route selection): the robot-step budget
+        c5a = stream_measure(args, 20, 3, rank, world, local, route="auto")
+        if c5a is not None and c5 is not None:
+            c5["auto_route"] = {k: c5a[k] for k in ("value", "latency_ms", "step_ms", "route_last_call", "clocks")}
 
     clocks_all = clk.stop()
     clocks = clk.window(*win_main)

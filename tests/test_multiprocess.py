@@ -96,3 +96,66 @@ def test_sharded_protocol_world2_equals_unsharded(block):
     assert sum(o[2] for o in out) == 2501
     for rank, res, _ in out:
         assert all(res), (rank, res)
+
+
+def _worker_bench_plumbing(rank, world, port, block, q):
+    """bench.py's make_pool on CPU, without the GPU pool: every rank streams the pool
+    through ams_gen.build_device_workload with the bench's chunk_needed (skip chunks this
+    rank owns no row of) and keeps the rows the library's shard map assigns it."""
+    dist = _init(rank, world, port)
+    import dataclasses
+    import hashlib
+    import torch
+    import ams_gen
+    import paper_2508_10259_b200 as ams
+    from paper_2508_10259_b200 import dist as adist
+    cfg = dataclasses.replace(ams_gen.CONFIGS["c4"], M=3 * ams_gen.CHUNK_ROWS + 1234, Q=64, d=64, components=16)
+    kept = {}
+    state = {"off": 0, "none_owned": 0}
+
+    def append_fn(e, j, n):
+        lo = state["off"]
+        for o in range(lo, lo + n):
+            if ams.ams_shard_locate(cfg.M, world, block, o)[0] == rank:
+                if e is None:
+                    state["none_owned"] += 1        # a skipped chunk held one of our rows
+                    continue
+                kept[o] = hashlib.sha256(e[o - lo].view(torch.int16).numpy().tobytes() +
+                                         j[o - lo].numpy().tobytes()).hexdigest()
+        state["off"] += n
+
+    need = lambda lo, hi: adist.owned_range_overlaps(cfg.M, world, block, rank, lo, hi)  # noqa: E731
+    qe, qj, lab = ams_gen.build_device_workload(cfg, torch.device("cpu"), append_fn, chunk_needed=need)
+    qh = hashlib.sha256(qe.view(torch.int16).numpy().tobytes() + qj.numpy().tobytes() + lab.numpy().tobytes())
+    q.put((rank, kept, state["none_owned"], state["off"], qh.hexdigest()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,block", [(2, 0), (3, 0), (2, 256), (3, 256)])
+def test_bench_sharded_generation_world(world, block):
+    """The multi-rank data plumbing of bench.py (what the driver's SCALE run executes
+    before any kernel): the union of the rows the ranks keep is the single-rank pool, row
+    for row; no rank skips a chunk that holds one of its rows; queries are identical on
+    every rank."""
+    import dataclasses
+    import hashlib
+    import torch
+    import ams_gen
+    out = _run(_worker_bench_plumbing, world, block)
+    cfg = dataclasses.replace(ams_gen.CONFIGS["c4"], M=3 * ams_gen.CHUNK_ROWS + 1234, Q=64, d=64, components=16)
+    full = {}
+    off = [0]
+
+    def append_all(e, j, n):
+        for r in range(n):
+            full[off[0] + r] = hashlib.sha256(e[r].view(torch.int16).numpy().tobytes() + j[r].numpy().tobytes()).hexdigest()
+        off[0] += n
+
+    qe, qj, lab = ams_gen.build_device_workload(cfg, torch.device("cpu"), append_all)
+    qh = hashlib.sha256(qe.view(torch.int16).numpy().tobytes() + qj.numpy().tobytes() + lab.numpy().tobytes())
+    union = {}
+    for rank, kept, none_owned, total, h in out:
+        assert none_owned == 0 and total == cfg.M and h == qh.hexdigest(), rank
+        assert not (set(union) & set(kept))
+        union.update(kept)
+    assert union == full
