@@ -600,10 +600,21 @@ __global__ void __launch_bounds__(kScanThreads, 1)
           const int64_t base = MERGE4 ? ((int64_t)c * prm.P + u) * KT
                                       : ((int64_t)c * prm.P + ((int64_t)u * CG + crank) * kScanEpiWarps + lg) * KT;
           if constexpr (SMEM_LISTS) {
+            // a list nothing ever entered (the common gated case) is padding: no reads; a
+            // used one is read whole into registers first (the loads are independent of the
+            // partial-list stores, so they are all in flight at once), then stored 16 B wide
+            float ts[KT];
+            int32_t ti[KT];
+            const bool used = best_s[sl] > -CUDART_INF_F;
 #pragma unroll
             for (int rr = 0; rr < KT; ++rr) {
-              prm.part_s[base + rr] = wls[(sl * KT + rr) * 32 + lane];
-              prm.part_i[base + rr] = wli[(sl * KT + rr) * 32 + lane];
+              ts[rr] = used ? __ldcg(wls + (sl * KT + rr) * 32 + lane) : -CUDART_INF_F;
+              ti[rr] = used ? __ldcg(wli + (sl * KT + rr) * 32 + lane) : -1;
+            }
+#pragma unroll
+            for (int rr = 0; rr < KT; rr += 4) {
+              *reinterpret_cast<float4*>(prm.part_s + base + rr) = make_float4(ts[rr], ts[rr + 1], ts[rr + 2], ts[rr + 3]);
+              *reinterpret_cast<int4*>(prm.part_i + base + rr) = make_int4(ti[rr], ti[rr + 1], ti[rr + 2], ti[rr + 3]);
             }
           } else {
 #pragma unroll
