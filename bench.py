@@ -164,10 +164,11 @@ def parse():
     ap.add_argument("--force-collective", action="store_true",
                     help="N = 1 only: run the multi-GPU code path (NCCL all-gather, shard merge, peer exchange) "
                          "over a 1-rank communicator -- a dry run of what --gpus N > 1 executes")
-    ap.add_argument("--kernel-policy", type=int, default=0, choices=list(range(8)),
+    ap.add_argument("--kernel-policy", type=int, default=0, choices=list(range(16)),
                     help="bit mask for A/B measurements: 1 = batches of <= 128 queries use the 128-query-tile "
                          "kernel instead of the small-batch kernel; 2 = two CTA pairs per 4-CTA cluster sharing "
-                         "multicast pool rows (opt-in); 4 = wide small-batch CTA pairs (two tiles per stage, opt-in)")
+                         "multicast pool rows (opt-in); 4 = wide small-batch CTA pairs (two tiles per stage, opt-in); 8 = ungated 129-256-query "
+                         "batches on the small-batch CTA pairs")
     return ap.parse_args()
 
 

@@ -432,9 +432,11 @@ ams_status_t ams_pool_launch_count(ams_pool_t pool, int64_t* launches);
  *   bit 2 set: the small-batch kernel on CTA pairs (129-256 queries, k <= 8) stages two
  *     256-row tiles per pipeline stage ("wide": every staged query byte serves twice the
  *     pool rows, single-buffered accumulators) instead of one ("narrow", the default:
- *     measured faster).
+ *     measured faster);
+ *   bit 3 set: ungated batches of 129-256 queries (k <= 8) also use the small-batch CTA
+ *     pairs (by default they take the 256-query-tile kernel, measured faster ungated).
  * Host-only; takes effect at the next ams_match.  AMS_ERR_INVALID_ARGUMENT for a NULL
- * pool or a policy outside [0, 7]. */
+ * pool or a policy outside [0, 15]. */
 ams_status_t ams_pool_set_kernel_policy(ams_pool_t pool, int32_t policy);
 
 ams_status_t ams_pool_last_plan(ams_pool_t pool, int32_t* splits, int32_t* partials,

@@ -263,7 +263,8 @@ def ams_pool_set_kernel_policy(pool: int, policy: int) -> None:
     """Bit mask, 0 = default.  Bit 0: no small-batch kernel (nq <= 128 uses the
     128-query-tile kernel).  Bit 1: 4-CTA clusters of two CTA pairs sharing multicast
     pool rows (opt-in; plan id 5).  Bit 2: wide small-batch CTA pairs (two tiles per
-    pipeline stage instead of one; opt-in)."""
+    pipeline stage instead of one; opt-in).  Bit 3: ungated 129-256-query batches on the
+    small-batch CTA pairs (default: the 256-query-tile kernel)."""
     _check(lib.ams_pool_set_kernel_policy(pool, int(policy)), "ams_pool_set_kernel_policy")
 
 

@@ -623,7 +623,12 @@ static ams_status_t match_impl(ams_pool_t pool, const void* q_emb, const float* 
   // test then rejects most columns for all 32 queries of a warp at once).  The order is
   // invisible to the caller: partial lists land at the caller's query index.
   // The small-batch kernel (pool rows on the MMA M side) needs no query order.
+  // Ungated batches of 129-256 queries stay on the 256-query-tile kernel: the CTA-pair
+  // small-batch kernel keeps its lists in global memory, and without a gate every list
+  // fills and is re-read on inserts (C3 pool, k = 8: 0.63-0.88 ms vs 0.455 ms; gated it
+  // is the faster one, 0.36-0.46 ms).  Policy bit 3 keeps them on the CTA pairs (A/B).
   const bool use_scan = !gate_first && p.cfg.dtype == AMS_DTYPE_BF16 && p.local > 0 && (p.kernel_policy & 1) == 0 &&
+                        (nq <= ams::kBlockM || a.gated || (p.kernel_policy & 8) != 0) &&
                         ams::scan_stages(p, nq, a.KT) > 0 &&
                         (int64_t)nq * ams::scan_lists_per_split(nq, a.KT, a.gated != 0) * a.KT <= p.part_cap;   // >= 1 split fits
   const bool sorted = p.cfg.dtype == AMS_DTYPE_BF16 && a.gated && p.local > 0 && nq >= kSortMinQueries && !use_scan;
@@ -966,7 +971,7 @@ ams_status_t ams_pool_launch_count(ams_pool_t pool, int64_t* launches) {
 }
 
 ams_status_t ams_pool_set_kernel_policy(ams_pool_t pool, int32_t policy) {
-  if (pool == nullptr || policy < 0 || policy > 7) return AMS_ERR_INVALID_ARGUMENT;
+  if (pool == nullptr || policy < 0 || policy > 15) return AMS_ERR_INVALID_ARGUMENT;
   pool->p.kernel_policy = policy;
   return AMS_OK;
 }

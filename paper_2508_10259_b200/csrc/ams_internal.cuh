@@ -146,7 +146,8 @@ struct Pool {
   CUtensorMap tmap_q{};      // bf16 queries [q_pad, d], box {64, 128}, SW128
   CUtensorMap tmap_qs[16]{}; // bf16 queries [q_pad, d], box {64, 8 (i + 1)}, SW128 (small-batch kernel)
   int32_t kernel_policy = 0; // bit 0: never the small-batch kernel; bit 1: 4-CTA multicast clusters;
-                             // bit 2: wide (two tiles per stage) small-batch CTA pairs
+                             // bit 2: wide (two tiles per stage) small-batch CTA pairs;
+                             // bit 3: ungated 129-256-query batches on the small-batch CTA pairs
 
   void* nccl_comm = nullptr;  // ncclComm_t
 

@@ -30,7 +30,7 @@ cfg = ams_gen.small_variant("c3", 1300, 200)
 w = ams_gen.generate_host(cfg)
 with ams.Pool(cfg.d, cfg.J, cfg.M, cfg.Q, 8) as pool:
     pool.append(T(w.emb), T(w.joints))
-    for nq, pol in ((60, 0), (200, 0), (200, 4)):
+    for nq, pol in ((60, 0), (200, 8), (200, 12)):
         ams.ams_pool_set_kernel_policy(pool.handle, pol)
         for gamma in (0.3, 3.5, INF):
             out = pool.match(T(w.q_emb[:nq]), T(w.q_joints[:nq]), 8, cfg.theta, gamma)

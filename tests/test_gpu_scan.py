@@ -31,13 +31,13 @@ def dev_t(a):
     return torch.from_numpy(np.ascontiguousarray(a)).to(torch.device("cuda", 0))
 
 
-def scan_eligible(nq, k):
+def scan_eligible(nq, k, gated=True, policy=0):
     """The library's rule: KT <= 32 and round_up(nq, 32) * KT <= 2048 (the per-lane
     register lists); nq <= 128 on one CTA per tile, 128 < nq <= 256 on a CTA pair with
-    KT = 8 only."""
+    KT = 8 only, gated (ungated ones take the 256-query-tile kernel unless policy bit 3)."""
     KT = 8 if k <= 8 else 16 if k <= 16 else 32 if k <= 32 else 64
     if nq > 128:
-        return nq <= 256 and KT == 8
+        return nq <= 256 and KT == 8 and (gated or (policy & 8) != 0)
     return KT <= 32 and -(-nq // 32) * 32 * KT <= 2048
 
 
@@ -59,7 +59,7 @@ def test_scan_kernel_parity(ams, name, M, nq):
         for gamma in (cfg.gamma, 1.5, INF):
             orc = oracle.match(w.emb, w.joints, w.q_emb, w.q_joints, cfg.k, cfg.theta, gamma)
             g, plan = run(ams, pool, w.q_emb, w.q_joints, cfg.k, cfg.theta, gamma)
-            assert plan["kernel_id"] == (4 if scan_eligible(nq, cfg.k) else 1 if nq <= 128 else 2)
+            assert plan["kernel_id"] == (4 if scan_eligible(nq, cfg.k, gamma != INF) else 1 if nq <= 128 else 2)
             stats = check_bf16(*g, orc, cfg.theta)
             if gamma == cfg.gamma:
                 assert np.array_equal(g[2].astype(bool), w.labels >= 0)   # P10 by construction
@@ -97,7 +97,7 @@ def test_scan_kernel_tiny_and_ragged_pools(ams, M, nq):
         for k in ((1, 16) if nq <= 128 else (1, 8)):
             for gamma in (0.3, INF):
                 orc = oracle.match(w.emb, w.joints, w.q_emb, w.q_joints, k, cfg.theta, gamma)
-                g, plan = run(ams, pool, w.q_emb, w.q_joints, k, cfg.theta, gamma)
+                g, plan = run(ams, pool, w.q_emb, w.q_joints, k, cfg.theta, gamma, policy=8)
                 assert plan["kernel_id"] == 4
                 check_bf16(*g, orc, cfg.theta)
 
@@ -183,7 +183,7 @@ def test_survey_batch_and_k_grid(ams, nq):
             for gamma in (cfg.gamma, INF):
                 orc = oracle.match(w.emb, w.joints, w.q_emb, w.q_joints, k, cfg.theta, gamma)
                 g, plan = run(ams, pool, w.q_emb, w.q_joints, k, cfg.theta, gamma)
-                assert plan["kernel_id"] == (4 if scan_eligible(nq, k) else 1 if nq <= 128 else 2)
+                assert plan["kernel_id"] == (4 if scan_eligible(nq, k, gamma != INF) else 1 if nq <= 128 else 2)
                 check_bf16(*g, orc, cfg.theta)
 
 
@@ -202,8 +202,8 @@ def test_wide_pair_matches_narrow_pair_and_oracle(ams, M, nq):
         for k in (1, 8):
             for gamma in (0.3, 2.5, INF):
                 orc = oracle.match(w.emb, w.joints, w.q_emb, w.q_joints, k, cfg.theta, gamma)
-                a, pa = run(ams, pool, w.q_emb, w.q_joints, k, cfg.theta, gamma, policy=4)
-                b, pb = run(ams, pool, w.q_emb, w.q_joints, k, cfg.theta, gamma, policy=0)
+                a, pa = run(ams, pool, w.q_emb, w.q_joints, k, cfg.theta, gamma, policy=4 | 8)
+                b, pb = run(ams, pool, w.q_emb, w.q_joints, k, cfg.theta, gamma, policy=8)
                 assert pa["kernel_id"] == 4 and pb["kernel_id"] == 4
                 check_bf16(*a, orc, cfg.theta)
                 for x, y in zip(a, b):
@@ -221,7 +221,23 @@ def test_wide_pair_appends_between_calls(ams):
             pool.append(dev_t(w.emb[done:done + step]), dev_t(w.joints[done:done + step]))
             done += step
             orc = oracle.match(w.emb[:done], w.joints[:done], w.q_emb, w.q_joints, 8, cfg.theta, INF)
-            for pol in (0, 4):
+            for pol in (8, 4 | 8):
                 a, pa = run(ams, pool, w.q_emb, w.q_joints, 8, cfg.theta, INF, policy=pol)
                 assert pa["kernel_id"] == 4
                 check_bf16(*a, orc, cfg.theta)
+
+
+def test_ungated_pair_batches_route_to_tile_kernel(ams):
+    """Ungated 129-256-query batches take the 256-query-tile kernel by default (plan id 2),
+    the small-batch CTA pairs with policy bit 3; both agree with the oracle."""
+    cfg = ams_gen.small_variant("c3", 4001, 200)
+    w = ams_gen.generate_host(cfg)
+    with ams.Pool(cfg.d, cfg.J, cfg.M, 256, 8) as pool:
+        pool.append(dev_t(w.emb), dev_t(w.joints))
+        orc = oracle.match(w.emb, w.joints, w.q_emb, w.q_joints, 8, cfg.theta, INF)
+        for pol, kid in ((0, 2), (8, 4)):
+            g, plan = run(ams, pool, w.q_emb, w.q_joints, 8, cfg.theta, INF, policy=pol)
+            assert plan["kernel_id"] == kid
+            check_bf16(*g, orc, cfg.theta)
+        g, plan = run(ams, pool, w.q_emb, w.q_joints, 8, cfg.theta, 0.3)   # gated: the pairs
+        assert plan["kernel_id"] == 4
