@@ -19,7 +19,8 @@ across N), ungated (the same batch with gate_radius = inf), scan (the north_star
 through the C ABI, H2D + D2H inside the timed region), peer_exchange (N > 1: the fused
 NVLink exchange of f1, checked bit-identical to the NCCL path), c4 (BASELINE configs[3]
 at every N: the 16.8M-row pool resharded over the N ranks, with its own 64-query scan
-and output hash), c2 (configs[1]), c5 (configs[4] streaming, 20 steps), cpu_baseline (the oracle on the host cores, a bounded query sample,
+and output hash), c2 (configs[1]), c5 (configs[4] streaming, 20 steps), scaling_sim (N = 1:
+per-GPU shard timings of C3 and C4 at 2/4/8 ranks predicting strong scaling), cpu_baseline (the oracle on the host cores, a bounded query sample,
 CPU model named), clocks (nvidia-smi during the main timed region; every leg carries its
 own window), gpu_launches (our kernels inside the timed region).
 """
@@ -160,6 +161,8 @@ def parse():
     ap.add_argument("--no-c4", action="store_true", help="skip the configs[3] (C4) block")
     ap.add_argument("--no-c2", action="store_true", help="skip the configs[1] (C2) block")
     ap.add_argument("--no-c5", action="store_true", help="skip the configs[4] (C5 streaming, 20 steps) block")
+    ap.add_argument("--no-scaling-sim", action="store_true",
+                    help="N = 1 only: skip the per-GPU shard timings that predict 2/4/8-GPU strong scaling")
     ap.add_argument("--no-peer", action="store_true", help="skip the fused peer-exchange side measurement (N > 1)")
     ap.add_argument("--force-collective", action="store_true",
                     help="N = 1 only: run the multi-GPU code path (NCCL all-gather, shard merge, peer exchange) "
@@ -583,6 +586,40 @@ def main():
         assert pool.size == c.M
         return pool, q, qj, labels
 
+    def shard_sim(c, q, qj, n_shards, reps):
+        """Per-GPU step time of an n_shards-way run, predicted on this one GPU: a pool
+        holding exactly rank 0's contiguous shard (rows [0, ceil(M/n))) through the world > 1
+        code path (1-rank NCCL communicator: shard merge, all-gather, final merge), the full
+        query batch.  Excludes only the cross-GPU transfer of the all-gather (G x nq x k x 12
+        B, ~3 MB at G = 8 for C3)."""
+        m_sh = -(-c.M // n_shards)
+        pool_s = adist.create_pool(c.d, c.J, m_sh, c.Q, c.k, dtype="bf16", shard_block=0, force_collective=True)
+        ams.ams_pool_set_kernel_policy(pool_s.handle, args.kernel_policy)
+        means = ams_gen.device_means(c, dev)
+        for ch in range((m_sh + ams_gen.CHUNK_ROWS - 1) // ams_gen.CHUNK_ROWS):
+            e, j = ams_gen.device_pool_chunk(c, ch, means, dev)
+            n = min(e.shape[0], m_sh - ch * ams_gen.CHUNK_ROWS)
+            pool_s.append(e[:n].contiguous(), j[:n].contiguous(), n)
+        o = (torch.empty(c.Q, c.k, dtype=torch.int64, device=dev), torch.empty(c.Q, c.k, dtype=torch.float32, device=dev),
+             torch.empty(c.Q, dtype=torch.uint8, device=dev))
+        fn = lambda: ams.ams_match(pool_s.handle, q, qj, c.Q, c.k, c.theta, c.gamma, *o, stream)  # noqa: E731
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        ms, win = timed(fn, reps)
+        pool_s.close()
+        return ms / reps, clk.window(*win)
+
+    def scaling_sim(c, q, qj, t1_ms, reps):
+        out = {"note": "predicted on 1 GPU: per-GPU step time of rank 0's shard through the world > 1 path "
+                       "(1-rank NCCL); excludes the cross-GPU all-gather transfer. efficiency = t1 / (N * tN)",
+               "t1_ms": t1_ms}
+        for n in (2, 4, 8):
+            t_n, cl = shard_sim(c, q, qj, n, reps)
+            out[f"n{n}"] = {"ms_per_step": t_n, "queries_per_s_per_rank": c.Q / (t_n / 1e3),
+                            "predicted_efficiency": t1_ms / (n * t_n), "clocks": cl}
+        return out
+
     def scan_leg(pool, c, q, qj, g, nq=64):
         """The north_star 64-query HBM-bound scan of pool `c` (per GPU shard)."""
         o = (torch.empty(nq, c.k, dtype=torch.int64, device=dev), torch.empty(nq, c.k, dtype=torch.float32, device=dev),
@@ -817,6 +854,9 @@ def main():
                          f"oracle mode A (fp64 brute force, OpenMP over queries) per ~1M-row chunk + oracle.merge, "
                          f"{dt:.1f} s in the oracle"}
     pool.close()
+    sim3 = None
+    if world == 1 and args.workload == "c3" and not args.no_scaling_sim and not args.gate_first:
+        sim3 = scaling_sim(cfg, q, qj, t_ms / args.steps, args.steps)
     del q, qj
 
     # ------------------------------------------------------------------ C4 (configs[3]) at every N
@@ -852,6 +892,8 @@ def main():
         if not args.no_scan:
             c4["scan"] = scan_leg(pool4, c4cfg, q4, qj4, c4cfg.gamma)
         pool4.close()
+        if world == 1 and not args.no_scaling_sim:
+            c4["scaling_sim"] = scaling_sim(c4cfg, q4, qj4, c_ms / reps4, reps4)
     # ------------------------------------------------------------------ C2 (configs[1]) at every N
     c2 = None
     if args.workload == "c3" and not args.no_c2:
@@ -917,7 +959,7 @@ def main():
                 "collective_path": bool(world > 1 or args.force_collective),
                 "roofline": roofline, "outputs_sha256": out_sha, "ungated": ungated, "scan": scan,
                 "gate_first_variant": variant, "auto_route": auto, "e2e": e2e, "peer_exchange": peer, "c4": c4,
-                "c2": c2, "c5": c5, "cpu_baseline": cpu,
+                "c2": c2, "c5": c5, "scaling_sim": sim3, "cpu_baseline": cpu,
                 "clocks": clocks, "clocks_whole_run": clocks_all,
                 "gpu_launches": launches, "plan": plan, "hit_rate": hit_rate, "path": "ams_match_gate_first"
                 if args.gate_first else "ams_match (dense tcgen05)",

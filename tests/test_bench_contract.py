@@ -14,7 +14,7 @@ def test_bench_help_lists_the_contract_flags():
                          timeout=120)
     assert out.returncode == 0
     for flag in ("--gpus", "--steps", "--warmup", "--impl", "--workload", "--kernel-policy", "--no-c4",
-                 "--force-collective", "--no-peer", "--no-ungated", "--no-c2", "--no-c5"):
+                 "--force-collective", "--no-peer", "--no-ungated", "--no-c2", "--no-c5", "--no-scaling-sim"):
         assert flag in out.stdout
 
 
