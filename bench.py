@@ -19,7 +19,8 @@ across N), ungated (the same batch with gate_radius = inf), scan (the north_star
 through the C ABI, H2D + D2H inside the timed region), peer_exchange (N > 1: the fused
 NVLink exchange of f1, checked bit-identical to the NCCL path), c4 (BASELINE configs[3]
 at every N: the 16.8M-row pool resharded over the N ranks, with its own 64-query scan
-and output hash), c2 (configs[1]), c5 (configs[4] streaming, 20 steps), scaling_sim (N = 1:
+and output hash), c1 (configs[0], fp32 exact), c2 (configs[1]), c5 (configs[4] streaming, 20 steps),
+scaling_sim (N = 1:
 per-GPU shard timings of C3 and C4 at 2/4/8 ranks predicting strong scaling), cpu_baseline (the oracle on the host cores, a bounded query sample,
 CPU model named), clocks (nvidia-smi during the main timed region; every leg carries its
 own window), gpu_launches (our kernels inside the timed region).
@@ -159,7 +160,7 @@ def parse():
     ap.add_argument("--no-variant", action="store_true", help="skip the gate-first side measurement")
     ap.add_argument("--no-ungated", action="store_true", help="skip the ungated (gate_radius = inf) sub-line")
     ap.add_argument("--no-c4", action="store_true", help="skip the configs[3] (C4) block")
-    ap.add_argument("--no-c2", action="store_true", help="skip the configs[1] (C2) block")
+    ap.add_argument("--no-c2", action="store_true", help="skip the configs[1] (C2) and configs[0] (C1) blocks")
     ap.add_argument("--no-c5", action="store_true", help="skip the configs[4] (C5 streaming, 20 steps) block")
     ap.add_argument("--no-scaling-sim", action="store_true",
                     help="N = 1 only: skip the per-GPU shard timings that predict 2/4/8-GPU strong scaling")
@@ -931,6 +932,36 @@ def main():
               "outputs_sha256": outputs_sha256(*o2), "clocks": clk.window(*win)}
         pool2.close()
 
+    # ------------------------------------------------------------------ C1 (configs[0]) fp32 exact, every N
+    c1 = None
+    if args.workload == "c3" and not args.no_c2:
+        c1cfg = ams_gen.CONFIGS["c1"]
+        w1 = ams_gen.generate_host(c1cfg)
+        pool1 = adist.create_pool(c1cfg.d, c1cfg.J, c1cfg.M, c1cfg.Q, c1cfg.k, dtype="fp32", shard_block=0,
+                                  force_collective=args.force_collective)
+        pool1.append(w1.emb, w1.joints, c1cfg.M)
+        q1 = torch.from_numpy(w1.q_emb).to(dev)
+        qj1 = torch.from_numpy(w1.q_joints).to(dev)
+        o1 = (torch.empty(c1cfg.Q, c1cfg.k, dtype=torch.int64, device=dev),
+              torch.empty(c1cfg.Q, c1cfg.k, dtype=torch.float32, device=dev),
+              torch.empty(c1cfg.Q, dtype=torch.uint8, device=dev))
+        fn1 = lambda: ams.ams_match(pool1.handle, q1, qj1, c1cfg.Q, c1cfg.k, c1cfg.theta, c1cfg.gamma, *o1,  # noqa: E731
+                                    stream)
+        for _ in range(10):
+            fn1()
+        torch.cuda.synchronize()
+        reps1 = 2000
+        m1, win = timed(fn1, reps1)
+        nd1 = w1.labels >= 0
+        c1 = {"workload": "c1 (BASELINE.json configs[0]): M=1024 d=512 fp32 J=7, Q=64, k=5, theta 0.9, gamma 0.3 "
+                          "(the bit-exact canonical fp32 path; launch/latency-bound)",
+              "value": c1cfg.Q * reps1 / (m1 / 1e3), "unit": "queries/s", "us_per_call": 1e3 * m1 / reps1,
+              "steps": reps1, "plan": ams.ams_pool_last_plan(pool1.handle),
+              "hits_equal_near_duplicates": bool(np.array_equal(o1[2].cpu().numpy().astype(bool), nd1)),
+              "top1_equals_source": bool(np.array_equal(o1[0][:, 0].cpu().numpy()[nd1], w1.labels[nd1])),
+              "outputs_sha256": outputs_sha256(*o1), "clocks": clk.window(*win)}
+        pool1.close()
+
     # ------------------------------------------------------------------ C5 (configs[4]) streaming
     c5 = None
     if args.workload == "c3" and not args.no_c5:
@@ -959,7 +990,7 @@ def main():
                 "collective_path": bool(world > 1 or args.force_collective),
                 "roofline": roofline, "outputs_sha256": out_sha, "ungated": ungated, "scan": scan,
                 "gate_first_variant": variant, "auto_route": auto, "e2e": e2e, "peer_exchange": peer, "c4": c4,
-                "c2": c2, "c5": c5, "scaling_sim": sim3, "cpu_baseline": cpu,
+                "c1": c1, "c2": c2, "c5": c5, "scaling_sim": sim3, "cpu_baseline": cpu,
                 "clocks": clocks, "clocks_whole_run": clocks_all,
                 "gpu_launches": launches, "plan": plan, "hit_rate": hit_rate, "path": "ams_match_gate_first"
                 if args.gate_first else "ams_match (dense tcgen05)",
