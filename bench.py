@@ -460,27 +460,23 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def lib_sha256() -> str:
-    import hashlib
-    with open(os.path.join(ROOT, "paper_2508_10259_b200", "libams.so"), "rb") as f:
-        return hashlib.sha256(f.read()).hexdigest()
-
-
 def traffic_of(workload: str, which: str):
     """(dram bytes per launch, source) of the dominant kernel from the committed ncu
-    summary -- only if that capture was taken of THIS library build (sha256 of
-    libams.so recorded by scripts/ncu_summary.py); otherwise (None, why)."""
+    summary -- only if that capture was taken of THIS build (the build id -- a hash of the
+    sources, headers and flags compiled into libams.so -- recorded by scripts/ncu_summary.py
+    matches the loaded library's ams_build_id()); otherwise (None, why)."""
+    import paper_2508_10259_b200 as ams
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             e = json.load(f)[workload][which]
     except Exception:
         return None, "no ncu --set full capture of this kernel/workload in profiles/ncu_summary.json"
-    sha = lib_sha256()
-    if e.get("lib_sha256") != sha:
+    bid = ams.ams_build_id()
+    if e.get("build_id") != bid:
         return None, (f"profiles/ncu_summary.json capture ({e.get('round')}, {e.get('report')}) is of another "
-                      f"library build; not reused")
+                      f"build; not reused")
     return e["dram_bytes_per_launch"], (f"ncu --set full capture {e.get('round')} ({e.get('report')}) of this "
-                                        f"library build (libams.so sha256 {sha[:16]}), per launch")
+                                        f"build (ams_build_id {bid[:16]}), per launch")
 
 
 def cpu_model() -> str:

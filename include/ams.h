@@ -242,6 +242,11 @@ ams_status_t ams_exchange_selftest(int32_t G, int32_t nq, int32_t k, int32_t rou
  * Errors: AMS_ERR_INVALID_ARGUMENT (null pool). */
 ams_status_t ams_pool_status(ams_pool_t pool);
 
+/* Identity of this build of the library: a hash of the sources, headers and compile flags
+ * it was built from (static string, never NULL; "unknown" if built without it).  Profiles
+ * record it so a reported DRAM-traffic figure can be tied to the code it measured. */
+const char* ams_build_id(void);
+
 /* ---- two-phase action hash (Algorithm 1) ----
  * Phase 1 hashes every s-byte segment of every input independently, phase 2 folds an
  * input's segment hashes ("modular calculation").

@@ -30,7 +30,7 @@ STATUS = {0: "AMS_OK", 1: "AMS_ERR_INVALID_ARGUMENT", 2: "AMS_ERR_CAPACITY", 3: 
 EXPORTS = ("ams_get_nccl_unique_id", "ams_pool_create", "ams_pool_append", "ams_match", "ams_match_gate_first",
            "ams_match_auto", "ams_pool_last_route",
            "ams_merge_topk", "ams_pool_enable_peer_exchange", "ams_exchange_selftest",
-           "ams_pool_status", "ams_pool_size",
+           "ams_pool_status", "ams_build_id", "ams_pool_size",
            "ams_pool_destroy", "ams_status_string", "ams_pool_set_profiling", "ams_pool_read_profile",
            "ams_pool_launch_count", "ams_pool_last_plan", "ams_pool_set_kernel_policy", "ams_shard_locate", "ams_shard_capacity",
            "ams_abi_version", "ams_hasher_create", "ams_hash_actions", "ams_hasher_last_stats", "ams_hasher_destroy",
@@ -112,6 +112,8 @@ def _load():
     L.ams_status_string.restype = ctypes.c_char_p
     L.ams_abi_version.argtypes = []
     L.ams_abi_version.restype = ctypes.c_int32
+    L.ams_build_id.argtypes = []
+    L.ams_build_id.restype = ctypes.c_char_p
     return L
 
 
@@ -158,6 +160,10 @@ def _stream(s) -> Optional[int]:
 # ----------------------------------------------------------------------------- C ABI
 def ams_abi_version() -> int:
     return int(lib.ams_abi_version())
+
+
+def ams_build_id() -> str:
+    return lib.ams_build_id().decode()
 
 
 def ams_status_string(st: int) -> str:

@@ -48,6 +48,21 @@ def _stale(out, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def build_id(srcs, hdrs, flags) -> str:
+    """Identity of a build: sha256 over the sources, headers and compile flags (nvcc output
+    itself is not byte-reproducible -- it embeds temporary file names -- so a hash of the
+    .so cannot tie a profile to the code it measured; this can).  Compiled into the
+    library (ams_build_id) and recorded next to every ncu capture."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in sorted(srcs + hdrs):
+        h.update(os.path.basename(f).encode())
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+    h.update(" ".join(flags).encode())
+    return h.hexdigest()[:32]
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
@@ -58,6 +73,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return OUT
     common = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
               "-I", os.path.join(ROOT, "include"), "-I", inc, "-Xptxas", "-v"]
+    common += [f"-DAMS_BUILD_ID=\"{build_id(srcs, hdrs, [*ARCH, '-O3', '-lineinfo', '-std=c++17'])}\""]
 
     def compile_one(src):
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")

@@ -264,6 +264,11 @@ extern "C" {
 
 int32_t ams_abi_version(void) { return AMS_ABI_VERSION; }
 
+#ifndef AMS_BUILD_ID
+#define AMS_BUILD_ID "unknown"
+#endif
+const char* ams_build_id(void) { return AMS_BUILD_ID; }
+
 const char* ams_status_string(ams_status_t st) {
   switch (st) {
     case AMS_OK: return "AMS_OK";

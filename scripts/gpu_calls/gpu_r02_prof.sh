@@ -1,8 +1,8 @@
 # round 2 profile refresh: default bench line, launch list of the bench command, ncu --set full
 # of the dominant kernels (C3 batch K2, C3 64-query scan K2s, hash TC, C4 batch K2) with the
-# library's sha256 recorded next to the reports (bench.py reuses the traffic only for that build)
+# library's build id recorded next to the reports (bench.py reuses the traffic only for that build)
 set -x
-sha256sum paper_2508_10259_b200/libams.so > gpurun_out/prof_libsha.txt
+python -c "import paper_2508_10259_b200 as a; print(a.ams_build_id())" > gpurun_out/prof_buildid.txt
 timeout 1200 python bench.py > gpurun_out/r02_bench_final.json 2> gpurun_out/r02_bench_final.err; echo "bench rc=$?"
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches_r02_c3.csv \
    python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-c4 > gpurun_out/ncu_launch.log 2>&1; echo "launch rc=$?"

@@ -7,7 +7,7 @@
         --launches c3:gpurun_out/launches_c3.csv
 
 Writes profiles/ncu_summary.json ({workload: {kernel: {...metrics, dram_bytes_per_launch}}},
-read by bench.py for roofline.traffic when lib_sha256 matches the library it runs),
+read by bench.py for roofline.traffic when build_id matches the library it runs),
 profiles/ncu_<round>_<workload>_<kernel>.txt
 (raw key metrics) and profiles/launches_<round>_<workload>.csv (+ a per-kernel share
 table).  Runs here (no GPU needed): `ncu -i` only reads the report files.
@@ -65,11 +65,11 @@ def main():
     ap.add_argument("--round", default="r01")
     ap.add_argument("--full", action="append", default=[])
     ap.add_argument("--launches", action="append", default=[])
-    ap.add_argument("--lib-sha-file", default=None,
-                    help="sha256sum of paper_2508_10259_b200/libams.so written on the GPU box by the capture "
-                         "command; bench.py reuses a capture's traffic only for that exact build")
+    ap.add_argument("--build-id-file", default=None,
+                    help="ams_build_id() of the library the capture ran, written on the GPU box by the capture "
+                         "command; bench.py reuses a capture's traffic only for that build")
     a = ap.parse_args()
-    lib_sha = open(a.lib_sha_file).read().split()[0] if a.lib_sha_file else None
+    build_id = open(a.build_id_file).read().split()[0] if a.build_id_file else None
     os.makedirs(PROF, exist_ok=True)
     path = os.path.join(PROF, "ncu_summary.json")
     summary = json.load(open(path)) if os.path.exists(path) else {}
@@ -78,7 +78,7 @@ def main():
         m = raw_metrics(rep)
         rd = to_base(m["dram__bytes_read.sum"]) if "dram__bytes_read.sum" in m else None
         wr = to_base(m["dram__bytes_write.sum"]) if "dram__bytes_write.sum" in m else None
-        entry = {"round": a.round, "report": os.path.basename(rep), "lib_sha256": lib_sha,
+        entry = {"round": a.round, "report": os.path.basename(rep), "build_id": build_id,
                  "dram_bytes_per_launch": (rd + wr) if rd is not None and wr is not None else None,
                  "duration_s": to_base(m["gpu__time_duration.sum"]) if "gpu__time_duration.sum" in m else None,
                  "metrics": {k: v["value"] for k, v in m.items()},

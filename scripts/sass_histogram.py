@@ -5,7 +5,7 @@ tcgen05 / TMEM / TMA use):  python scripts/sass_histogram.py > profiles/sass_<ro
 Counts, per kernel instantiation: UTC*MMA (tcgen05.mma: HMMA = f16/bf16, IMMA = i8),
 UTCBAR (tcgen05.commit), LDTM (tcgen05.ld), UTMALDG (TMA tensor loads), UBLKCP (bulk
 copies), LDGSTS (cp.async), UTMACCTL (tensor-map prefetch), plus the total instruction
-count.  The library's sha256 heads the file so a reader can tie it to a build."""
+count.  The library's build id (ams_build_id: sources + flags) heads the file."""
 import collections
 import hashlib
 import os
@@ -43,9 +43,9 @@ def main():
             for o in OPS:
                 if op.startswith(o):
                     counts[cur][o] += 1
-    with open(LIB, "rb") as f:
-        sha = hashlib.sha256(f.read()).hexdigest()
-    print(f"# libams.so sha256 {sha}")
+    sys.path.insert(0, ROOT)
+    import paper_2508_10259_b200 as ams
+    print(f"# libams.so ams_build_id {ams.ams_build_id()}")
     print(f"# {'kernel':<100s} " + " ".join(f"{o:>8s}" for o in OPS) + f" {'instr':>8s}")
     names = demangle(order)
     for n, dn in sorted(zip(order, names), key=lambda t: t[1]):
