@@ -444,6 +444,12 @@ ams_status_t ams_pool_launch_count(ams_pool_t pool, int64_t* launches);
  * pool or a policy outside [0, 15]. */
 ams_status_t ams_pool_set_kernel_policy(ams_pool_t pool, int32_t policy);
 
+/* Plan of the last ams_match / ams_match_gate_first / ams_match_auto on this pool (for
+ * tests and benchmarks): row splits, partial lists per query, grid size and the kernel:
+ * 0 fp32 exact thread-per-row (gated fp32 calls), 1 tcgen05 128-query tiles on one CTA,
+ * 2 tcgen05 CTA pairs (256-query tiles), 3 gate-first, 4 small-batch (pool rows on the
+ * MMA M side; one CTA or a CTA pair), 5 CTA pairs in 4-CTA multicast clusters, 6 fp32
+ * exact tiled (ungated fp32 calls), -1 none yet.  Any output pointer may be NULL. */
 ams_status_t ams_pool_last_plan(ams_pool_t pool, int32_t* splits, int32_t* partials,
                                 int32_t* grid, int32_t* kernel_id);
 

@@ -673,7 +673,17 @@ static ams_status_t match_impl(ams_pool_t pool, const void* q_emb, const float* 
     p.last_partials = 0;
     p.last_grid = 0;
   } else if (p.local > 0) {
-    if (p.cfg.dtype == AMS_DTYPE_FP32) {
+    if (p.cfg.dtype == AMS_DTYPE_FP32 && !a.gated &&
+        (int64_t)nq * ams::f32_tile_lists(p.local) * a.KT <= p.part_cap) {
+      // ungated fp32: every pair is scored -- the tiled exact kernel (plan id 6)
+      P = ams::f32_tile_lists(p.local);
+      if (e0) AMS_CUDA_TRY(cudaEventRecord(e0, s));
+      AMS_CUDA_TRY(ams::launch_match_f32_tile(p, a, s));
+      if (e1) AMS_CUDA_TRY(cudaEventRecord(e1, s));
+      p.last_splits = P;
+      p.last_grid = P * ((nq + 15) / 16);
+      p.last_kernel = 6;
+    } else if (p.cfg.dtype == AMS_DTYPE_FP32) {
       int S;
       plan_simt(p, nq, a.KT, S);
       P = S * ams::kSimtThreads;

@@ -201,6 +201,10 @@ cudaError_t launch_query_prep(Pool& p, const void* q_src, const float* qj_src, i
 // p.q_perm <- the queries ordered by joint 0 (counting sort into linear bins; one block)
 cudaError_t launch_query_order(Pool& p, const float* qj_src, int32_t nq, cudaStream_t s);
 cudaError_t launch_match_simt(Pool& p, const MatchArgs& a, int32_t splits, cudaStream_t s);
+// fp32 exact, ungated calls: tiles of 32 rows x 16 queries, one partial list per (query,
+// row tile); f32_tile_lists(L) = the number of lists per query
+int f32_tile_lists(int64_t L);
+cudaError_t launch_match_f32_tile(Pool& p, const MatchArgs& a, cudaStream_t s);
 // cg = 1: one CTA per 128x256 tile; cg = 2: CTA pair (cta_group::2) per 256x256 tile
 // sorted: queries were staged through p.q_perm (partials land at the caller's query index)
 // cl: CTAs per cluster (cg, or 4 for cg = 2: two CTA pairs sharing multicast pool rows;

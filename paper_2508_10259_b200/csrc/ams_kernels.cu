@@ -267,6 +267,81 @@ __global__ void __launch_bounds__(kSimtThreads)
 }
 
 // ---------------------------------------------------------------------------------
+// fp32 exact matcher for UNGATED calls (configs[0]'s "plus an ungated run"): every pair is
+// scored, so the thread-per-row kernel above (one dependent 512-long fmaf chain per pair
+// per thread, uncoalesced row reads) is latency-bound.  Here a block owns a tile of
+// kTileRows rows x kTileQ queries; K advances in chunks of kTileK staged transposed in
+// shared memory; each thread runs 2 x 2 independent canonical chains (acc = fmaf(q_t, e_t,
+// acc), t ascending -- exactly the oracle's order), then s = RN(RN(acc * iq) * ie).  One
+// thread per query inserts the tile's kTileRows scores in row order (insert_monotone keeps
+// the lowest index first among ties) and writes the tile's list: partial list p = row
+// tile of query q at part[(q * P + p) * KT], P = ceil(L / kTileRows).
+// ---------------------------------------------------------------------------------
+constexpr int kTileRows = 32, kTileQ = 16, kTileK = 64;
+constexpr int kTileThreads = (kTileRows / 2) * (kTileQ / 2);   // 128
+
+template <int KT>
+__global__ void __launch_bounds__(kTileThreads)
+    match_f32_tile_kernel(const float* __restrict__ emb, const float* __restrict__ inv_e, int64_t L,
+                          const float* __restrict__ q, const float* __restrict__ inv_q, int32_t nq, int32_t d,
+                          int32_t k, float* __restrict__ part_s, int32_t* __restrict__ part_i, int32_t P) {
+  __shared__ float sR[kTileK][kTileRows + 1];
+  __shared__ float sQ[kTileK][kTileQ + 1];
+  __shared__ float sS[kTileQ][kTileRows + 1];
+  const int rt = blockIdx.x, qt = blockIdx.y;
+  const int64_t r0 = (int64_t)rt * kTileRows;
+  const int q0 = qt * kTileQ;
+  const int tid = threadIdx.x;
+  const int rg = tid % (kTileRows / 2), qg = tid / (kTileRows / 2);   // rows 2rg, 2rg+1; queries 2qg, 2qg+1
+  float acc[2][2] = {{0.0f, 0.0f}, {0.0f, 0.0f}};
+  for (int t0 = 0; t0 < d; t0 += kTileK) {
+    __syncthreads();
+    for (int i = tid; i < kTileRows * kTileK; i += kTileThreads) {   // coalesced along t
+      const int r = i / kTileK, t = i % kTileK;
+      sR[t][r] = (r0 + r < L) ? emb[(r0 + r) * d + t0 + t] : 0.0f;
+    }
+    for (int i = tid; i < kTileQ * kTileK; i += kTileThreads) {
+      const int c = i / kTileK, t = i % kTileK;
+      sQ[t][c] = (q0 + c < nq) ? q[(int64_t)(q0 + c) * d + t0 + t] : 0.0f;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int t = 0; t < kTileK; ++t) {
+      const float e0 = sR[t][2 * rg], e1 = sR[t][2 * rg + 1];
+      const float a0 = sQ[t][2 * qg], a1 = sQ[t][2 * qg + 1];
+      acc[0][0] = __fmaf_rn(a0, e0, acc[0][0]);
+      acc[0][1] = __fmaf_rn(a1, e0, acc[0][1]);
+      acc[1][0] = __fmaf_rn(a0, e1, acc[1][0]);
+      acc[1][1] = __fmaf_rn(a1, e1, acc[1][1]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int64_t j = r0 + 2 * rg + i;
+      const int qi = q0 + 2 * qg + c;
+      const float s = (j < L && qi < nq) ? __fmul_rn(__fmul_rn(acc[i][c], inv_q[qi]), inv_e[j]) : -CUDART_INF_F;
+      sS[2 * qg + c][2 * rg + i] = s;
+    }
+  __syncthreads();
+  if (tid < kTileQ && q0 + tid < nq) {
+    TopK<KT, int32_t> top;
+    top.init(true);
+    for (int r = 0; r < kTileRows; ++r) {
+      const float s = sS[tid][r];
+      if (r0 + r < L && s > top.kth_s) top.insert_monotone(s, (int32_t)(r0 + r), k);
+    }
+    const int64_t base = ((int64_t)(q0 + tid) * P + rt) * KT;
+#pragma unroll
+    for (int r = 0; r < KT; ++r) {
+      part_s[base + r] = top.s[r];
+      part_i[base + r] = top.i[r];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------
 // Warp-cooperative k-way merge: lanes build register top-k lists from a strided subset
 // of the input lists (sorted lists: stop at the first entry that cannot enter), then k
 // rounds of a butterfly arg-max by (score desc, index asc) emit the merged list.
@@ -534,6 +609,26 @@ cudaError_t launch_match_simt(Pool& p, const MatchArgs& a, int32_t S, cudaStream
     default: AMS_SIMT(64); break;
   }
 #undef AMS_SIMT
+  ++p.launches;
+  return cudaGetLastError();
+}
+
+int f32_tile_lists(int64_t L) { return (int)((L + kTileRows - 1) / kTileRows); }
+
+cudaError_t launch_match_f32_tile(Pool& p, const MatchArgs& a, cudaStream_t s) {
+  const int32_t P = f32_tile_lists(p.local);
+  const dim3 grid((unsigned)P, (unsigned)((a.nq + kTileQ - 1) / kTileQ));
+#define AMS_F32T(KT_)                                                                                    \
+  match_f32_tile_kernel<KT_><<<grid, kTileThreads, 0, s>>>(static_cast<const float*>(p.emb), p.inv_norm, p.local, \
+                                                          static_cast<const float*>(p.q_stage), p.q_inv, a.nq,     \
+                                                          p.cfg.dim, a.k, p.part_s, p.part_i, P)
+  switch (a.KT) {
+    case 8: AMS_F32T(8); break;
+    case 16: AMS_F32T(16); break;
+    case 32: AMS_F32T(32); break;
+    default: AMS_F32T(64); break;
+  }
+#undef AMS_F32T
   ++p.launches;
   return cudaGetLastError();
 }

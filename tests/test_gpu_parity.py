@@ -234,3 +234,27 @@ def test_self_match_score_and_norms(ams, nq):
         assert np.all(idx[:, 0] <= src)
         assert np.all(np.abs(score[:, 0].astype(np.float64) - 1.0) <= 1e-5), np.abs(score[:, 0] - 1).max()
         assert np.all(hit == 1)
+
+
+@pytest.mark.parametrize("M,nq,d", [(1, 1, 64), (31, 15, 64), (33, 17, 128), (1024, 64, 512), (1025, 100, 768),
+                                    (5000, 33, 1024)])
+@pytest.mark.parametrize("k", [1, 5, 16, 40])
+def test_fp32_ungated_tile_kernel_bit_exact(ams, M, nq, d, k):
+    """Ungated fp32 calls take the tiled exact kernel (plan id 6: 32-row x 16-query tiles,
+    the canonical fmaf chain per pair); gated ones keep the thread-per-row kernel (plan id
+    0).  Both byte-identical to the oracle, with duplicate rows (ties to the lower index)
+    and ragged tiles."""
+    rng = np.random.Generator(np.random.PCG64(M * 7 + nq + d + k))
+    e = rng.standard_normal((M, d)).astype(np.float32)
+    if M > 4:
+        e[3] = e[1]
+    qv = rng.standard_normal((nq, d)).astype(np.float32)
+    j = rng.uniform(-1, 1, (M, 7)).astype(np.float32)
+    qj = rng.uniform(-1, 1, (nq, 7)).astype(np.float32)
+    with ams.Pool(d, 7, M, nq, 64, dtype="fp32") as pool:
+        pool.append(to_dev(e), to_dev(j))
+        for gamma, kid in ((INF, 6), (0.8, 0)):
+            out = [t.cpu().numpy() for t in pool.match(to_dev(qv), to_dev(qj), k, 0.1, gamma)]
+            torch.cuda.synchronize()
+            assert ams.ams_pool_last_plan(pool.handle)["kernel_id"] == kid
+            check_exact(*out, oracle.match(e, j, qv, qj, k, 0.1, gamma))
