@@ -71,6 +71,8 @@ __global__ void append_kernel(const void* __restrict__ src, const float* __restr
 // Query prep: stage the query rows, inv_q, zero-padded joints.  One warp per query.
 // ---------------------------------------------------------------------------------
 // Staged row q holds the caller's query perm[q] (perm == nullptr: identity).
+constexpr int kPrepWarps = 8;   // queries (warps) per query_prep block
+
 template <bool BF16>
 __global__ void query_prep_kernel(const void* __restrict__ src, const float* __restrict__ jsrc, int32_t nq,
                                   int32_t d, int32_t J, int32_t JP, const int32_t* __restrict__ perm,
@@ -80,33 +82,70 @@ __global__ void query_prep_kernel(const void* __restrict__ src, const float* __r
   const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (q >= nq) return;
   const int64_t o = perm != nullptr ? (int64_t)perm[q] : (int64_t)q;
-  if (BF16) {
+  if constexpr (BF16) {
     const uint4* s4 = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(src) + o * d);
     uint4* d4 = reinterpret_cast<uint4*>(static_cast<uint16_t*>(q_stage) + (int64_t)q * d);
     double ss = 0.0;
-    for (int c = lane; c < d / 8; c += 32) {
-      const uint4 w = s4[c];
-      if (s4 != d4) d4[c] = w;
-      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+    // 4 pieces per lane in flight before any store (s4 may alias d4 as far as the compiler
+    // knows, which would otherwise serialise every load behind the previous store)
+    for (int c0 = 0; c0 < d / 8; c0 += 128) {
+      uint4 wv[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const double a = bf16_lo(ws[k]), b = bf16_hi(ws[k]);
-        ss += a * a;
-        ss += b * b;
+      for (int u = 0; u < 4; ++u) {
+        const int c = c0 + 32 * u + lane;
+        wv[u] = c < d / 8 ? __ldg(s4 + c) : make_uint4(0u, 0u, 0u, 0u);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = c0 + 32 * u + lane;
+        if (c >= d / 8) continue;
+        if (s4 != d4) d4[c] = wv[u];
+        const uint32_t ws[4] = {wv[u].x, wv[u].y, wv[u].z, wv[u].w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const double a = bf16_lo(ws[k]), b = bf16_hi(ws[k]);
+          ss += a * a;
+          ss += b * b;
+        }
       }
     }
     ss = warp_sum_f64(ss);
     if (lane == 0) q_inv[q] = ss > 0.0 ? __double2float_rn(1.0 / sqrt(ss)) : 0.0f;
   } else {
+    // the warp stages the query through shared memory in coalesced 1024-value chunks (and
+    // copies it to q_stage); lane 0 runs the canonical chain (t ascending, one fmaf chain)
+    // from shared memory -- one memory round trip per chunk instead of one per few values
+    __shared__ __align__(16) float qbuf[kPrepWarps][1024];
     const float* s = static_cast<const float*>(src) + o * d;
     float* e = static_cast<float*>(q_stage) + (int64_t)q * d;
-    if (s != e)
-      for (int c = lane; c < d; c += 32) e[c] = s[c];
-    if (lane == 0) {
-      float ss = 0.0f;
-      for (int t = 0; t < d; ++t) ss = __fmaf_rn(s[t], s[t], ss);
-      q_inv[q] = ss > 0.0f ? __fdiv_rn(1.0f, __fsqrt_rn(ss)) : 0.0f;
+    float* buf = qbuf[threadIdx.x >> 5];
+    float ss = 0.0f;
+    for (int c0 = 0; c0 < d; c0 += 1024) {
+      const int n = min(1024, d - c0);   // a multiple of 32 (d % 64 == 0)
+      __syncwarp();
+      float v[32];   // all of the lane's loads in flight before any store (see the bf16 branch)
+#pragma unroll
+      for (int u = 0; u < 32; ++u) v[u] = 32 * u < n ? __ldg(s + c0 + 32 * u + lane) : 0.0f;
+#pragma unroll
+      for (int u = 0; u < 32; ++u)
+        if (32 * u < n) {
+          buf[32 * u + lane] = v[u];
+          if (s != e) e[c0 + 32 * u + lane] = v[u];
+        }
+      __syncwarp();
+      if (lane == 0) {   // n % 4 == 0 (d % 64 == 0); 16-byte shared loads, several in flight
+        const float4* b4 = reinterpret_cast<const float4*>(buf);
+#pragma unroll 8
+        for (int t4 = 0; t4 < n / 4; ++t4) {
+          const float4 v = b4[t4];
+          ss = __fmaf_rn(v.x, v.x, ss);
+          ss = __fmaf_rn(v.y, v.y, ss);
+          ss = __fmaf_rn(v.z, v.z, ss);
+          ss = __fmaf_rn(v.w, v.w, ss);
+        }
+      }
     }
+    if (lane == 0) q_inv[q] = ss > 0.0f ? __fdiv_rn(1.0f, __fsqrt_rn(ss)) : 0.0f;
   }
   if (lane < JP) q_joints[(int64_t)q * JP + lane] = lane < J ? jsrc[o * J + lane] : 0.0f;
 }
@@ -222,6 +261,8 @@ __global__ void __launch_bounds__(kOrderThreads)
 // ascending), s = (acc * inv_q) * inv_e; running top-k in registers.  Partial list
 // p = split * 128 + t of query q lands at part[(q * P + p) * KT].
 // ---------------------------------------------------------------------------------
+constexpr int kSimtChunk = 1024;   // floats of a pool row staged per round trip (4 KB per warp)
+
 template <int KT>
 __global__ void __launch_bounds__(kSimtThreads)
     match_simt_f32_kernel(const float* __restrict__ emb, const float* __restrict__ inv_e,
@@ -229,7 +270,7 @@ __global__ void __launch_bounds__(kSimtThreads)
                           const float* __restrict__ inv_q, const float* __restrict__ qj, int32_t d, int32_t JP,
                           int32_t S, int32_t k, float g2, int32_t gated, float* __restrict__ part_s,
                           int32_t* __restrict__ part_i, int32_t P) {
-  extern __shared__ float qs[];
+  extern __shared__ __align__(16) float qs[];
   const int qi = blockIdx.x / S;
   const int sp = blockIdx.x % S;
   for (int t = threadIdx.x; t < d; t += blockDim.x) qs[t] = q[(int64_t)qi * d + t];
@@ -241,8 +282,17 @@ __global__ void __launch_bounds__(kSimtThreads)
   const int64_t lo = L * sp / S, hi = L * (sp + 1) / S;
   TopK<KT, int32_t> top;
   top.init(true);
-  for (int64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) {
-    if (gated) {
+  // Rows are walked warp-synchronously (lane = row); the rows of a step that pass the gate
+  // are scored one at a time: the warp stages the row through its shared-memory buffer
+  // in coalesced 16-byte pieces (one memory round trip per kSimtChunk values instead of
+  // one per few values of a lone thread's loads), then the owning lane runs the canonical
+  // chain from shared memory (acc = fmaf(q_t, e_t, acc), t ascending -- the oracle's order).
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float* rowbuf = qs + ((d + 3) & ~3) + w * kSimtChunk;   // [warps][kSimtChunk]
+  for (int64_t jb = lo + (threadIdx.x & ~31); jb < hi; jb += blockDim.x) {
+    const int64_t j = jb + lane;
+    bool ok = j < hi;
+    if (ok && gated) {
       float ds = 0.0f;
 #pragma unroll
       for (int t = 0; t < 16; ++t)
@@ -250,13 +300,38 @@ __global__ void __launch_bounds__(kSimtThreads)
           const float df = __fsub_rn(r[t], pj[joint_offset(j, t, JP)]);
           ds = __fmaf_rn(df, df, ds);
         }
-      if (!(ds <= g2)) continue;
+      ok = ds <= g2;
     }
-    const float* e = emb + j * d;
-    float acc = 0.0f;
-    for (int t = 0; t < d; ++t) acc = __fmaf_rn(qs[t], e[t], acc);
-    const float s = __fmul_rn(__fmul_rn(acc, iq), inv_e[j]);
-    if (s > top.kth_s) top.insert_monotone(s, (int32_t)j, k);
+    uint32_t m = __ballot_sync(0xffffffffu, ok);
+    while (m != 0u) {
+      const int src = __ffs(m) - 1;
+      m &= m - 1u;
+      const int64_t jr = jb + src;
+      const float4* e4 = reinterpret_cast<const float4*>(emb + jr * d);   // rows 16-B aligned: d % 64 == 0
+      float acc = 0.0f;
+      for (int c0 = 0; c0 < d; c0 += kSimtChunk) {
+        const int n4 = min(kSimtChunk, d - c0) / 4;
+        __syncwarp();
+        for (int i = lane; i < n4; i += 32) reinterpret_cast<float4*>(rowbuf)[i] = __ldg(e4 + c0 / 4 + i);
+        __syncwarp();
+        if (lane == src) {
+          const float4* q4 = reinterpret_cast<const float4*>(qs + c0);
+          const float4* r4 = reinterpret_cast<const float4*>(rowbuf);
+#pragma unroll 4
+          for (int t4 = 0; t4 < n4; ++t4) {
+            const float4 ev = r4[t4], qv = q4[t4];
+            acc = __fmaf_rn(qv.x, ev.x, acc);
+            acc = __fmaf_rn(qv.y, ev.y, acc);
+            acc = __fmaf_rn(qv.z, ev.z, acc);
+            acc = __fmaf_rn(qv.w, ev.w, acc);
+          }
+        }
+      }
+      if (lane == src) {
+        const float sc = __fmul_rn(__fmul_rn(acc, iq), inv_e[jr]);
+        if (sc > top.kth_s) top.insert_monotone(sc, (int32_t)jr, k);
+      }
+    }
   }
   const int64_t base = ((int64_t)qi * P + (int64_t)sp * blockDim.x + threadIdx.x) * KT;
 #pragma unroll
@@ -576,7 +651,7 @@ cudaError_t launch_append(Pool& p, const void* emb_src, const float* joints_src,
 
 cudaError_t launch_query_prep(Pool& p, const void* q_src, const float* qj_src, int32_t nq, const int32_t* perm,
                               cudaStream_t s) {
-  const int wpb = 8;
+  const int wpb = kPrepWarps;
   const auto& c = p.cfg;
   if (c.dtype == AMS_DTYPE_BF16)
     query_prep_kernel<true><<<blocks_for(nq, wpb), wpb * 32, 0, s>>>(q_src, qj_src, nq, c.dim, c.joint_dim,
@@ -596,9 +671,10 @@ cudaError_t launch_query_order(Pool& p, const float* qj_src, int32_t nq, cudaStr
 
 cudaError_t launch_match_simt(Pool& p, const MatchArgs& a, int32_t S, cudaStream_t s) {
   const int32_t P = S * kSimtThreads;
-  const size_t smem = (size_t)p.cfg.dim * sizeof(float);
+  const size_t smem = ((size_t)((p.cfg.dim + 3) & ~3) + (size_t)(kSimtThreads / 32) * kSimtChunk) * sizeof(float);
   const dim3 grid((unsigned)(a.nq * S));
 #define AMS_SIMT(KT_)                                                                                  \
+  cudaFuncSetAttribute(match_simt_f32_kernel<KT_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
   match_simt_f32_kernel<KT_><<<grid, kSimtThreads, smem, s>>>(                                        \
       static_cast<const float*>(p.emb), p.inv_norm, p.joints, p.local, static_cast<const float*>(p.q_stage), \
       p.q_inv, p.q_joints, p.cfg.dim, p.JP, S, a.k, a.g2, a.gated, p.part_s, p.part_i, P)
