@@ -73,11 +73,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return OUT
     common = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
               "-I", os.path.join(ROOT, "include"), "-I", inc, "-Xptxas", "-v"]
-    common += [f"-DAMS_BUILD_ID=\"{build_id(srcs, hdrs, [*ARCH, '-O3', '-lineinfo', '-std=c++17'])}\""]
+    bid = build_id(srcs, hdrs, [*ARCH, "-O3", "-lineinfo", "-std=c++17"])
+    common += [f"-DAMS_BUILD_ID=\"{bid}\""]
 
     def compile_one(src):
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")
-        if force or _stale(obj, [src, *hdrs]):
+        # the object that embeds the build id (ams_capi.cu) is stale whenever the id changes,
+        # not only when its own sources change
+        stamp = obj + ".build_id"
+        id_changed = "AMS_BUILD_ID" in open(src).read() and (
+            not os.path.exists(stamp) or open(stamp).read().strip() != bid)
+        if force or id_changed or _stale(obj, [src, *hdrs]):
             log = os.path.join(BUILD, "ptxas_" + os.path.basename(src) + ".log")
             cmd = [*common, "-c", src, "-o", obj]
             r = subprocess.run(cmd, capture_output=True, text=True)
@@ -85,6 +91,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 f.write(r.stdout + r.stderr)
             if r.returncode != 0:
                 raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr[-6000:]}")
+            with open(stamp, "w") as f:
+                f.write(bid)
         return obj
 
     with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:

@@ -144,3 +144,16 @@ def test_binding_fails_loudly_without_library(tmp_path):
     code = "import sys; sys.path.insert(0, %r); import paper_2508_10259_b200" % str(tmp_path)
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True)
     assert r.returncode != 0 and "no CPU fallback" in r.stderr
+
+
+def test_library_built_from_these_sources(ams):
+    """The in-tree libams.so reports the build id of the sources, headers and flags in this
+    tree (paper_2508_10259_b200/build.py:build_id): the library under test is not stale."""
+    import glob
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("_ams_build", os.path.join(ROOT, "paper_2508_10259_b200", "build.py"))
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)
+    srcs = sorted(glob.glob(os.path.join(b.CSRC, "*.cu")))
+    hdrs = sorted(glob.glob(os.path.join(b.CSRC, "*.cuh"))) + [os.path.join(ROOT, "include", "ams.h")]
+    assert ams.ams_build_id() == b.build_id(srcs, hdrs, [*b.ARCH, "-O3", "-lineinfo", "-std=c++17"])
