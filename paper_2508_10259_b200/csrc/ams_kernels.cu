@@ -560,11 +560,38 @@ __global__ void merge_partials_kernel(const float* __restrict__ part_s, const in
 }
 
 // Small batches with many partial lists (the small-batch kernel leaves 4-8 per row
-// split): one 128-thread block per query instead of one warp, so nq < ~1000 still fills
-// the GPU.  Each thread gathers lists t, t + 128, ... into its TopK; the lists are
-// staged in shared memory and warp 0 merges them (lane l: threads l, l + 32, l + 64,
-// l + 96) and emits the top k exactly as merge_partials_kernel does.
-constexpr int kMergeBlockThreads = 128;   // KT <= 32: <= 32 KB of staging
+// split): one 512-thread block per query instead of one warp, so nq < ~1000 still fills
+// the GPU.  Selection by rank, with no serial insert chains (ncu of the insert-based
+// version: a 64-query ungated C3 merge took 30 us, one or two dependent-issue warps per
+// SM walking 588 lists through register inserts):
+//   1. every list head >= lb (the kernels' lower bound) goes to shared memory;
+//   2. each head's rank among them (the number of heads ordered before it): the lists
+//      are sorted and hold disjoint rows, so a top-k row's list head has rank < k (k heads
+//      ordered before it would be k rows ordered before the row), and the row is ordered
+//      no later than the k-th head; those <= k lists are "walked";
+//   3. entries 0..k-1 of the walked lists that are ordered no later than the k-th head
+//      (or >= lb when fewer than k heads exist) are the candidates, <= k * k of them;
+//   4. a candidate's rank among the candidates is its output position (keys are distinct
+//      rows, so ranks are unique); positions past the candidates are padding.
+// The order is (score desc, local index asc) exactly as merge_partials_kernel's
+// warp_emit.  More than kMergeMaxHeads heads >= lb (an fp32 call without bounds) falls
+// back to per-thread lists on the first 128 threads, merged by warp 0.
+constexpr int kMergeBlockThreads = 512;
+constexpr int kMergeFallbackThreads = 128;   // KT <= 32: <= 32 KB of fallback staging
+constexpr int kMergeMaxHeads = 512;          // rank pass: one head x 512 comparisons per thread
+
+// number of (s[g], i[g]), g < n4 (a multiple of 4, padded with (-inf, -1)), ordered before (v, j)
+__device__ __forceinline__ int rank_of(const float* __restrict__ s, const int32_t* __restrict__ i, int n4, float v,
+                                       int32_t j) {
+  int r = 0;
+  for (int g = 0; g < n4; g += 4) {
+    const float4 a = *reinterpret_cast<const float4*>(s + g);
+    const int4 b = *reinterpret_cast<const int4*>(i + g);
+    r += (better(a.x, b.x, v, j) ? 1 : 0) + (better(a.y, b.y, v, j) ? 1 : 0) + (better(a.z, b.z, v, j) ? 1 : 0) +
+         (better(a.w, b.w, v, j) ? 1 : 0);
+  }
+  return r;
+}
 
 template <int KT>
 __global__ void __launch_bounds__(kMergeBlockThreads)
@@ -573,24 +600,128 @@ __global__ void __launch_bounds__(kMergeBlockThreads)
                                 uint8_t* __restrict__ out_hit, float threshold, int32_t rank, int32_t world,
                                 int64_t B, const uint32_t* __restrict__ bound, const uint32_t* __restrict__ slots,
                                 int32_t slot_stride) {
-  __shared__ float ss[KT][kMergeBlockThreads];
-  __shared__ int32_t si[KT][kMergeBlockThreads];
+  __shared__ float ss[KT][kMergeFallbackThreads];
+  __shared__ int32_t si[KT][kMergeFallbackThreads];
+  __shared__ __align__(16) float hs[kMergeMaxHeads + 4];
+  __shared__ __align__(16) int32_t hi[kMergeMaxHeads + 4];
+  __shared__ int32_t hp[kMergeMaxHeads];
+  __shared__ __align__(16) float cs[KT * KT + 4];
+  __shared__ __align__(16) int32_t ci[KT * KT + 4];
+  __shared__ int32_t walk[KT];
+  __shared__ int32_t n_heads, n_cand, kth_i;
+  __shared__ float kth_s;
   const int q = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31;
   const float lb = tc_lower_bound(bound, slots, slot_stride, k, q);
+  float* qs = out_s + (int64_t)q * k;
+  int64_t* qi = out_i + (int64_t)q * k;
+  if (tid == 0) {
+    n_heads = 0;
+    n_cand = 0;
+  }
+  __syncthreads();
+  // 1. heads >= lb (up to 4 heads per thread in flight together)
+  for (int p0 = tid; p0 < P; p0 += kMergeBlockThreads * 4) {
+    float vs[4];
+    int32_t vj[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int p = p0 + u * kMergeBlockThreads;
+      vj[u] = -1;
+      vs[u] = -CUDART_INF_F;
+      if (p < P) {
+        const int64_t base = ((int64_t)q * P + p) * KT;
+        vj[u] = part_i[base];
+        vs[u] = part_s[base];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (vj[u] < 0 || vs[u] < lb) continue;
+      const int h = atomicAdd(&n_heads, 1);
+      if (h < kMergeMaxHeads) {
+        hs[h] = vs[u];
+        hi[h] = vj[u];
+        hp[h] = p0 + u * kMergeBlockThreads;
+      }
+    }
+  }
+  __syncthreads();
+  const int H = n_heads;
+  if (H <= kMergeMaxHeads) {
+    // 2. ranks of the heads; the walked lists in rank order and the k-th head
+    const int H4 = (H + 3) & ~3;
+    if (tid < H4 - H) {
+      hs[H + tid] = -CUDART_INF_F;
+      hi[H + tid] = -1;
+    }
+    __syncthreads();
+    const int W = H < k ? H : k;
+    for (int h = tid; h < H; h += kMergeBlockThreads) {
+      const float v = hs[h];
+      const int32_t j = hi[h];
+      const int r = rank_of(hs, hi, H4, v, j);
+      if (r < k) walk[r] = hp[h];
+      if (r == W - 1) {
+        kth_s = H < k ? lb : v;
+        kth_i = H < k ? INT32_MAX : j;   // (lb, max): every entry >= lb passes
+      }
+    }
+    __syncthreads();
+    // 3. candidates: entries of the walked lists ordered no later than the k-th head
+    if (W > 0) {
+      const float ts = kth_s;
+      const int32_t tj = kth_i;
+      for (int e = tid; e < W * k; e += kMergeBlockThreads) {
+        const int w = e / k, r = e - w * k;
+        const int64_t base = ((int64_t)q * P + walk[w]) * KT + r;
+        const int32_t j = part_i[base];
+        const float v = part_s[base];
+        if (j < 0 || better(ts, tj, v, j)) continue;
+        const int c = atomicAdd(&n_cand, 1);   // < W * k <= KT * KT
+        cs[c] = v;
+        ci[c] = j;
+      }
+    }
+    __syncthreads();
+    // 4. output position = rank among the candidates
+    const int C = n_cand, C4 = (C + 3) & ~3;
+    if (tid < C4 - C) {
+      cs[C + tid] = -CUDART_INF_F;
+      ci[C + tid] = -1;
+    }
+    __syncthreads();
+    for (int c = tid; c < C; c += kMergeBlockThreads) {
+      const float v = cs[c];
+      const int32_t j = ci[c];
+      const int r = rank_of(cs, ci, C4, v, j);
+      if (r < k) {
+        qs[r] = v;
+        qi[r] = shard_global((int64_t)j, rank, world, B);
+        if (r == 0 && out_hit != nullptr) out_hit[q] = v >= threshold ? 1 : 0;
+      }
+    }
+    for (int r = C + tid; r < k; r += kMergeBlockThreads) {
+      qs[r] = -CUDART_INF_F;
+      qi[r] = -1;
+    }
+    if (C == 0 && tid == 0 && out_hit != nullptr) out_hit[q] = 0;
+    return;
+  }
+  if (tid >= kMergeFallbackThreads) return;   // no block barriers below
   TopK<KT, int32_t> t;
   t.init(true);
-  gather_lists<KT>(part_s, part_i, q, P, k, lb, tid, kMergeBlockThreads, t);
+  gather_lists<KT>(part_s, part_i, q, P, k, lb, tid, kMergeFallbackThreads, t);
 #pragma unroll
   for (int r = 0; r < KT; ++r) {
     ss[r][tid] = t.s[r];
     si[r][tid] = t.i[r];
   }
-  __syncthreads();
+  ptx::named_bar_sync(1, kMergeFallbackThreads);
   if (tid >= 32) return;
   TopK<KT, int32_t> m;
   m.init(true);
-  for (int w = 0; w < kMergeBlockThreads / 32; ++w) {
+  for (int w = 0; w < kMergeFallbackThreads / 32; ++w) {
     const int src = w * 32 + lane;
     for (int r = 0; r < k; ++r) {
       const int32_t j = si[r][src];
@@ -599,8 +730,7 @@ __global__ void __launch_bounds__(kMergeBlockThreads)
       m.insert(v, j, k);
     }
   }
-  warp_emit(m, k, lane, out_s + (int64_t)q * k, out_i + (int64_t)q * k, out_hit ? out_hit + q : nullptr,
-            threshold, rank, world, B, true);
+  warp_emit(m, k, lane, qs, qi, out_hit ? out_hit + q : nullptr, threshold, rank, world, B, true);
 }
 
 template <int KT>

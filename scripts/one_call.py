@@ -1,11 +1,12 @@
 #!/usr/bin/env python
 """A few identical ams_match calls on a config's pool, for ncu captures of one kernel.
 
-    python scripts/one_call.py c3 --nq 200 --k 8 [--policy P] [--gamma G] [--calls N] [--gate-first]
+    python scripts/one_call.py c3 --nq 200 --k 8 [--policy P] [--gamma G] [--calls N] [--gate-first] [--timeline]
 
 Builds the pool with the ams_gen recipe (not timed), then issues N calls (default 5);
 prints the median CUDA-event time per call and the plan.  ncu: -k regex:match_scan
---launch-skip 3 -c 1 captures the 4th call's kernel.
+--launch-skip 3 -c 1 captures the 4th call's kernel.  --timeline then prints the kernels of
+three back-to-back calls with their in-stream durations and the idle gaps between them.
 """
 import math
 import os
@@ -48,6 +49,21 @@ def main():
     ms = statistics.median(ts)
     print(f"{name} nq={nq} k={k} gamma={gamma} policy={policy} ms={ms:.4f} GB/s={cfg.M * row_bytes / ms / 1e6:.0f} "
           f"plan={ams.ams_pool_last_plan(pool.handle)}", flush=True)
+    if "--timeline" in sys.argv:
+        # in-stream kernel durations and the gaps between them (CUPTI via torch.profiler;
+        # natural clocks and warm L2, unlike a serialised ncu launch list)
+        from torch.profiler import ProfilerActivity, profile
+        torch.cuda.synchronize()
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            for _ in range(3):
+                fn(pool.handle, q, qj, nq, k, cfg.theta, gamma, *out, s)
+            torch.cuda.synchronize()
+        evs = sorted((e for e in prof.events() if e.device_type.name == "CUDA"), key=lambda e: e.time_range.start)
+        prev = None
+        for e in evs:
+            gap = "" if prev is None else f" gap={e.time_range.start - prev:8.2f}"
+            print(f"    {e.name.split('(')[0][:60]:60s} dur={e.time_range.elapsed_us():8.2f} us{gap}", flush=True)
+            prev = e.time_range.end
 
 
 if __name__ == "__main__":

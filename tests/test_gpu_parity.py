@@ -258,3 +258,28 @@ def test_fp32_ungated_tile_kernel_bit_exact(ams, M, nq, d, k):
             torch.cuda.synchronize()
             assert ams.ams_pool_last_plan(pool.handle)["kernel_id"] == kid
             check_exact(*out, oracle.match(e, j, qv, qj, k, 0.1, gamma))
+
+
+@pytest.mark.parametrize("M,nq,k", [(20011, 9, 5), (20011, 3, 32), (9000, 40, 16), (5000, 1, 1), (2100, 200, 32)])
+def test_block_merge_rank_and_fallback_paths(ams, M, nq, k):
+    """The block-per-query merge (nq < 8 x SMs, >= 64 partial lists, k <= 32) selects by
+    rank over the list heads >= the kernels' bound; more than 512 such heads (an ungated
+    fp32 call: no bound, every list full) takes the per-thread-list fallback.  fp32
+    ungated calls with 626 / 282 / 157 / 66 lists cover both sides of the cap, byte-
+    identical to the oracle, with duplicate rows (ties to the lower index)."""
+    rng = np.random.Generator(np.random.PCG64(M + 31 * nq + k))
+    d = 128
+    e = rng.standard_normal((M, d)).astype(np.float32)
+    e[5] = e[2]
+    e[M - 1] = e[7]
+    qv = rng.standard_normal((nq, d)).astype(np.float32)
+    qv[0] = e[2]
+    j = rng.uniform(-1, 1, (M, 7)).astype(np.float32)
+    qj = rng.uniform(-1, 1, (nq, 7)).astype(np.float32)
+    with ams.Pool(d, 7, M, nq, k, dtype="fp32") as pool:
+        pool.append(to_dev(e), to_dev(j))
+        out = [t.cpu().numpy() for t in pool.match(to_dev(qv), to_dev(qj), k, 0.2, INF)]
+        torch.cuda.synchronize()
+        plan = ams.ams_pool_last_plan(pool.handle)
+        assert plan["kernel_id"] == 6 and plan["partials"] == (M + 31) // 32
+        check_exact(*out, oracle.match(e, j, qv, qj, k, 0.2, INF))
