@@ -638,7 +638,15 @@ static ams_status_t match_impl(ams_pool_t pool, const void* q_emb, const float* 
                         (int64_t)nq * ams::scan_lists_per_split(nq, a.KT, a.gated != 0) * a.KT <= p.part_cap;   // >= 1 split fits
   const bool sorted = p.cfg.dtype == AMS_DTYPE_BF16 && a.gated && p.local > 0 && nq >= kSortMinQueries && !use_scan;
   if (sorted) AMS_CUDA_TRY(ams::launch_query_order(p, qj_src, nq, s));
-  AMS_CUDA_TRY(ams::launch_query_prep(p, q_src, qj_src, nq, sorted ? p.q_perm : nullptr, s));
+  // the dense bf16 kernels start from zeroed per-query bounds (+ the K2 wave counter) and,
+  // ungated, zeroed union slots: the prep kernel clears them (no memset node between it
+  // and the dense kernel, which is then its programmatic dependent).  Slots: K2 indexes
+  // them by padded query tile (<= round_up(nq, 256) rows), the small-batch kernel by query.
+  const bool dense_bf16 = !gate_first && p.cfg.dtype == AMS_DTYPE_BF16 && p.local > 0;
+  const int32_t zero_bound = dense_bf16 ? nq + 1 : 0;
+  const int32_t zero_slots = dense_bf16 && !a.gated ? (int32_t)round_up(nq, 2 * ams::kBlockM) * a.KT : 0;
+  AMS_CUDA_TRY(ams::launch_query_prep(p, q_src, qj_src, nq, sorted ? p.q_perm : nullptr, zero_bound, zero_slots, s));
+  a.zeroed = dense_bf16 ? 1 : 0;
   if (b >= 0) AMS_CUDA_TRY(cudaEventRecord(p.consumed[b], s));   // staging b read (order + prep)
 
   const bool multi = p.collective;

@@ -191,13 +191,16 @@ struct MatchArgs {
   int32_t gated;      // g2 < +inf
   float threshold;
   int32_t slots;      // the tcgen05 kernel filled p.slots (union bound) for the merge
+  int32_t zeroed;     // query prep already zeroed p.bound / p.slots for this call
 };
 
 cudaError_t launch_append(Pool& p, const void* emb_src, const float* joints_src, int64_t n_src,
                           int64_t first_global, cudaStream_t s);
-// perm (device, may be null = identity): staged row q is the caller's query perm[q]
+// perm (device, may be null = identity): staged row q is the caller's query perm[q].
+// Also zeroes p.bound[0, zero_bound) and p.slots[0, zero_slots) for the dense kernel that
+// follows, which launch_match_tc / launch_match_scan then no longer memset (zero_bound > 0).
 cudaError_t launch_query_prep(Pool& p, const void* q_src, const float* qj_src, int32_t nq, const int32_t* perm,
-                              cudaStream_t s);
+                              int32_t zero_bound, int32_t zero_slots, cudaStream_t s);
 // p.q_perm <- the queries ordered by joint 0 (counting sort into linear bins; one block)
 cudaError_t launch_query_order(Pool& p, const float* qj_src, int32_t nq, cudaStream_t s);
 cudaError_t launch_match_simt(Pool& p, const MatchArgs& a, int32_t splits, cudaStream_t s);

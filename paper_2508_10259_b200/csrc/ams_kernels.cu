@@ -77,7 +77,16 @@ template <bool BF16>
 __global__ void query_prep_kernel(const void* __restrict__ src, const float* __restrict__ jsrc, int32_t nq,
                                   int32_t d, int32_t J, int32_t JP, const int32_t* __restrict__ perm,
                                   void* __restrict__ q_stage, float* __restrict__ q_inv,
-                                  float* __restrict__ q_joints) {
+                                  float* __restrict__ q_joints, uint32_t* __restrict__ zero_a, int32_t n_zero_a,
+                                  uint32_t* __restrict__ zero_b, int32_t n_zero_b) {
+  // the dense kernel that follows (launched as a programmatic dependent) may start its
+  // prologue now; it reads nothing of ours before griddep_wait()
+  ptx::griddep_launch_dependents();
+  {   // its per-query bounds and union slots start at zero (replaces two memset nodes)
+    const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+    for (int i = gt; i < n_zero_a; i += gs) zero_a[i] = 0u;
+    for (int i = gt; i < n_zero_b; i += gs) zero_b[i] = 0u;
+  }
   const int lane = threadIdx.x & 31;
   const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (q >= nq) return;
@@ -546,6 +555,7 @@ __global__ void merge_partials_kernel(const float* __restrict__ part_s, const in
                                       float threshold, int32_t rank, int32_t world, int64_t B,
                                       const uint32_t* __restrict__ bound, const uint32_t* __restrict__ slots,
                                       int32_t slot_stride) {
+  ptx::griddep_wait();   // a programmatic dependent of the match kernel
   const int lane = threadIdx.x & 31;
   const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (q >= nq) return;
@@ -610,6 +620,7 @@ __global__ void __launch_bounds__(kMergeBlockThreads)
   __shared__ int32_t walk[KT];
   __shared__ int32_t n_heads, n_cand, kth_i;
   __shared__ float kth_s;
+  ptx::griddep_wait();   // a programmatic dependent of the match kernel
   const int q = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31;
   const float lb = tc_lower_bound(bound, slots, slot_stride, k, q);
@@ -780,15 +791,17 @@ cudaError_t launch_append(Pool& p, const void* emb_src, const float* joints_src,
 }
 
 cudaError_t launch_query_prep(Pool& p, const void* q_src, const float* qj_src, int32_t nq, const int32_t* perm,
-                              cudaStream_t s) {
+                              int32_t zero_bound, int32_t zero_slots, cudaStream_t s) {
   const int wpb = kPrepWarps;
   const auto& c = p.cfg;
   if (c.dtype == AMS_DTYPE_BF16)
-    query_prep_kernel<true><<<blocks_for(nq, wpb), wpb * 32, 0, s>>>(q_src, qj_src, nq, c.dim, c.joint_dim,
-                                                                     p.JP, perm, p.q_stage, p.q_inv, p.q_joints);
+    query_prep_kernel<true><<<blocks_for(nq, wpb), wpb * 32, 0, s>>>(
+        q_src, qj_src, nq, c.dim, c.joint_dim, p.JP, perm, p.q_stage, p.q_inv, p.q_joints, p.bound, zero_bound,
+        p.slots, zero_slots);
   else
-    query_prep_kernel<false><<<blocks_for(nq, wpb), wpb * 32, 0, s>>>(q_src, qj_src, nq, c.dim, c.joint_dim,
-                                                                      p.JP, perm, p.q_stage, p.q_inv, p.q_joints);
+    query_prep_kernel<false><<<blocks_for(nq, wpb), wpb * 32, 0, s>>>(
+        q_src, qj_src, nq, c.dim, c.joint_dim, p.JP, perm, p.q_stage, p.q_inv, p.q_joints, p.bound, zero_bound,
+        p.slots, zero_slots);
   ++p.launches;
   return cudaGetLastError();
 }
@@ -849,14 +862,28 @@ cudaError_t launch_merge_partials(Pool& p, const MatchArgs& a, int32_t P, float*
   // few queries, many lists: a block per query (the warp-per-query grid would leave most
   // SMs idle); KT = 64 keeps the warp kernel (64 KB of staging per block)
   const bool per_block = a.nq < 8 * p.num_sms && P >= 64 && a.KT <= 32;
-#define AMS_MERGE(KT_)                                                                                  \
-  if (per_block)                                                                                        \
-    merge_partials_block_kernel<KT_ <= 32 ? KT_ : 32><<<(unsigned)a.nq, kMergeBlockThreads, 0, s>>>(     \
-        p.part_s, p.part_i, a.nq, P, a.k, out_s, out_i, out_hit, a.threshold, c.rank, c.world, p.B, bnd, sl, \
-        a.KT);                                                                                          \
-  else                                                                                                  \
-    merge_partials_kernel<KT_><<<g, wpb * 32, 0, s>>>(p.part_s, p.part_i, a.nq, P, a.k, out_s, out_i, out_hit, \
-                                                       a.threshold, c.rank, c.world, p.B, bnd, sl, a.KT)
+  // a programmatic dependent of the match kernel: its launch overlaps that kernel's tail
+  cudaLaunchConfig_t cfg{};
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (per_block) {
+    cfg.gridDim = dim3((unsigned)a.nq);
+    cfg.blockDim = dim3(kMergeBlockThreads);
+  } else {
+    cfg.gridDim = dim3(g);
+    cfg.blockDim = dim3(wpb * 32);
+  }
+  cudaError_t e = cudaSuccess;
+#define AMS_MERGE(KT_)                                                                                      \
+  e = per_block ? cudaLaunchKernelEx(&cfg, merge_partials_block_kernel<KT_ <= 32 ? KT_ : 32>, p.part_s, p.part_i, \
+                                     a.nq, P, a.k, out_s, out_i, out_hit, a.threshold, c.rank, c.world, p.B, bnd, \
+                                     sl, (int32_t)a.KT)                                                        \
+                : cudaLaunchKernelEx(&cfg, merge_partials_kernel<KT_>, p.part_s, p.part_i, a.nq, P, a.k, out_s,  \
+                                     out_i, out_hit, a.threshold, c.rank, c.world, p.B, bnd, sl, (int32_t)a.KT)
   switch (a.KT) {
     case 8: AMS_MERGE(8); break;
     case 16: AMS_MERGE(16); break;
@@ -865,7 +892,7 @@ cudaError_t launch_merge_partials(Pool& p, const MatchArgs& a, int32_t P, float*
   }
 #undef AMS_MERGE
   ++p.launches;
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_merge_lists(const MatchArgs& a, int32_t G, int32_t kin, const float* in_s, const int64_t* in_i,

@@ -205,6 +205,10 @@ __global__ void __launch_bounds__(kScanThreads, 1)
   if (CG == 2) ptx::cluster_sync();   // peer barriers initialised before any remote traffic
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  // launched as a programmatic dependent of the query prep: everything above (barrier
+  // init, TMEM allocation, descriptor prefetch) overlapped it; its outputs (staged
+  // queries, norms, joints, zeroed bounds / slots) are read only below
+  ptx::griddep_wait();
   const int n_kb = prm.d / kBlockK;
 
   if (warp == kProducerWarp) {
@@ -633,6 +637,7 @@ __global__ void __launch_bounds__(kScanThreads, 1)
     }
   }
 
+  ptx::griddep_launch_dependents();   // the merge may be scheduled (it waits for our completion)
   ptx::tc_fence_before();
   __syncthreads();
   if (CG == 2) ptx::cluster_sync();   // no CTA leaves while its peer may still signal it
@@ -663,13 +668,15 @@ cudaError_t launch_scan_t(Pool& p, const ScanParams& prm, int box, int grid, cud
   cfg.blockDim = dim3(kScanThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // see griddep_wait()
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, kern, p.tmap_qs[box_index(box)], CG == 1 ? p.tmap_pool : p.tmap_pool2, prm);
 }
 
@@ -749,13 +756,14 @@ cudaError_t launch_match_scan(Pool& p, const MatchArgs& a, int32_t S, int32_t gr
   prm.g2 = a.g2;
   prm.k = a.k;
   if (prm.stages == 0 || grid % cg != 0) return cudaErrorInvalidValue;
-  cudaError_t e = cudaMemsetAsync(p.bound, 0, (size_t)(a.nq + 1) * sizeof(uint32_t), s);
-  if (e != cudaSuccess) return e;
+  cudaError_t e = cudaSuccess;
+  if (!a.zeroed && (e = cudaMemsetAsync(p.bound, 0, (size_t)(a.nq + 1) * sizeof(uint32_t), s)) != cudaSuccess)
+    return e;
   prm.slots = a.slots ? p.slots : nullptr;
   prm.glist_s = p.scan_glist_s;
   prm.glist_i = p.scan_glist_i;
   if (cg == 2 && (prm.glist_s == nullptr || grid > p.num_sms)) return cudaErrorInvalidValue;
-  if (prm.slots != nullptr) {
+  if (prm.slots != nullptr && !a.zeroed) {
     e = cudaMemsetAsync(p.slots, 0, (size_t)a.nq * a.KT * sizeof(uint32_t), s);
     if (e != cudaSuccess) return e;
   }

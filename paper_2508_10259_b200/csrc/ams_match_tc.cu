@@ -302,6 +302,10 @@ __global__ void __maxnreg__(168)
   __syncthreads();
   if (CL > 1) ptx::cluster_sync();   // peer barriers initialised before any remote traffic
   ptx::tc_fence_after();
+  // launched as a programmatic dependent of the query prep: everything above (barrier
+  // init, TMEM allocation, descriptor prefetch) overlapped it; its outputs (staged
+  // queries, norms, joints, zeroed bounds / slots) are read only below
+  ptx::griddep_wait();
   const uint32_t tmem_base = *tmem_holder;
 
   const int n_kb = prm.d / kBlockK;
@@ -574,6 +578,7 @@ __global__ void __maxnreg__(168)
     }
   }
 
+  ptx::griddep_launch_dependents();   // the merge may be scheduled (it waits for our completion)
   ptx::tc_fence_before();
   __syncthreads();
   if (CL > 1) ptx::cluster_sync();   // no CTA leaves while a peer may still signal it
@@ -594,13 +599,15 @@ cudaError_t launch_tc_t(Pool& p, const TcParams& prm, int grid, cudaStream_t s) 
   cfg.blockDim = dim3(kThreadsTc);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // see griddep_wait()
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CL;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, kern, p.tmap_q, CG == 1 ? p.tmap_pool : CL == CG ? p.tmap_pool2 : p.tmap_pool4,
                             prm);
 }
@@ -677,11 +684,12 @@ cudaError_t launch_match_tc(Pool& p, const MatchArgs& a, int32_t S, int32_t grid
   prm.gated = a.gated;
   prm.P = S * kEpiHalves;
   prm.g2 = a.g2;
-  cudaError_t e = cudaMemsetAsync(p.bound, 0, (size_t)(a.nq + 1) * sizeof(uint32_t), s);
-  if (e != cudaSuccess) return e;
+  cudaError_t e = cudaSuccess;
+  if (!a.zeroed && (e = cudaMemsetAsync(p.bound, 0, (size_t)(a.nq + 1) * sizeof(uint32_t), s)) != cudaSuccess)
+    return e;
   // ungated: the union bound needs >= k lists per query (each list fills one slot)
   prm.slots = (!a.gated && prm.P >= a.k) ? p.slots : nullptr;   // a.slots says so to the merge
-  if (prm.slots != nullptr) {
+  if (prm.slots != nullptr && !a.zeroed) {
     e = cudaMemsetAsync(p.slots, 0, (size_t)prm.n_qt * kBlockM * cg * a.KT * sizeof(uint32_t), s);
     if (e != cudaSuccess) return e;
   }
