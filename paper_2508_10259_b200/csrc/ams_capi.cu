@@ -642,11 +642,14 @@ static ams_status_t match_impl(ams_pool_t pool, const void* q_emb, const float* 
   // ungated, zeroed union slots: the prep kernel clears them (no memset node between it
   // and the dense kernel, which is then its programmatic dependent).  Slots: K2 indexes
   // them by padded query tile (<= round_up(nq, 256) rows), the small-batch kernel by query.
+  // (gate-first: the candidate counts)
   const bool dense_bf16 = !gate_first && p.cfg.dtype == AMS_DTYPE_BF16 && p.local > 0;
-  const int32_t zero_bound = dense_bf16 ? nq + 1 : 0;
+  const bool gf_bf16 = gate_first && p.cfg.dtype == AMS_DTYPE_BF16;
+  const int32_t zero_bound = dense_bf16 ? nq + 1 : gf_bf16 ? nq : 0;
   const int32_t zero_slots = dense_bf16 && !a.gated ? (int32_t)round_up(nq, 2 * ams::kBlockM) * a.KT : 0;
-  AMS_CUDA_TRY(ams::launch_query_prep(p, q_src, qj_src, nq, sorted ? p.q_perm : nullptr, zero_bound, zero_slots, s));
-  a.zeroed = dense_bf16 ? 1 : 0;
+  AMS_CUDA_TRY(ams::launch_query_prep(p, q_src, qj_src, nq, sorted ? p.q_perm : nullptr, gf_bf16 ? p.gf_cnt : p.bound,
+                                      zero_bound, p.slots, zero_slots, s));
+  a.zeroed = dense_bf16 || gf_bf16 ? 1 : 0;
   if (b >= 0) AMS_CUDA_TRY(cudaEventRecord(p.consumed[b], s));   // staging b read (order + prep)
 
   const bool multi = p.collective;

@@ -28,7 +28,7 @@
 namespace ams {
 namespace {
 
-constexpr int kGfThreads = 256;   // queries per block
+constexpr int kGfThreads = 256;   // threads per gate-scan block (= queries per block at QT = 256)
 constexpr int kGfTile = kRowAlign; // 256 rows per staged joint tile
 
 // The rows a scan visits: a contiguous range of a tile-transposed joint array, either
@@ -50,7 +50,10 @@ __device__ __forceinline__ int snap_bin(float v, float lo, float scale) {
   return (f >= 0.0f && f < (float)kSnapBins) ? (int)f : (f >= 0.0f ? kSnapBins - 1 : 0);
 }
 
-template <int JP>
+// QT queries per block (32..256): warp w takes query slot w % (QT/32) and, when QT < 256,
+// row part w / (QT/32) of every staged tile, so a small batch keeps all 8 warps busy on
+// its few queries instead of running 256-thread blocks of mostly inactive warps.
+template <int JP, int QT>
 __global__ void __launch_bounds__(kGfThreads)
     gate_scan_kernel(const GfRows rows, const float* __restrict__ q_joints, int32_t nq, int32_t S, float g2,
                      int32_t cap, uint32_t* __restrict__ cnt, int32_t* __restrict__ cand, int32_t sorted) {
@@ -58,9 +61,14 @@ __global__ void __launch_bounds__(kGfThreads)
   __shared__ __align__(16) float pn[kGfTile];       // per row: sum of squares of the first 4 joints
   __shared__ unsigned int pmax_bits;
   __shared__ float blk_lo[kGfThreads / 32], blk_hi[kGfThreads / 32];
+  constexpr int kSlots = QT / 32, kParts = kGfThreads / QT;   // query slots x row parts = 8 warps
+  constexpr int kC8 = kGfTile / 8 / kParts;                    // 8-row groups per row part
+  static_assert(kC8 % 4 == 0, "row parts must hold whole 32-row groups");
+  ptx::griddep_wait();   // a programmatic dependent of the query prep (joints, zeroed counts)
   const float* __restrict__ pool_joints = rows.jt;
   const int qg = blockIdx.x, sp = blockIdx.y;
-  const int q = qg * kGfThreads + threadIdx.x;
+  const int q = qg * QT + ((int)(threadIdx.x >> 5) % kSlots) * 32 + (int)(threadIdx.x & 31);
+  const int c8_lo = ((int)(threadIdx.x >> 5) / kSlots) * kC8;
   const bool active = q < nq;
   float qj[JP];
 #pragma unroll
@@ -161,7 +169,7 @@ __global__ void __launch_bounds__(kGfThreads)
       if (active && c >= cmin && c < nvalid && ds <= g2) emit(c);
     };
 #pragma unroll 1
-    for (int c8 = 0; c8 < kGfTile / 8; ++c8) {
+    for (int c8 = c8_lo; c8 < c8_lo + kC8; ++c8) {
       if (sorted && (c8 & 3) == 0) {
         // warp-level two-joint test of the next 32 rows (ams_match_tc.cu
         // epi_chunk_sorted): ineligible for every lane when it fails
@@ -216,19 +224,79 @@ __global__ void __launch_bounds__(kGfThreads)
       for (int c = 8 * c8; c < 8 * c8 + 8; ++c) exact(c);
     }
   }
+  ptx::griddep_launch_dependents();
+}
+
+// Tiny batches (nq <= kGfRowsMaxQ) on the plain row range: thread per row, the exact
+// canonical gate of the row against every query, no staging and no block barriers, so
+// the scan streams the pool's joints (4 JP bytes per row) at HBM speed instead of paying
+// the warp-per-32-queries kernel's per-tile overhead for one or two live lanes (C5 pool,
+// 1 query: 64 us there).  Eligible rows go to the query's bucket as in gate_scan_kernel
+// (bucket order is irrelevant: the score kernel orders by (score, index)).
+constexpr int kGfRowsMaxQ = 16;
+constexpr int kGfRowsThreads = 256;
+
+template <int JP>
+__global__ void __launch_bounds__(kGfRowsThreads)
+    gate_rows_kernel(const float* __restrict__ pool_joints, int64_t L, const float* __restrict__ q_joints,
+                     int32_t nq, float g2, int32_t cap, uint32_t* __restrict__ cnt, int32_t* __restrict__ cand) {
+  __shared__ float qs[kGfRowsMaxQ * JP];
+  ptx::griddep_wait();   // a programmatic dependent of the query prep
+  for (int i = threadIdx.x; i < nq * JP; i += kGfRowsThreads) qs[i] = q_joints[i];
+  __syncthreads();
+  constexpr int kU = 4;   // rows per thread in flight
+  const int64_t stride = (int64_t)gridDim.x * kGfRowsThreads;
+  for (int64_t j0 = (int64_t)blockIdx.x * kGfRowsThreads + threadIdx.x; j0 < L; j0 += kU * stride) {
+    float pj[kU][JP];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t j = j0 + u * stride;
+#pragma unroll
+      for (int t = 0; t < JP; ++t) pj[u][t] = j < L ? __ldcs(pool_joints + joint_offset(j, t, JP)) : 0.0f;
+    }
+    for (int qi = 0; qi < nq; ++qi) {
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        float ds = 0.0f;
+#pragma unroll
+        for (int t = 0; t < JP; ++t) {
+          const float df = __fsub_rn(qs[qi * JP + t], pj[u][t]);
+          ds = __fmaf_rn(df, df, ds);
+        }
+        if (ds <= g2 && j0 + u * stride < L) {   // (g2 may be +inf: the row bound is explicit)
+          const uint32_t slot = atomicAdd(&cnt[qi], 1u);
+          if (slot < (uint32_t)cap) cand[(int64_t)qi * cap + slot] = (int32_t)(j0 + u * stride);
+        }
+      }
+    }
+  }
+  ptx::griddep_launch_dependents();
 }
 
 __device__ __forceinline__ float bf16_dot_lane(const uint4* __restrict__ a, const uint4* __restrict__ b, int n16,
                                                int lane) {
-  // lanes take 16-byte pieces lane, lane+32, ...; fp32 accumulation in a fixed order
+  // lanes take 16-byte pieces lane, lane+32, ...; fp32 accumulation in a fixed order.
+  // Pieces are loaded 8 at a time before their FMAs (one round trip per 8 instead of per
+  // piece: a d = 4096 row is 16 pieces per lane); the FMA order is unchanged.
   float acc = 0.0f;
-  for (int i = lane; i < n16; i += 32) {
-    const uint4 x = __ldg(a + i), y = __ldg(b + i);
-    const uint32_t xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w};
+  constexpr int kB = 8;
+  for (int i0 = lane; i0 < n16; i0 += 32 * kB) {
+    uint4 x[kB], y[kB];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      acc = __fmaf_rn(__uint_as_float(xs[u] << 16), __uint_as_float(ys[u] << 16), acc);
-      acc = __fmaf_rn(__uint_as_float(xs[u] & 0xFFFF0000u), __uint_as_float(ys[u] & 0xFFFF0000u), acc);
+    for (int u = 0; u < kB; ++u) {
+      const int i = i0 + 32 * u;
+      x[u] = i < n16 ? __ldg(a + i) : make_uint4(0u, 0u, 0u, 0u);
+      y[u] = i < n16 ? __ldg(b + i) : make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (int u = 0; u < kB; ++u) {
+      if (i0 + 32 * u >= n16) break;
+      const uint32_t xs[4] = {x[u].x, x[u].y, x[u].z, x[u].w}, ys[4] = {y[u].x, y[u].y, y[u].z, y[u].w};
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        acc = __fmaf_rn(__uint_as_float(xs[v] << 16), __uint_as_float(ys[v] << 16), acc);
+        acc = __fmaf_rn(__uint_as_float(xs[v] & 0xFFFF0000u), __uint_as_float(ys[v] & 0xFFFF0000u), acc);
+      }
     }
   }
 #pragma unroll
@@ -244,6 +312,7 @@ __global__ void score_kernel(const uint16_t* __restrict__ emb, const float* __re
                              const int32_t* __restrict__ cand, float* __restrict__ out_s, int64_t* __restrict__ out_i,
                              uint8_t* __restrict__ out_hit, float threshold, int32_t rank, int32_t world,
                              int64_t B, const int32_t* __restrict__ perm) {
+  ptx::griddep_wait();   // a programmatic dependent of the gate scan (buckets complete)
   const int lane = threadIdx.x & 31;
   const int qi = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (qi >= nq) return;
@@ -286,8 +355,21 @@ __global__ void score_kernel(const uint16_t* __restrict__ emb, const float* __re
       if (s > top.kth_s) top.insert_monotone(s, (int32_t)j, k);
     }
   }
-  // k rounds of a butterfly arg-max over the lanes' lists (only lane 0's list is
-  // populated on the bucket path)
+  if (n <= (uint32_t)cap) {
+    // bucket path: lane 0's list is the whole (sorted) result -- write it directly
+    if (lane == 0) {
+#pragma unroll
+      for (int r = 0; r < KT; ++r) {
+        if (r >= k) break;
+        const bool v = top.i[r] >= 0;
+        out_s[qo * k + r] = v ? top.s[r] : -CUDART_INF_F;
+        out_i[qo * k + r] = v ? shard_global((int64_t)top.i[r], rank, world, B) : -1;
+      }
+      if (out_hit != nullptr) out_hit[qo] = (top.i[0] >= 0 && top.s[0] >= threshold) ? 1 : 0;
+    }
+    return;
+  }
+  // overflow path: k rounds of a butterfly arg-max over the lanes' lists
   float s0 = -CUDART_INF_F;
   int64_t i0 = -1;
   for (int r = 0; r < k; ++r) {
@@ -430,49 +512,98 @@ cudaError_t snap_refresh(Pool& p, cudaStream_t s) {
   return cudaSuccess;
 }
 
+// gate-first kernels are programmatic dependents of the kernel before them (query prep,
+// then the gate scan): each starts with griddep_wait()
+inline cudaLaunchConfig_t gf_config(dim3 grid, int threads, cudaStream_t s, cudaLaunchAttribute* attr) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(threads);
+  cfg.stream = s;
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cfg;
+}
+
+// One gate-scan launch over `tiles` joint tiles with QT queries per block: ~2 full waves
+// of resident blocks, but >= 8 tiles per block so per-block setup stays amortised.
+// (Resident blocks per SM depend only on the kernel and the B200's limits: cached.)
+template <int JP, int QT>
+cudaError_t launch_gate_scan(Pool& p, const MatchArgs& a, int32_t cap, const GfRows& rows, int64_t tiles,
+                             int32_t sorted, cudaStream_t s) {
+  static int occ = 0;
+  if (occ == 0) {
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gate_scan_kernel<JP, QT>, kGfThreads, 0);
+    if (e != cudaSuccess) return e;
+    occ = std::max(occ, 1);
+  }
+  const int n_qg = (a.nq + QT - 1) / QT;
+  const int S = (int)std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(1, tiles / 8),
+                                                            (2 * (int64_t)occ * p.num_sms + n_qg - 1) / n_qg));
+  cudaLaunchAttribute attr[1];
+  const cudaLaunchConfig_t cfg = gf_config(dim3(n_qg, S), kGfThreads, s, attr);
+  ++p.launches;
+  return cudaLaunchKernelEx(&cfg, gate_scan_kernel<JP, QT>, rows, static_cast<const float*>(p.q_joints), a.nq, S,
+                            a.g2, cap, p.gf_cnt, p.gf_cand, sorted);
+}
+
+template <int JP>
+cudaError_t launch_gate_scan_q(Pool& p, const MatchArgs& a, int32_t cap, const GfRows& rows, int64_t tiles,
+                               int32_t sorted, cudaStream_t s) {
+  // queries per block: the batch rounded up to a power-of-two warp multiple; the other
+  // warps split the rows (C5 pool, 64 queries: 340 us with 256 queries per block)
+  if (a.nq <= 32) return launch_gate_scan<JP, 32>(p, a, cap, rows, tiles, sorted, s);
+  if (a.nq <= 64) return launch_gate_scan<JP, 64>(p, a, cap, rows, tiles, sorted, s);
+  if (a.nq <= 128) return launch_gate_scan<JP, 128>(p, a, cap, rows, tiles, sorted, s);
+  return launch_gate_scan<JP, kGfThreads>(p, a, cap, rows, tiles, sorted, s);
+}
+
 template <int JP>
 cudaError_t launch_gf_jp(Pool& p, const MatchArgs& a, int32_t cap, float* out_s, int64_t* out_i, uint8_t* out_hit,
                          bool sorted, cudaStream_t s) {
-  const int n_qg = (a.nq + kGfThreads - 1) / kGfThreads;
   const int64_t n_pt = (p.local + kGfTile - 1) / kGfTile;
-  // ~2 full waves of resident blocks (6 blocks/SM: 34 KB smem, 256 threads)
-  // but keep >= 8 tiles per block so per-block setup stays amortised for small batches
-  int S = (int)std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(1, n_pt / 8),
-                                                      (12 * (int64_t)p.num_sms + n_qg - 1) / n_qg));
-  cudaError_t e = cudaMemsetAsync(p.gf_cnt, 0, (size_t)a.nq * sizeof(uint32_t), s);
-  if (e != cudaSuccess) return e;
-  // Sorted batches on large pools scan the joint-0 index: each block of 256 queries
-  // visits only the rows within gamma of its joint-0 interval (plus the unsorted tail).
+  cudaError_t e = cudaSuccess;
+  if (!a.zeroed && (e = cudaMemsetAsync(p.gf_cnt, 0, (size_t)a.nq * sizeof(uint32_t), s)) != cudaSuccess) return e;
+  // Sorted batches on large pools scan the joint-0 index: each block of queries visits
+  // only the rows within gamma of its joint-0 interval (plus the unsorted tail).
   const bool snap = sorted && p.local >= kSnapMinRows;
   if (snap && (e = snap_refresh(p, s)) != cudaSuccess) return e;
   const int64_t plain_begin = snap ? p.snap_L : 0;
   if (snap) {
     const GfRows rows{p.snap_j, p.snap_id, 0, p.snap_L, p.snap_off,
                       reinterpret_cast<const float*>(p.snap_aux + kSnapBins + 2)};
-    gate_scan_kernel<JP><<<dim3(n_qg, S), kGfThreads, 0, s>>>(rows, p.q_joints, a.nq, S, a.g2, cap, p.gf_cnt,
-                                                                p.gf_cand, 1);
-    ++p.launches;
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = launch_gate_scan_q<JP>(p, a, cap, rows, n_pt, 1, s)) != cudaSuccess) return e;
   }
-  if (p.local > plain_begin) {
-    const int64_t tail_tiles = (p.local + kGfTile - 1) / kGfTile - plain_begin / kGfTile;
-    const int St = snap ? (int)std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(1, tail_tiles / 8),
-                                                                      (12 * (int64_t)p.num_sms + n_qg - 1) / n_qg))
-                        : S;
-    const GfRows rows{p.joints, nullptr, plain_begin, p.local, nullptr, nullptr};
-    gate_scan_kernel<JP><<<dim3(n_qg, St), kGfThreads, 0, s>>>(rows, p.q_joints, a.nq, St, a.g2, cap, p.gf_cnt,
-                                                                 p.gf_cand, sorted ? 1 : 0);
+  if (p.local > plain_begin && plain_begin == 0 && a.nq <= kGfRowsMaxQ) {
+    // tiny batch over the whole pool: the row-parallel kernel (~2 waves of 8 blocks per SM)
+    const unsigned grid = (unsigned)std::max<int64_t>(
+        1, std::min<int64_t>((p.local + kGfRowsThreads - 1) / kGfRowsThreads, 16 * (int64_t)p.num_sms));
+    cudaLaunchAttribute attr[1];
+    const cudaLaunchConfig_t cfg = gf_config(dim3(grid), kGfRowsThreads, s, attr);
     ++p.launches;
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = cudaLaunchKernelEx(&cfg, gate_rows_kernel<JP>, static_cast<const float*>(p.joints), p.local,
+                                static_cast<const float*>(p.q_joints), a.nq, a.g2, cap, p.gf_cnt, p.gf_cand)) !=
+        cudaSuccess)
+      return e;
+  } else if (p.local > plain_begin) {
+    const int64_t tail_tiles = (p.local + kGfTile - 1) / kGfTile - plain_begin / kGfTile;
+    const GfRows rows{p.joints, nullptr, plain_begin, p.local, nullptr, nullptr};
+    if ((e = launch_gate_scan_q<JP>(p, a, cap, rows, tail_tiles, sorted ? 1 : 0, s)) != cudaSuccess) return e;
   }
   const int wpb = 4;
   const unsigned g = (unsigned)((a.nq + wpb - 1) / wpb);
   const auto& c = p.cfg;
-#define AMS_GF(KT_)                                                                                         \
-  score_kernel<KT_, JP><<<g, wpb * 32, 0, s>>>(static_cast<const uint16_t*>(p.emb), p.inv_norm, p.joints, p.local, \
-                                               static_cast<const uint16_t*>(p.q_stage), p.q_inv, p.q_joints, c.dim, \
-                                               a.nq, a.k, a.g2, cap, p.gf_cnt, p.gf_cand, out_s, out_i, out_hit,    \
-                                               a.threshold, c.rank, c.world, p.B, sorted ? p.q_perm : nullptr)
+  cudaLaunchAttribute attr[1];
+  const cudaLaunchConfig_t cfg = gf_config(dim3(g), wpb * 32, s, attr);
+#define AMS_GF(KT_)                                                                                           \
+  e = cudaLaunchKernelEx(&cfg, score_kernel<KT_, JP>, static_cast<const uint16_t*>(p.emb),                    \
+                         static_cast<const float*>(p.inv_norm), static_cast<const float*>(p.joints), p.local,   \
+                         static_cast<const uint16_t*>(p.q_stage), static_cast<const float*>(p.q_inv),           \
+                         static_cast<const float*>(p.q_joints), c.dim, a.nq, a.k, a.g2, cap,                   \
+                         static_cast<const uint32_t*>(p.gf_cnt), static_cast<const int32_t*>(p.gf_cand), out_s, \
+                         out_i, out_hit, a.threshold, c.rank, c.world, p.B,                                    \
+                         static_cast<const int32_t*>(sorted ? p.q_perm : nullptr))
   switch (a.KT) {
     case 8: AMS_GF(8); break;
     case 16: AMS_GF(16); break;
@@ -481,7 +612,7 @@ cudaError_t launch_gf_jp(Pool& p, const MatchArgs& a, int32_t cap, float* out_s,
   }
 #undef AMS_GF
   ++p.launches;
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 // Pass-rate estimate for ams_match_auto: exact canonical gate over a strided sample of

@@ -145,6 +145,7 @@ struct Pool {
   CUtensorMap tmap_pool4{};  // bf16 pool [cap_pad, d], box {64, 64}, SW128 (multicast quarter tile)
   CUtensorMap tmap_q{};      // bf16 queries [q_pad, d], box {64, 128}, SW128
   CUtensorMap tmap_qs[16]{}; // bf16 queries [q_pad, d], box {64, 8 (i + 1)}, SW128 (small-batch kernel)
+  size_t simt_smem_opt[4] = {0, 0, 0, 0};   // dynamic smem opted in per SIMT kernel (KT 8/16/32/64)
   int32_t kernel_policy = 0; // bit 0: never the small-batch kernel; bit 1: 4-CTA multicast clusters;
                              // bit 2: wide (two tiles per stage) small-batch CTA pairs;
                              // bit 3: ungated 129-256-query batches on the small-batch CTA pairs
@@ -191,16 +192,18 @@ struct MatchArgs {
   int32_t gated;      // g2 < +inf
   float threshold;
   int32_t slots;      // the tcgen05 kernel filled p.slots (union bound) for the merge
-  int32_t zeroed;     // query prep already zeroed p.bound / p.slots for this call
+  int32_t zeroed;     // query prep already zeroed this call's counters (p.bound / p.slots or p.gf_cnt)
 };
 
 cudaError_t launch_append(Pool& p, const void* emb_src, const float* joints_src, int64_t n_src,
                           int64_t first_global, cudaStream_t s);
 // perm (device, may be null = identity): staged row q is the caller's query perm[q].
-// Also zeroes p.bound[0, zero_bound) and p.slots[0, zero_slots) for the dense kernel that
-// follows, which launch_match_tc / launch_match_scan then no longer memset (zero_bound > 0).
+// Also zeroes zero_a[0, n_zero_a) and zero_b[0, n_zero_b): the counters of the kernel that
+// follows (dense: p.bound and p.slots; gate-first: p.gf_cnt), which its launcher then no
+// longer memsets (MatchArgs::zeroed), so that kernel can be the prep's programmatic dependent.
 cudaError_t launch_query_prep(Pool& p, const void* q_src, const float* qj_src, int32_t nq, const int32_t* perm,
-                              int32_t zero_bound, int32_t zero_slots, cudaStream_t s);
+                              uint32_t* zero_a, int32_t n_zero_a, uint32_t* zero_b, int32_t n_zero_b,
+                              cudaStream_t s);
 // p.q_perm <- the queries ordered by joint 0 (counting sort into linear bins; one block)
 cudaError_t launch_query_order(Pool& p, const float* qj_src, int32_t nq, cudaStream_t s);
 cudaError_t launch_match_simt(Pool& p, const MatchArgs& a, int32_t splits, cudaStream_t s);

@@ -82,7 +82,7 @@ __global__ void query_prep_kernel(const void* __restrict__ src, const float* __r
   // the dense kernel that follows (launched as a programmatic dependent) may start its
   // prologue now; it reads nothing of ours before griddep_wait()
   ptx::griddep_launch_dependents();
-  {   // its per-query bounds and union slots start at zero (replaces two memset nodes)
+  {   // its counters (per-query bounds and union slots, or candidate counts) start at zero
     const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
     for (int i = gt; i < n_zero_a; i += gs) zero_a[i] = 0u;
     for (int i = gt; i < n_zero_b; i += gs) zero_b[i] = 0u;
@@ -280,6 +280,7 @@ __global__ void __launch_bounds__(kSimtThreads)
                           int32_t S, int32_t k, float g2, int32_t gated, float* __restrict__ part_s,
                           int32_t* __restrict__ part_i, int32_t P) {
   extern __shared__ __align__(16) float qs[];
+  ptx::griddep_wait();   // a programmatic dependent of the query prep
   const int qi = blockIdx.x / S;
   const int sp = blockIdx.x % S;
   for (int t = threadIdx.x; t < d; t += blockDim.x) qs[t] = q[(int64_t)qi * d + t];
@@ -372,6 +373,7 @@ __global__ void __launch_bounds__(kTileThreads)
   __shared__ float sR[kTileK][kTileRows + 1];
   __shared__ float sQ[kTileK][kTileQ + 1];
   __shared__ float sS[kTileQ][kTileRows + 1];
+  ptx::griddep_wait();   // a programmatic dependent of the query prep
   const int rt = blockIdx.x, qt = blockIdx.y;
   const int64_t r0 = (int64_t)rt * kTileRows;
   const int q0 = qt * kTileQ;
@@ -791,17 +793,18 @@ cudaError_t launch_append(Pool& p, const void* emb_src, const float* joints_src,
 }
 
 cudaError_t launch_query_prep(Pool& p, const void* q_src, const float* qj_src, int32_t nq, const int32_t* perm,
-                              int32_t zero_bound, int32_t zero_slots, cudaStream_t s) {
+                              uint32_t* zero_a, int32_t n_zero_a, uint32_t* zero_b, int32_t n_zero_b,
+                              cudaStream_t s) {
   const int wpb = kPrepWarps;
   const auto& c = p.cfg;
   if (c.dtype == AMS_DTYPE_BF16)
     query_prep_kernel<true><<<blocks_for(nq, wpb), wpb * 32, 0, s>>>(
-        q_src, qj_src, nq, c.dim, c.joint_dim, p.JP, perm, p.q_stage, p.q_inv, p.q_joints, p.bound, zero_bound,
-        p.slots, zero_slots);
+        q_src, qj_src, nq, c.dim, c.joint_dim, p.JP, perm, p.q_stage, p.q_inv, p.q_joints, zero_a, n_zero_a,
+        zero_b, n_zero_b);
   else
     query_prep_kernel<false><<<blocks_for(nq, wpb), wpb * 32, 0, s>>>(
-        q_src, qj_src, nq, c.dim, c.joint_dim, p.JP, perm, p.q_stage, p.q_inv, p.q_joints, p.bound, zero_bound,
-        p.slots, zero_slots);
+        q_src, qj_src, nq, c.dim, c.joint_dim, p.JP, perm, p.q_stage, p.q_inv, p.q_joints, zero_a, n_zero_a,
+        zero_b, n_zero_b);
   ++p.launches;
   return cudaGetLastError();
 }
@@ -812,35 +815,63 @@ cudaError_t launch_query_order(Pool& p, const float* qj_src, int32_t nq, cudaStr
   return cudaGetLastError();
 }
 
+// fp32 kernels: programmatic dependents of the query prep (launch overlaps its tail)
+inline cudaLaunchConfig_t pdl_config(dim3 grid, dim3 block, size_t smem, cudaStream_t s, cudaLaunchAttribute* attr) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cfg;
+}
+
 cudaError_t launch_match_simt(Pool& p, const MatchArgs& a, int32_t S, cudaStream_t s) {
   const int32_t P = S * kSimtThreads;
   const size_t smem = ((size_t)((p.cfg.dim + 3) & ~3) + (size_t)(kSimtThreads / 32) * kSimtChunk) * sizeof(float);
-  const dim3 grid((unsigned)(a.nq * S));
-#define AMS_SIMT(KT_)                                                                                  \
-  cudaFuncSetAttribute(match_simt_f32_kernel<KT_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-  match_simt_f32_kernel<KT_><<<grid, kSimtThreads, smem, s>>>(                                        \
-      static_cast<const float*>(p.emb), p.inv_norm, p.joints, p.local, static_cast<const float*>(p.q_stage), \
-      p.q_inv, p.q_joints, p.cfg.dim, p.JP, S, a.k, a.g2, a.gated, p.part_s, p.part_i, P)
+  cudaLaunchAttribute attr[1];
+  const cudaLaunchConfig_t cfg = pdl_config(dim3((unsigned)(a.nq * S)), dim3(kSimtThreads), smem, s, attr);
+  cudaError_t e = cudaSuccess;
+  // the dynamic shared-memory opt-in is set once per pool and size (a host call per match otherwise)
+  size_t* opted = p.simt_smem_opt;
+#define AMS_SIMT(KT_, SLOT_)                                                                                  \
+  if (opted[SLOT_] < smem) {                                                                                  \
+    if ((e = cudaFuncSetAttribute(match_simt_f32_kernel<KT_>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                                  (int)smem)) != cudaSuccess)                                                 \
+      return e;                                                                                               \
+    opted[SLOT_] = smem;                                                                                      \
+  }                                                                                                           \
+  e = cudaLaunchKernelEx(&cfg, match_simt_f32_kernel<KT_>, static_cast<const float*>(p.emb),                 \
+                         static_cast<const float*>(p.inv_norm), static_cast<const float*>(p.joints), p.local,  \
+                         static_cast<const float*>(p.q_stage), static_cast<const float*>(p.q_inv),             \
+                         static_cast<const float*>(p.q_joints), p.cfg.dim, p.JP, S, a.k, a.g2, a.gated, p.part_s, \
+                         p.part_i, P)
   switch (a.KT) {
-    case 8: AMS_SIMT(8); break;
-    case 16: AMS_SIMT(16); break;
-    case 32: AMS_SIMT(32); break;
-    default: AMS_SIMT(64); break;
+    case 8: AMS_SIMT(8, 0); break;
+    case 16: AMS_SIMT(16, 1); break;
+    case 32: AMS_SIMT(32, 2); break;
+    default: AMS_SIMT(64, 3); break;
   }
 #undef AMS_SIMT
   ++p.launches;
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 int f32_tile_lists(int64_t L) { return (int)((L + kTileRows - 1) / kTileRows); }
 
 cudaError_t launch_match_f32_tile(Pool& p, const MatchArgs& a, cudaStream_t s) {
   const int32_t P = f32_tile_lists(p.local);
-  const dim3 grid((unsigned)P, (unsigned)((a.nq + kTileQ - 1) / kTileQ));
-#define AMS_F32T(KT_)                                                                                    \
-  match_f32_tile_kernel<KT_><<<grid, kTileThreads, 0, s>>>(static_cast<const float*>(p.emb), p.inv_norm, p.local, \
-                                                          static_cast<const float*>(p.q_stage), p.q_inv, a.nq,     \
-                                                          p.cfg.dim, a.k, p.part_s, p.part_i, P)
+  cudaLaunchAttribute attr[1];
+  const cudaLaunchConfig_t cfg =
+      pdl_config(dim3((unsigned)P, (unsigned)((a.nq + kTileQ - 1) / kTileQ)), dim3(kTileThreads), 0, s, attr);
+  cudaError_t e = cudaSuccess;
+#define AMS_F32T(KT_)                                                                                        \
+  e = cudaLaunchKernelEx(&cfg, match_f32_tile_kernel<KT_>, static_cast<const float*>(p.emb),                 \
+                         static_cast<const float*>(p.inv_norm), p.local, static_cast<const float*>(p.q_stage), \
+                         static_cast<const float*>(p.q_inv), a.nq, p.cfg.dim, a.k, p.part_s, p.part_i, P)
   switch (a.KT) {
     case 8: AMS_F32T(8); break;
     case 16: AMS_F32T(16); break;
@@ -849,7 +880,7 @@ cudaError_t launch_match_f32_tile(Pool& p, const MatchArgs& a, cudaStream_t s) {
   }
 #undef AMS_F32T
   ++p.launches;
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_merge_partials(Pool& p, const MatchArgs& a, int32_t P, float* out_s, int64_t* out_i,

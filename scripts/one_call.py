@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """A few identical ams_match calls on a config's pool, for ncu captures of one kernel.
 
-    python scripts/one_call.py c3 --nq 200 --k 8 [--policy P] [--gamma G] [--calls N] [--gate-first] [--timeline]
+    python scripts/one_call.py c3 --nq 200 --k 8 [--policy P] [--gamma G] [--calls N] [--gate-first | --auto] [--timeline]
 
 Builds the pool with the ams_gen recipe (not timed), then issues N calls (default 5);
 prints the median CUDA-event time per call and the plan.  ncu: -k regex:match_scan
@@ -31,11 +31,23 @@ def main():
     dev = torch.device("cuda", 0)
     pool = ams.Pool(cfg.d, cfg.J, cfg.M, max(nq, 1), max(k, 1), dtype="bf16", device=0)
     ams.ams_pool_set_kernel_policy(pool.handle, policy)
-    q, qj, _ = ams_gen.build_device_workload(cfg, dev, lambda e, j, n: pool.append(e, j, n), Q=max(nq, 64))
+    if cfg.dtype == "fp32":   # configs[0]: the host recipe (no mixture components)
+        w = ams_gen.generate_host(cfg)
+        pool.close()
+        pool = ams.Pool(cfg.d, cfg.J, cfg.M, max(nq, 1), max(k, 1), dtype="fp32", device=0)
+        ams.ams_pool_set_kernel_policy(pool.handle, policy)
+        pool.append(torch.from_numpy(w.emb).to(dev), torch.from_numpy(w.joints).to(dev))
+        reps = (nq + cfg.Q - 1) // cfg.Q
+        q = torch.from_numpy(w.q_emb).to(dev).repeat(reps, 1)
+        qj = torch.from_numpy(w.q_joints).to(dev).repeat(reps, 1)
+    else:
+        q, qj, _ = ams_gen.build_device_workload(cfg, dev, lambda e, j, n: pool.append(e, j, n), Q=max(nq, 64))
     q, qj = q[:nq].contiguous(), qj[:nq].contiguous()
     out = (torch.empty(nq, k, dtype=torch.int64, device=dev), torch.empty(nq, k, dtype=torch.float32, device=dev),
            torch.empty(nq, dtype=torch.uint8, device=dev))
     fn = ams.ams_match_gate_first if "--gate-first" in sys.argv else ams.ams_match
+    if "--auto" in sys.argv:   # the routed entry point (cost model; may run the gate estimate)
+        fn = ams.ams_match_auto
     s = torch.cuda.current_stream()
     ts = []
     for _ in range(calls):

@@ -56,6 +56,21 @@ def test_gate_first_bucket_overflow_is_exact(ams, gamma):
     check_bf16(*g, orc, cfg.theta)
 
 
+@pytest.mark.parametrize("nq", [1, 2, 16, 17, 32, 33, 64, 65, 128, 129, 256])
+@pytest.mark.parametrize("gamma", [0.6, INF])
+def test_gate_first_batch_shapes(ams, nq, gamma):
+    """Batch-size dispatch of the gate scan: <= 16 queries take the row-parallel kernel
+    (thread per row, exact gate against every query), larger batches the warp kernel with
+    32 / 64 / 128 / 256 queries per block (warps split the rows when fewer than 256).  A
+    ragged pool (rows past the last full tile) and gamma = inf (every row eligible: with
+    k = 5 the buckets overflow and the exact scan runs) for each side of every boundary."""
+    cfg = ams_gen.small_variant("c5", 3001, nq)
+    w = ams_gen.generate_host(cfg)
+    orc = oracle.match(w.emb, w.joints, w.q_emb, w.q_joints, cfg.k, cfg.theta, gamma)
+    g = run(ams, w, cfg.k, cfg.theta, gamma, True)
+    check_bf16(*g, orc, cfg.theta)
+
+
 def test_gate_first_ties_and_padding(ams):
     rng = np.random.Generator(np.random.PCG64(5))
     d, J, M = 128, 7, 3000
