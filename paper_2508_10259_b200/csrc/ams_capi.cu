@@ -244,7 +244,7 @@ void free_all(Pool& p) {
   void* ptrs[] = {p.scan_glist_s, p.scan_glist_i, p.emb, p.inv_norm, p.joints, p.q_stage, p.q_inv, p.q_joints,
                   p.q_joints_raw[0], p.q_joints_raw[1],
                   p.q_raw[0], p.q_raw[1], p.q_perm, p.bound, p.slots,
-                  p.gf_cnt, p.gf_cand, p.snap_j, p.snap_id, p.snap_off, p.snap_aux,
+                  p.gf_cnt, p.gf_cand, p.gf_qbins, p.snap_j, p.snap_id, p.snap_off, p.snap_aux,
                   p.part_s, p.part_i, p.shard_s, p.shard_i, p.gath_s, p.gath_i, p.stage_emb,
                   p.stage_joints, p.est_dev};
   for (void* q : ptrs)
@@ -399,7 +399,8 @@ ams_status_t ams_pool_create(const ams_pool_config_t* cfg, ams_pool_t* out) {
   }
   if (ok && c.dtype == AMS_DTYPE_BF16) {
     p.gf_cap = std::max(256, 8 * c.max_k);
-    ok = alloc((void**)&p.gf_cnt, (size_t)p.q_pad * 4) && alloc((void**)&p.gf_cand, (size_t)p.q_pad * p.gf_cap * 4);
+    ok = alloc((void**)&p.gf_cnt, (size_t)p.q_pad * 4) && alloc((void**)&p.gf_cand, (size_t)p.q_pad * p.gf_cap * 4) &&
+         alloc((void**)&p.gf_qbins, (size_t)(ams::kQBins + 3) * 4);
   }
   if (ok) ok = alloc((void**)&p.est_dev, 16);
   p.collective = c.world > 1 || c.nccl_id != nullptr;
@@ -636,8 +637,17 @@ static ams_status_t match_impl(ams_pool_t pool, const void* q_emb, const float* 
                         (nq <= ams::kBlockM || a.gated || (p.kernel_policy & 8) != 0) &&
                         ams::scan_stages(p, nq, a.KT) > 0 &&
                         (int64_t)nq * ams::scan_lists_per_split(nq, a.KT, a.gated != 0) * a.KT <= p.part_cap;   // >= 1 split fits
-  const bool sorted = p.cfg.dtype == AMS_DTYPE_BF16 && a.gated && p.local > 0 && nq >= kSortMinQueries && !use_scan;
-  if (sorted) AMS_CUDA_TRY(ams::launch_query_order(p, qj_src, nq, s));
+  // Gated gate-first batches of 17..1024 queries are staged in joint-0 bins instead (the
+  // row kernel looks up, per pool row, the queries within gamma of its joint 0).
+  const bool qbins = gate_first && p.cfg.dtype == AMS_DTYPE_BF16 && a.gated && p.local > 0 &&
+                     nq > ams::kGfRowsMaxQ && nq <= ams::kGfBinnedMaxQ;
+  const bool sorted =
+      qbins || (p.cfg.dtype == AMS_DTYPE_BF16 && a.gated && p.local > 0 && nq >= kSortMinQueries && !use_scan);
+  a.qbins = qbins ? 1 : 0;
+  if (qbins)
+    AMS_CUDA_TRY(ams::launch_query_order_j0(p, qj_src, nq, s));
+  else if (sorted)
+    AMS_CUDA_TRY(ams::launch_query_order(p, qj_src, nq, s));
   // the dense bf16 kernels start from zeroed per-query bounds (+ the K2 wave counter) and,
   // ungated, zeroed union slots: the prep kernel clears them (no memset node between it
   // and the dense kernel, which is then its programmatic dependent).  Slots: K2 indexes

@@ -233,8 +233,7 @@ __global__ void __launch_bounds__(kGfThreads)
 // the warp-per-32-queries kernel's per-tile overhead for one or two live lanes (C5 pool,
 // 1 query: 64 us there).  Eligible rows go to the query's bucket as in gate_scan_kernel
 // (bucket order is irrelevant: the score kernel orders by (score, index)).
-constexpr int kGfRowsMaxQ = 16;
-constexpr int kGfRowsThreads = 256;
+constexpr int kGfRowsThreads = 256;   // (kGfRowsMaxQ: ams_internal.cuh)
 
 template <int JP>
 __global__ void __launch_bounds__(kGfRowsThreads)
@@ -267,6 +266,239 @@ __global__ void __launch_bounds__(kGfRowsThreads)
           const uint32_t slot = atomicAdd(&cnt[qi], 1u);
           if (slot < (uint32_t)cap) cand[(int64_t)qi * cap + slot] = (int32_t)(j0 + u * stride);
         }
+      }
+    }
+  }
+  ptx::griddep_launch_dependents();
+}
+
+// ------------------------------------------------------------ mid-size batches (17..1024)
+// The queries are staged in kQBins linear joint-0 bins (query_order_j0_kernel); a pool
+// row can pass the canonical gate only for queries whose joint 0 is within gamma of its
+// own (the canonical partial sums only grow: RN(RN(q0 - r0)^2) > g2 fails the gate), so
+// gate_rows_binned_kernel visits, per row, only the queries of the bins overlapping
+// [r0 - gp, r0 + gp] (gp = sqrt(g2) rounded up, widened by 2^-20, plus one bin on each
+// side for the rounding of the bin arithmetic -- the argument of the pool-side joint-0
+// index) and runs the exact gate with an early exit once a partial sum exceeds g2.  Per
+// row that is ~nq * 2 gamma / span(joint 0) queries instead of nq, so the scan stays
+// bound by reading the joints (C5 pool, 256 queries: 309 us in the warp kernel, whose
+// ALU cost is per (row, query) pair).
+__device__ __forceinline__ int qbin(float v, float lo, float scale) {
+  const float f = (v - lo) * scale;
+  return (f >= 0.0f && f < (float)kQBins) ? (int)f : (f >= 0.0f ? kQBins - 1 : 0);
+}
+
+constexpr int kQOrderThreads = 256;
+
+__global__ void __launch_bounds__(kQOrderThreads)
+    query_order_j0_kernel(const float* __restrict__ jsrc, int32_t J, int32_t nq, int32_t* __restrict__ perm,
+                          int32_t* __restrict__ qbins) {
+  __shared__ uint32_t hist[kQBins];
+  __shared__ float red_lo[kQOrderThreads / 32], red_hi[kQOrderThreads / 32];
+  __shared__ uint32_t wsum[kQOrderThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  float l = CUDART_INF_F, h = -CUDART_INF_F;
+  for (int q = tid; q < nq; q += kQOrderThreads) {
+    const float v = jsrc[(int64_t)q * J];
+    if (v == v) {
+      l = fminf(l, v);
+      h = fmaxf(h, v);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    l = fminf(l, __shfl_xor_sync(0xffffffffu, l, o));
+    h = fmaxf(h, __shfl_xor_sync(0xffffffffu, h, o));
+  }
+  if (lane == 0) {
+    red_lo[w] = l;
+    red_hi[w] = h;
+  }
+  for (int b = tid; b < kQBins; b += kQOrderThreads) hist[b] = 0u;
+  __syncthreads();
+  l = red_lo[0];
+  h = red_hi[0];
+  for (int i = 1; i < kQOrderThreads / 32; ++i) {
+    l = fminf(l, red_lo[i]);
+    h = fmaxf(h, red_hi[i]);
+  }
+  const float span = h - l;
+  const float lo = l < CUDART_INF_F ? l : 0.0f;
+  const float scale = (span > 1e-30f && span < CUDART_INF_F) ? (float)kQBins / span : 0.0f;
+  for (int q = tid; q < nq; q += kQOrderThreads) atomicAdd(&hist[qbin(jsrc[(int64_t)q * J], lo, scale)], 1u);
+  __syncthreads();
+  // exclusive scan: thread t owns bins [4t, 4t + 4)
+  constexpr int per = kQBins / kQOrderThreads;
+  uint32_t v[per], run = 0;
+#pragma unroll
+  for (int i = 0; i < per; ++i) {
+    v[i] = hist[tid * per + i];
+    run += v[i];
+  }
+  uint32_t incl = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[w] = incl;
+  __syncthreads();
+  uint32_t base = 0;
+  for (int i = 0; i < w; ++i) base += wsum[i];
+  base += incl - run;
+#pragma unroll
+  for (int i = 0; i < per; ++i) {
+    qbins[tid * per + i] = (int32_t)base;
+    hist[tid * per + i] = base;
+    base += v[i];
+  }
+  if (tid == 0) {
+    qbins[kQBins] = nq;
+    qbins[kQBins + 1] = __float_as_int(lo);
+    qbins[kQBins + 2] = __float_as_int(scale);
+  }
+  __syncthreads();
+  for (int q = tid; q < nq; q += kQOrderThreads) {
+    const uint32_t pos = atomicAdd(&hist[qbin(jsrc[(int64_t)q * J], lo, scale)], 1u);
+    perm[pos] = q;   // order within a bin is irrelevant: a row visits whole bins
+  }
+}
+
+// Per warp, 32 consecutive rows per step (coalesced joint loads; the rows' joints go to
+// shared memory); each lane's row contributes the queries of its joint-0 window, and the
+// warp's (row, query) pairs are then dealt 32 at a time to the lanes (owner row by a
+// 5-step search over the lanes' prefix sums), so the gate arithmetic runs on full warps
+// instead of one divergent per-lane loop (ncu of that version: 26 % lane efficiency).
+template <int JP>
+__global__ void __launch_bounds__(kGfRowsThreads)
+    gate_rows_binned_kernel(const float* __restrict__ pool_joints, int64_t begin, int64_t L,
+                            const float* __restrict__ q_joints, int32_t nq, float g2, int32_t cap,
+                            uint32_t* __restrict__ cnt, int32_t* __restrict__ cand, const int32_t* __restrict__ qbins) {
+  constexpr int QS = JP + 1;   // padded strides (conflict-free for distinct rows / queries)
+  extern __shared__ __align__(16) float qs[];                        // [nq][QS] staged (binned) order
+  int32_t* off = reinterpret_cast<int32_t*>(qs + (size_t)nq * QS);   // [kQBins + 1]
+  __shared__ float rows_s[kGfRowsThreads / 32][32 * QS];
+  __shared__ int32_t pre_s[kGfRowsThreads / 32][32], qa_s[kGfRowsThreads / 32][32];
+  ptx::griddep_wait();   // a programmatic dependent of the query prep
+  for (int i = threadIdx.x; i < nq * JP; i += kGfRowsThreads) qs[(i / JP) * QS + i % JP] = q_joints[i];
+  for (int i = threadIdx.x; i <= kQBins; i += kGfRowsThreads) off[i] = qbins[i];
+  const float lo = __int_as_float(qbins[kQBins + 1]), scale = __int_as_float(qbins[kQBins + 2]);
+  const float gp = __fmul_ru(__fsqrt_ru(g2), 1.00000095367431640625f);   // (1 + 2^-20)
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  float* rs = rows_s[wib];
+  int32_t* pre = pre_s[wib];
+  int32_t* qa_w = qa_s[wib];
+  const int64_t nwarps = (int64_t)gridDim.x * (kGfRowsThreads / 32);
+  for (int64_t base = begin + ((int64_t)blockIdx.x * (kGfRowsThreads / 32) + wib) * 32; base < L;
+       base += nwarps * 32) {
+    const int64_t j = base + lane;
+    int c = 0, qa = 0;
+    if (j < L) {
+#pragma unroll
+      for (int t = 0; t < JP; ++t) rs[lane * QS + t] = __ldcs(pool_joints + joint_offset(j, t, JP));
+      const float r0 = rs[lane * QS];
+      const int ba = max(0, qbin(__fsub_rd(r0, gp), lo, scale) - 1);
+      const int bb = min(kQBins - 1, qbin(__fadd_ru(r0, gp), lo, scale) + 1);
+      qa = off[ba];
+      c = off[bb + 1] - qa;
+    }
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    pre[lane] = incl - c;
+    qa_w[lane] = qa;
+    __syncwarp();
+    for (int p = lane; p < total; p += 32) {
+      int r = 0;   // the last lane whose pair range starts at or before p
+#pragma unroll
+      for (int st = 16; st > 0; st >>= 1)
+        if (pre[r + st] <= p) r += st;
+      const int qi = qa_w[r] + (p - pre[r]);
+      const float* rj = rs + r * QS;
+      const float* qj = qs + qi * QS;
+      // the canonical gate (joint order, fsub then fmaf); partial sums only grow, so
+      // most pairs stop after joint 1
+      float df = __fsub_rn(qj[0], rj[0]);
+      float ds = __fmaf_rn(df, df, 0.0f);
+      if (JP > 1) {
+        df = __fsub_rn(qj[1], rj[1]);
+        ds = __fmaf_rn(df, df, ds);
+      }
+      if (!(ds <= g2)) continue;
+#pragma unroll
+      for (int t = 2; t < JP; ++t) {
+        df = __fsub_rn(qj[t], rj[t]);
+        ds = __fmaf_rn(df, df, ds);
+      }
+      if (ds <= g2) {
+        const uint32_t slot = atomicAdd(&cnt[qi], 1u);
+        if (slot < (uint32_t)cap) cand[(int64_t)qi * cap + slot] = (int32_t)(base + r);
+      }
+    }
+    __syncwarp();
+  }
+  ptx::griddep_launch_dependents();
+}
+
+// Rows in joint-0 order (the pool-side snapshot index, positions [0, snap_L)): the 32 rows
+// of a warp span a tiny joint-0 interval, so their windows nearly coincide and the warp
+// walks the union window with a warp-uniform loop -- every lane tests its own row against
+// the same query (a broadcast shared-memory read) -- instead of dealing pairs.
+template <int JP>
+__global__ void __launch_bounds__(kGfRowsThreads)
+    gate_rows_snap_kernel(const float* __restrict__ snap_j, const int32_t* __restrict__ snap_id, int64_t L,
+                          const float* __restrict__ q_joints, int32_t nq, float g2, int32_t cap,
+                          uint32_t* __restrict__ cnt, int32_t* __restrict__ cand, const int32_t* __restrict__ qbins) {
+  extern __shared__ __align__(16) float qs[];                        // [nq][JP] staged (binned) order
+  int32_t* off = reinterpret_cast<int32_t*>(qs + (size_t)nq * (JP + 1));   // [kQBins + 1]
+  ptx::griddep_wait();   // a programmatic dependent of the query prep
+  for (int i = threadIdx.x; i < nq * JP; i += kGfRowsThreads) qs[i] = q_joints[i];
+  for (int i = threadIdx.x; i <= kQBins; i += kGfRowsThreads) off[i] = qbins[i];
+  const float lo = __int_as_float(qbins[kQBins + 1]), scale = __int_as_float(qbins[kQBins + 2]);
+  const float gp = __fmul_ru(__fsqrt_ru(g2), 1.00000095367431640625f);   // (1 + 2^-20)
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t nwarps = (int64_t)gridDim.x * (kGfRowsThreads / 32);
+  for (int64_t base = ((int64_t)blockIdx.x * (kGfRowsThreads / 32) + wib) * 32; base < L; base += nwarps * 32) {
+    const int64_t pos = base + lane;
+    const bool valid = pos < L;
+    float pj[JP];
+#pragma unroll
+    for (int t = 0; t < JP; ++t) pj[t] = valid ? __ldcs(snap_j + joint_offset(pos, t, JP)) : 0.0f;
+    // the union of the lanes' windows (NaN joints pass no gate: fminf / fmaxf drop them)
+    float wmin = valid ? pj[0] : CUDART_INF_F, wmax = valid ? pj[0] : -CUDART_INF_F;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      wmin = fminf(wmin, __shfl_xor_sync(0xffffffffu, wmin, o));
+      wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
+    }
+    if (!(wmin <= wmax)) continue;
+    const int ba = max(0, qbin(__fsub_rd(wmin, gp), lo, scale) - 1);
+    const int bb = min(kQBins - 1, qbin(__fadd_ru(wmax, gp), lo, scale) + 1);
+    const int qa = off[ba], qb = off[bb + 1];
+    for (int qi = qa; qi < qb; ++qi) {
+      const float* qj = qs + qi * JP;
+      // the canonical gate (joint order, fsub then fmaf); partial sums only grow
+      float df = __fsub_rn(qj[0], pj[0]);
+      float ds = __fmaf_rn(df, df, 0.0f);
+      if (JP > 1) {
+        df = __fsub_rn(qj[1], pj[1]);
+        ds = __fmaf_rn(df, df, ds);
+      }
+      if (!(ds <= g2 && valid)) continue;
+#pragma unroll
+      for (int t = 2; t < JP; ++t) {
+        df = __fsub_rn(qj[t], pj[t]);
+        ds = __fmaf_rn(df, df, ds);
+      }
+      if (ds <= g2) {
+        const uint32_t slot = atomicAdd(&cnt[qi], 1u);
+        if (slot < (uint32_t)cap) cand[(int64_t)qi * cap + slot] = snap_id[pos];
       }
     }
   }
@@ -567,7 +799,7 @@ cudaError_t launch_gf_jp(Pool& p, const MatchArgs& a, int32_t cap, float* out_s,
   if (!a.zeroed && (e = cudaMemsetAsync(p.gf_cnt, 0, (size_t)a.nq * sizeof(uint32_t), s)) != cudaSuccess) return e;
   // Sorted batches on large pools scan the joint-0 index: each block of queries visits
   // only the rows within gamma of its joint-0 interval (plus the unsorted tail).
-  const bool snap = sorted && p.local >= kSnapMinRows;
+  const bool snap = sorted && !a.qbins && p.local >= kSnapMinRows;
   if (snap && (e = snap_refresh(p, s)) != cudaSuccess) return e;
   const int64_t plain_begin = snap ? p.snap_L : 0;
   if (snap) {
@@ -575,7 +807,48 @@ cudaError_t launch_gf_jp(Pool& p, const MatchArgs& a, int32_t cap, float* out_s,
                       reinterpret_cast<const float*>(p.snap_aux + kSnapBins + 2)};
     if ((e = launch_gate_scan_q<JP>(p, a, cap, rows, n_pt, 1, s)) != cudaSuccess) return e;
   }
-  if (p.local > plain_begin && plain_begin == 0 && a.nq <= kGfRowsMaxQ) {
+  if (a.qbins && p.local > 0) {
+    // 17..1024 gated queries in joint-0 bins: pools of >= 64 K rows scan their joint-0
+    // snapshot with warp-uniform windows, the rows appended since (or a small pool) with
+    // the pair-dealing kernel
+    const bool use_snap = p.local >= kSnapMinRows;
+    if (use_snap && (e = snap_refresh(p, s)) != cudaSuccess) return e;
+    const int64_t tail = use_snap ? p.snap_L : 0;
+    const size_t smem = (size_t)a.nq * (JP + 1) * 4 + (size_t)(kQBins + 1) * 4;
+    static size_t opted[2] = {0, 0};   // dynamic shared memory above 48 KB needs the opt-in (once)
+    if (smem > opted[0]) {
+      if ((e = cudaFuncSetAttribute(gate_rows_binned_kernel<JP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem)) != cudaSuccess ||
+          (e = cudaFuncSetAttribute(gate_rows_snap_kernel<JP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem)) != cudaSuccess)
+        return e;
+      opted[0] = smem;
+    }
+    cudaLaunchAttribute attr[1];
+    if (use_snap) {
+      const unsigned grid = (unsigned)std::max<int64_t>(
+          1, std::min<int64_t>((tail + kGfRowsThreads - 1) / kGfRowsThreads, 8 * (int64_t)p.num_sms));
+      cudaLaunchConfig_t cfg = gf_config(dim3(grid), kGfRowsThreads, s, attr);
+      cfg.dynamicSmemBytes = smem;
+      ++p.launches;
+      if ((e = cudaLaunchKernelEx(&cfg, gate_rows_snap_kernel<JP>, static_cast<const float*>(p.snap_j),
+                                  static_cast<const int32_t*>(p.snap_id), tail, static_cast<const float*>(p.q_joints),
+                                  a.nq, a.g2, cap, p.gf_cnt, p.gf_cand, static_cast<const int32_t*>(p.gf_qbins))) !=
+          cudaSuccess)
+        return e;
+    }
+    if (p.local > tail) {
+      const unsigned grid = (unsigned)std::max<int64_t>(
+          1, std::min<int64_t>((p.local - tail + kGfRowsThreads - 1) / kGfRowsThreads, 8 * (int64_t)p.num_sms));
+      cudaLaunchConfig_t cfg = gf_config(dim3(grid), kGfRowsThreads, s, attr);
+      cfg.dynamicSmemBytes = smem;
+      ++p.launches;
+      if ((e = cudaLaunchKernelEx(&cfg, gate_rows_binned_kernel<JP>, static_cast<const float*>(p.joints), tail,
+                                  p.local, static_cast<const float*>(p.q_joints), a.nq, a.g2, cap, p.gf_cnt,
+                                  p.gf_cand, static_cast<const int32_t*>(p.gf_qbins))) != cudaSuccess)
+        return e;
+    }
+  } else if (p.local > plain_begin && plain_begin == 0 && a.nq <= kGfRowsMaxQ) {
     // tiny batch over the whole pool: the row-parallel kernel (~2 waves of 8 blocks per SM)
     const unsigned grid = (unsigned)std::max<int64_t>(
         1, std::min<int64_t>((p.local + kGfRowsThreads - 1) / kGfRowsThreads, 16 * (int64_t)p.num_sms));
@@ -660,6 +933,13 @@ cudaError_t launch_gate_estimate(Pool& p, const float* qj_raw, int32_t nq, float
   if (e != cudaSuccess || n_rows == 0) return e;
   gate_estimate_kernel<<<(n_rows + 255) / 256, 256, 0, s>>>(p.joints, p.JP, L, row_step, n_rows, qj_raw,
                                                             p.cfg.joint_dim, q_step, n_q, g2, out);
+  ++p.launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_query_order_j0(Pool& p, const float* qj_src, int32_t nq, cudaStream_t s) {
+  if (nq > kGfBinnedMaxQ) return cudaErrorInvalidValue;
+  query_order_j0_kernel<<<1, kQOrderThreads, 0, s>>>(qj_src, p.cfg.joint_dim, nq, p.q_perm, p.gf_qbins);
   ++p.launches;
   return cudaGetLastError();
 }

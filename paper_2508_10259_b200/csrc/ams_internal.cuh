@@ -18,6 +18,9 @@ constexpr int kRowAlign = 256;   // shard storage is padded to a multiple of thi
 constexpr int kEpiHalves = 2;    // epilogue warps per TMEM lane group (column halves)
 constexpr int kSimtThreads = 128;
 constexpr int kSnapBins = 65536;  // joint-0 bins of the gate-first index
+constexpr int kQBins = 1024;      // joint-0 bins of a mid-size gate-first batch (query side)
+constexpr int kGfRowsMaxQ = 16;   // gate-first batches up to this size: row kernel, unsorted
+constexpr int kGfBinnedMaxQ = 1024;   // ... up to this size (gated): row kernel over joint-0 query bins
 
 // --------------------------------------------------------------------------- shard map
 // Block-cyclic: global ordinal o -> block b = o / B, owner b % G, local (b / G) * B + o % B.
@@ -131,6 +134,7 @@ struct Pool {
   int32_t gf_cap = 0;
   uint32_t* gf_cnt = nullptr;  // [q_pad]
   int32_t* gf_cand = nullptr;  // [q_pad, gf_cap] local rows
+  int32_t* gf_qbins = nullptr; // [kQBins + 1] staged-query offsets of the joint-0 query bins, then {lo, scale}
   // gate-first joint-0 index (built lazily by the first sorted gate-first call): local rows
   // [0, snap_L) bucket-sorted by joint 0 into kSnapBins linear bins; rows appended since
   // are scanned in plain order until the next rebuild
@@ -193,6 +197,7 @@ struct MatchArgs {
   float threshold;
   int32_t slots;      // the tcgen05 kernel filled p.slots (union bound) for the merge
   int32_t zeroed;     // query prep already zeroed this call's counters (p.bound / p.slots or p.gf_cnt)
+  int32_t qbins;      // gate-first: queries staged in joint-0 bin order (launch_query_order_j0)
 };
 
 cudaError_t launch_append(Pool& p, const void* emb_src, const float* joints_src, int64_t n_src,
@@ -243,6 +248,10 @@ cudaError_t launch_merge_lists(const MatchArgs& a, int32_t G, int32_t kin, const
 // sorted: queries were staged through p.q_perm (outputs land at the caller's query index)
 cudaError_t launch_gate_first(Pool& p, const MatchArgs& a, float* out_s, int64_t* out_i, uint8_t* out_hit,
                               bool sorted, cudaStream_t s);
+// p.q_perm <- the queries in kQBins linear joint-0 bins (one block; nq <= kGfBinnedMaxQ),
+// p.gf_qbins <- the bins' staged offsets and {lo, scale}: the gate-first row kernel then
+// visits, per pool row, only the queries of the bins within gamma of its joint 0
+cudaError_t launch_query_order_j0(Pool& p, const float* qj_src, int32_t nq, cudaStream_t s);
 cudaError_t launch_exchange_push(int KT, const float* ps, const int32_t* pi, int32_t nq, int32_t P, int32_t k,
                                  const PeerTable& pt, unsigned long long epoch, unsigned int* done, int32_t world_ids,
                                  int64_t B, cudaStream_t s);

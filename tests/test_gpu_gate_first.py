@@ -71,6 +71,30 @@ def test_gate_first_batch_shapes(ams, nq, gamma):
     check_bf16(*g, orc, cfg.theta)
 
 
+@pytest.mark.parametrize("nq,gamma", [(17, 0.3), (40, 0.8), (300, 0.3), (1024, 0.2)])
+def test_gate_first_binned_snapshot_and_tail(ams, nq, gamma):
+    """17..1024 gated queries are staged in joint-0 bins; on a pool of >= 64 K rows the
+    first call builds the joint-0 row snapshot and scans it with warp-uniform windows, and
+    rows appended afterwards (below the rebuild threshold) are scanned by the pair-dealing
+    kernel.  Both calls against the oracle, the second after a 5,000-row append."""
+    cfg = ams_gen.small_variant("c2", 75000, nq)
+    w = ams_gen.generate_host(cfg)
+    M0 = 70000
+    with ams.Pool(cfg.d, cfg.J, cfg.M, nq, cfg.k) as pool:
+        pool.append(T(w.emb[:M0]), T(w.joints[:M0]))
+        out = [t.cpu().numpy() for t in pool.match(T(w.q_emb), T(w.q_joints), cfg.k, cfg.theta, gamma,
+                                                    gate_first=True)]
+        torch.cuda.synchronize()
+        check_bf16(*out, oracle.match(w.emb[:M0], w.joints[:M0], w.q_emb, w.q_joints, cfg.k, cfg.theta, gamma),
+                   cfg.theta)
+        pool.append(T(w.emb[M0:]), T(w.joints[M0:]))
+        out = [t.cpu().numpy() for t in pool.match(T(w.q_emb), T(w.q_joints), cfg.k, cfg.theta, gamma,
+                                                    gate_first=True)]
+        torch.cuda.synchronize()
+        assert ams.ams_pool_last_plan(pool.handle)["kernel_id"] == 3
+    check_bf16(*out, oracle.match(w.emb, w.joints, w.q_emb, w.q_joints, cfg.k, cfg.theta, gamma), cfg.theta)
+
+
 def test_gate_first_ties_and_padding(ams):
     rng = np.random.Generator(np.random.PCG64(5))
     d, J, M = 128, 7, 3000
