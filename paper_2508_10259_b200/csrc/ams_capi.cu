@@ -638,9 +638,12 @@ static ams_status_t match_impl(ams_pool_t pool, const void* q_emb, const float* 
                         ams::scan_stages(p, nq, a.KT) > 0 &&
                         (int64_t)nq * ams::scan_lists_per_split(nq, a.KT, a.gated != 0) * a.KT <= p.part_cap;   // >= 1 split fits
   // Gated gate-first batches of 17..1024 queries are staged in joint-0 bins instead (the
-  // row kernel looks up, per pool row, the queries within gamma of its joint 0).
-  const bool qbins = gate_first && p.cfg.dtype == AMS_DTYPE_BF16 && a.gated && p.local > 0 &&
-                     nq > ams::kGfRowsMaxQ && nq <= ams::kGfBinnedMaxQ;
+  // row kernels look up, per pool row, the queries within gamma of its joint 0).
+  // (Up to 1024 queries, whose joints fit in shared memory: at 1024 the two designs are
+  // even on C3's pool, and at 2048 the block kernel over the 2-D query order wins, 0.27 vs
+  // 0.50 ms, so larger batches keep it.)
+  const bool qbins = gate_first && p.cfg.dtype == AMS_DTYPE_BF16 && a.gated && p.local > 0 && nq > ams::kGfRowsMaxQ &&
+                     nq <= ams::kGfBinnedMaxQ;
   const bool sorted =
       qbins || (p.cfg.dtype == AMS_DTYPE_BF16 && a.gated && p.local > 0 && nq >= kSortMinQueries && !use_scan);
   a.qbins = qbins ? 1 : 0;

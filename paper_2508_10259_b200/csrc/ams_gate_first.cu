@@ -454,7 +454,7 @@ __global__ void __launch_bounds__(kGfRowsThreads)
     gate_rows_snap_kernel(const float* __restrict__ snap_j, const int32_t* __restrict__ snap_id, int64_t L,
                           const float* __restrict__ q_joints, int32_t nq, float g2, int32_t cap,
                           uint32_t* __restrict__ cnt, int32_t* __restrict__ cand, const int32_t* __restrict__ qbins) {
-  extern __shared__ __align__(16) float qs[];                        // [nq][JP] staged (binned) order
+  extern __shared__ __align__(16) float qs[];                              // [nq][JP] staged (binned) order
   int32_t* off = reinterpret_cast<int32_t*>(qs + (size_t)nq * (JP + 1));   // [kQBins + 1]
   ptx::griddep_wait();   // a programmatic dependent of the query prep
   for (int i = threadIdx.x; i < nq * JP; i += kGfRowsThreads) qs[i] = q_joints[i];
@@ -815,14 +815,14 @@ cudaError_t launch_gf_jp(Pool& p, const MatchArgs& a, int32_t cap, float* out_s,
     if (use_snap && (e = snap_refresh(p, s)) != cudaSuccess) return e;
     const int64_t tail = use_snap ? p.snap_L : 0;
     const size_t smem = (size_t)a.nq * (JP + 1) * 4 + (size_t)(kQBins + 1) * 4;
-    static size_t opted[2] = {0, 0};   // dynamic shared memory above 48 KB needs the opt-in (once)
-    if (smem > opted[0]) {
+    static size_t opted = 0;   // dynamic shared memory above 48 KB needs the opt-in (once)
+    if (smem > opted) {
       if ((e = cudaFuncSetAttribute(gate_rows_binned_kernel<JP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem)) != cudaSuccess ||
           (e = cudaFuncSetAttribute(gate_rows_snap_kernel<JP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem)) != cudaSuccess)
         return e;
-      opted[0] = smem;
+      opted = smem;
     }
     cudaLaunchAttribute attr[1];
     if (use_snap) {
@@ -938,7 +938,6 @@ cudaError_t launch_gate_estimate(Pool& p, const float* qj_raw, int32_t nq, float
 }
 
 cudaError_t launch_query_order_j0(Pool& p, const float* qj_src, int32_t nq, cudaStream_t s) {
-  if (nq > kGfBinnedMaxQ) return cudaErrorInvalidValue;
   query_order_j0_kernel<<<1, kQOrderThreads, 0, s>>>(qj_src, p.cfg.joint_dim, nq, p.q_perm, p.gf_qbins);
   ++p.launches;
   return cudaGetLastError();

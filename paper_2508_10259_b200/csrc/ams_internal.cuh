@@ -20,7 +20,8 @@ constexpr int kSimtThreads = 128;
 constexpr int kSnapBins = 65536;  // joint-0 bins of the gate-first index
 constexpr int kQBins = 1024;      // joint-0 bins of a mid-size gate-first batch (query side)
 constexpr int kGfRowsMaxQ = 16;   // gate-first batches up to this size: row kernel, unsorted
-constexpr int kGfBinnedMaxQ = 1024;   // ... up to this size (gated): row kernel over joint-0 query bins
+constexpr int kGfBinnedMaxQ = 1024;   // gated batches above kGfRowsMaxQ: joint-0 query bins; up to this
+                                      // size their joints are staged in shared memory
 
 // --------------------------------------------------------------------------- shard map
 // Block-cyclic: global ordinal o -> block b = o / B, owner b % G, local (b / G) * B + o % B.
@@ -248,7 +249,7 @@ cudaError_t launch_merge_lists(const MatchArgs& a, int32_t G, int32_t kin, const
 // sorted: queries were staged through p.q_perm (outputs land at the caller's query index)
 cudaError_t launch_gate_first(Pool& p, const MatchArgs& a, float* out_s, int64_t* out_i, uint8_t* out_hit,
                               bool sorted, cudaStream_t s);
-// p.q_perm <- the queries in kQBins linear joint-0 bins (one block; nq <= kGfBinnedMaxQ),
+// p.q_perm <- the queries in kQBins linear joint-0 bins (one block),
 // p.gf_qbins <- the bins' staged offsets and {lo, scale}: the gate-first row kernel then
 // visits, per pool row, only the queries of the bins within gamma of its joint 0
 cudaError_t launch_query_order_j0(Pool& p, const float* qj_src, int32_t nq, cudaStream_t s);

@@ -71,12 +71,14 @@ def test_gate_first_batch_shapes(ams, nq, gamma):
     check_bf16(*g, orc, cfg.theta)
 
 
-@pytest.mark.parametrize("nq,gamma", [(17, 0.3), (40, 0.8), (300, 0.3), (1024, 0.2)])
+@pytest.mark.parametrize("nq,gamma", [(17, 0.3), (40, 0.8), (300, 0.3), (1024, 0.2), (1025, 0.3)])
 def test_gate_first_binned_snapshot_and_tail(ams, nq, gamma):
-    """17..1024 gated queries are staged in joint-0 bins; on a pool of >= 64 K rows the
-    first call builds the joint-0 row snapshot and scans it with warp-uniform windows, and
-    rows appended afterwards (below the rebuild threshold) are scanned by the pair-dealing
-    kernel.  Both calls against the oracle, the second after a 5,000-row append."""
+    """Gated batches of 17..1024 queries are staged in joint-0 bins; on a pool of >= 64 K
+    rows the first call builds the joint-0 row snapshot and scans it with warp-uniform
+    windows, and rows appended afterwards (below the rebuild threshold) are scanned by the
+    pair-dealing kernel.  1025 queries: the 2-D query order and the block kernel over the
+    snapshot and the appended tail.  Both calls against the oracle, the second after a
+    5,000-row append."""
     cfg = ams_gen.small_variant("c2", 75000, nq)
     w = ams_gen.generate_host(cfg)
     M0 = 70000
@@ -93,6 +95,16 @@ def test_gate_first_binned_snapshot_and_tail(ams, nq, gamma):
         torch.cuda.synchronize()
         assert ams.ams_pool_last_plan(pool.handle)["kernel_id"] == 3
     check_bf16(*out, oracle.match(w.emb, w.joints, w.q_emb, w.q_joints, cfg.k, cfg.theta, gamma), cfg.theta)
+
+
+@pytest.mark.parametrize("M,nq", [(3001, 100), (20011, 1024)])
+def test_gate_first_binned_small_pool(ams, M, nq):
+    """Pools below the snapshot threshold: the binned batch goes to the pair-dealing kernel
+    over the whole pool."""
+    cfg = ams_gen.small_variant("c2", M, nq)
+    w = ams_gen.generate_host(cfg)
+    orc = oracle.match(w.emb, w.joints, w.q_emb, w.q_joints, cfg.k, cfg.theta, 0.5)
+    check_bf16(*run(ams, w, cfg.k, cfg.theta, 0.5, True), orc, cfg.theta)
 
 
 def test_gate_first_ties_and_padding(ams):
