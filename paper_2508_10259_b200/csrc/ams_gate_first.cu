@@ -8,11 +8,17 @@
 // the gate for every (query, row) pair first -- reading only the pool's joints (4*JP
 // bytes per row instead of 2d) -- and computes dot products for eligible pairs only.
 //
-//   K1 gate_scan_kernel   block = 256 queries (thread = query) x a contiguous row split;
-//                         pool joint tiles ([JP][256] fp32, tile-transposed) staged in
-//                         shared memory; packed f32x2 4-joint filter per 8 rows, one warp
-//                         vote, exact canonical gate for fired rows; eligible rows are
-//                         appended to the query's candidate bucket (atomic slot).
+//   K1 the gate, one of (by batch; every one appends eligible rows to the query's
+//      candidate bucket through an atomic slot, and the bucket order is irrelevant):
+//      gate_rows_kernel        <= 16 queries: thread per row, exact gate vs every query;
+//      gate_rows_snap_kernel   17..1024 gated queries in joint-0 bins, rows in the
+//                              pool's joint-0 snapshot order: warp-uniform query windows;
+//      gate_rows_binned_kernel the same for rows outside the snapshot: (row, query)
+//                              pairs dealt to lanes;
+//      gate_scan_kernel        otherwise: block = QT queries x a row split; pool joint
+//                              tiles ([JP][256] fp32, tile-transposed) staged in shared
+//                              memory; packed f32x2 4-joint filter per 8 rows, one warp
+//                              vote, exact canonical gate for fired rows.
 //   K2 score_kernel       warp per query: bf16 dot product per candidate (lanes split d,
 //                         fixed butterfly order), s = (acc*inv_q)*inv_e, register top-k;
 //                         a bucket that overflowed is recomputed exactly by the warp
