@@ -14,3 +14,8 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:matc
    -o gpurun_out/ncu_r02_c3_200q_k8_pair -f python scripts/one_call.py c3 --nq 200 --k 8 > gpurun_out/ncu_pair.log 2>&1; echo "pair rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:phase1_tc_kernel -c 1 \
    -o gpurun_out/ncu_r02_hash_phase1_tc -f python scripts/hash_speed.py > gpurun_out/ncu_hash2.log 2>&1; echo "hash rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:gate_rows_snap --launch-skip 3 -c 1 \
+   -o gpurun_out/ncu_r02_c5_64q_gate_rows_snap -f python scripts/one_call.py c5 --nq 64 --gate-first > gpurun_out/ncu_gsnap.log 2>&1; echo "gsnap rc=$?"
+timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29533 \
+    bench.py --gpus 1 --steps 10 --warmup 3 --force-collective --no-cpu-baseline > gpurun_out/r02_dry_collective2.json 2> gpurun_out/r02_dry_collective2.err
+echo "dry rc=$?"
