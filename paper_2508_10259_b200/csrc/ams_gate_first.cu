@@ -766,11 +766,11 @@ inline cudaLaunchConfig_t gf_config(dim3 grid, int threads, cudaStream_t s, cuda
 
 // One gate-scan launch over `tiles` joint tiles with QT queries per block: ~2 full waves
 // of resident blocks, but >= 8 tiles per block so per-block setup stays amortised.
-// (Resident blocks per SM depend only on the kernel and the B200's limits: cached.)
+// (Resident blocks per SM depend only on the kernel and the device: cached on the pool.)
 template <int JP, int QT>
 cudaError_t launch_gate_scan(Pool& p, const MatchArgs& a, int32_t cap, const GfRows& rows, int64_t tiles,
                              int32_t sorted, cudaStream_t s) {
-  static int occ = 0;
+  int& occ = p.gf_occ[JP == 4 ? 0 : JP == 8 ? 1 : 2][QT == 32 ? 0 : QT == 64 ? 1 : QT == 128 ? 2 : 3];
   if (occ == 0) {
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gate_scan_kernel<JP, QT>, kGfThreads, 0);
     if (e != cudaSuccess) return e;
@@ -821,7 +821,7 @@ cudaError_t launch_gf_jp(Pool& p, const MatchArgs& a, int32_t cap, float* out_s,
     if (use_snap && (e = snap_refresh(p, s)) != cudaSuccess) return e;
     const int64_t tail = use_snap ? p.snap_L : 0;
     const size_t smem = (size_t)a.nq * (JP + 1) * 4 + (size_t)(kQBins + 1) * 4;
-    static size_t opted = 0;   // dynamic shared memory above 48 KB needs the opt-in (once)
+    size_t& opted = p.gf_rows_smem_opt;   // dynamic shared memory above 48 KB needs the opt-in (once per pool)
     if (smem > opted) {
       if ((e = cudaFuncSetAttribute(gate_rows_binned_kernel<JP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem)) != cudaSuccess ||

@@ -136,6 +136,9 @@ struct Pool {
   uint32_t* gf_cnt = nullptr;  // [q_pad]
   int32_t* gf_cand = nullptr;  // [q_pad, gf_cap] local rows
   int32_t* gf_qbins = nullptr; // [kQBins + 1] staged-query offsets of the joint-0 query bins, then {lo, scale}
+  // per-device launch facts of the gate-first kernels, cached on the pool (one device)
+  size_t gf_rows_smem_opt = 0;  // dynamic shared memory opted in for the binned row kernels
+  int gf_occ[3][4] = {};        // resident gate_scan blocks per SM, [JP 4/8/16][QT 32/64/128/256]
   // gate-first joint-0 index (built lazily by the first sorted gate-first call): local rows
   // [0, snap_L) bucket-sorted by joint 0 into kSnapBins linear bins; rows appended since
   // are scanned in plain order until the next rebuild
