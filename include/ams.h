@@ -28,7 +28,11 @@
  *   - Work is enqueued on the caller's stream `stream` (a cudaStream_t passed as void*;
  *     NULL = legacy default stream); calls return after enqueue.  Inputs must stay
  *     valid until the stream reaches that point.  An append is visible to every later
- *     match on the same stream.
+ *     match on the same stream.  Inside a call, the kernels after the first are launched
+ *     as programmatic dependents of their predecessor (they start early and wait on the
+ *     device for its results); the call's first kernel is an ordinary launch, so it
+ *     waits for all earlier work on `stream`, and so does the caller's next ordinary
+ *     launch for the whole call.
  *   - A pool is NOT thread-safe; callers serialise calls on one pool ("a
  *     single pool serializes writers").  Calls on one pool share its device workspace
  *     (staging, partial lists), so they must also be ordered on the device: issue them on

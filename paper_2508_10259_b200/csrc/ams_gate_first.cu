@@ -753,15 +753,7 @@ cudaError_t snap_refresh(Pool& p, cudaStream_t s) {
 // gate-first kernels are programmatic dependents of the kernel before them (query prep,
 // then the gate scan): each starts with griddep_wait()
 inline cudaLaunchConfig_t gf_config(dim3 grid, int threads, cudaStream_t s, cudaLaunchAttribute* attr) {
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = grid;
-  cfg.blockDim = dim3(threads);
-  cfg.stream = s;
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cfg;
+  return pdl_config(grid, dim3(threads), 0, s, attr);
 }
 
 // One gate-scan launch over `tiles` joint tiles with QT queries per block: ~2 full waves

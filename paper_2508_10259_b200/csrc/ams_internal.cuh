@@ -194,6 +194,23 @@ struct Pool {
 
 // --------------------------------------------------------------------------- launchers
 // All return cudaError_t of the launch; `launches` is incremented per kernel launched.
+// Launch configuration of a programmatic dependent launch: the kernel may start while
+// the previous kernel on `s` is still running and must call ptx::griddep_wait() before it
+// reads that kernel's results (ams.h: "programmatic dependents").  attr: caller storage.
+inline cudaLaunchConfig_t pdl_config(dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                                     cudaLaunchAttribute* attr) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cfg;
+}
+
 struct MatchArgs {
   int32_t nq, k, KT;
   float g2;           // fp32(gate_radius^2); +inf disables the gate

@@ -816,19 +816,6 @@ cudaError_t launch_query_order(Pool& p, const float* qj_src, int32_t nq, cudaStr
 }
 
 // fp32 kernels: programmatic dependents of the query prep (launch overlaps its tail)
-inline cudaLaunchConfig_t pdl_config(dim3 grid, dim3 block, size_t smem, cudaStream_t s, cudaLaunchAttribute* attr) {
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cfg;
-}
-
 cudaError_t launch_match_simt(Pool& p, const MatchArgs& a, int32_t S, cudaStream_t s) {
   const int32_t P = S * kSimtThreads;
   const size_t smem = ((size_t)((p.cfg.dim + 3) & ~3) + (size_t)(kSimtThreads / 32) * kSimtChunk) * sizeof(float);
@@ -894,20 +881,9 @@ cudaError_t launch_merge_partials(Pool& p, const MatchArgs& a, int32_t P, float*
   // SMs idle); KT = 64 keeps the warp kernel (64 KB of staging per block)
   const bool per_block = a.nq < 8 * p.num_sms && P >= 64 && a.KT <= 32;
   // a programmatic dependent of the match kernel: its launch overlaps that kernel's tail
-  cudaLaunchConfig_t cfg{};
-  cfg.stream = s;
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  if (per_block) {
-    cfg.gridDim = dim3((unsigned)a.nq);
-    cfg.blockDim = dim3(kMergeBlockThreads);
-  } else {
-    cfg.gridDim = dim3(g);
-    cfg.blockDim = dim3(wpb * 32);
-  }
+  const cudaLaunchConfig_t cfg = per_block ? pdl_config(dim3((unsigned)a.nq), dim3(kMergeBlockThreads), 0, s, attr)
+                                           : pdl_config(dim3(g), dim3(wpb * 32), 0, s, attr);
   cudaError_t e = cudaSuccess;
 #define AMS_MERGE(KT_)                                                                                      \
   e = per_block ? cudaLaunchKernelEx(&cfg, merge_partials_block_kernel<KT_ <= 32 ? KT_ : 32>, p.part_s, p.part_i, \
