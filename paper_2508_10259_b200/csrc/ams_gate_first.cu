@@ -470,12 +470,22 @@ __global__ void __launch_bounds__(kGfRowsThreads)
   __syncthreads();
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t nwarps = (int64_t)gridDim.x * (kGfRowsThreads / 32);
-  for (int64_t base = ((int64_t)blockIdx.x * (kGfRowsThreads / 32) + wib) * 32; base < L; base += nwarps * 32) {
+  // the next group's joints are loaded before the current group's windows are walked
+  // (software pipelining: ncu showed the warps waiting on these loads)
+  const int64_t first = ((int64_t)blockIdx.x * (kGfRowsThreads / 32) + wib) * 32;
+  float pj_next[JP];
+#pragma unroll
+  for (int t = 0; t < JP; ++t)
+    pj_next[t] = first + lane < L ? __ldcs(snap_j + joint_offset(first + lane, t, JP)) : 0.0f;
+  for (int64_t base = first; base < L; base += nwarps * 32) {
     const int64_t pos = base + lane;
     const bool valid = pos < L;
     float pj[JP];
 #pragma unroll
-    for (int t = 0; t < JP; ++t) pj[t] = valid ? __ldcs(snap_j + joint_offset(pos, t, JP)) : 0.0f;
+    for (int t = 0; t < JP; ++t) pj[t] = pj_next[t];
+    const int64_t npos = pos + nwarps * 32;
+#pragma unroll
+    for (int t = 0; t < JP; ++t) pj_next[t] = npos < L ? __ldcs(snap_j + joint_offset(npos, t, JP)) : 0.0f;
     // the union of the lanes' windows (NaN joints pass no gate: fminf / fmaxf drop them)
     float wmin = valid ? pj[0] : CUDART_INF_F, wmax = valid ? pj[0] : -CUDART_INF_F;
 #pragma unroll
