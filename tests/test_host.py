@@ -157,3 +157,21 @@ def test_library_built_from_these_sources(ams):
     srcs = sorted(glob.glob(os.path.join(b.CSRC, "*.cu")))
     hdrs = sorted(glob.glob(os.path.join(b.CSRC, "*.cuh"))) + [os.path.join(ROOT, "include", "ams.h")]
     assert ams.ams_build_id() == b.build_id(srcs, hdrs, [*b.ARCH, "-O3", "-lineinfo", "-std=c++17"])
+
+
+def test_committed_profiles_are_of_this_build():
+    """The evidence chain: the ncu captures bench.py reads roofline.traffic from
+    (profiles/ncu_summary.json: C3 K2, the 64-query scan) and the committed default bench
+    line were taken of the library these sources build (ams_build_id, a hash of sources,
+    headers and flags), and that line carries the matched traffic."""
+    import json
+    import paper_2508_10259_b200 as ams
+    bid = ams.ams_build_id()
+    summ = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+    for wl, kern in (("c3", "match_tc"), ("c3", "match_scan")):
+        assert summ[wl][kern]["build_id"] == bid, (wl, kern, summ[wl][kern]["build_id"], bid)
+    text = open(os.path.join(ROOT, "profiles", "bench_r02_default.json")).read()
+    line = json.loads([x for x in text.splitlines() if x.strip().startswith("{")][-1])
+    assert line["roofline"]["traffic"] == summ["c3"]["match_tc"]["dram_bytes_per_launch"]
+    assert line["scan"]["roofline"]["traffic"] == summ["c3"]["match_scan"]["dram_bytes_per_launch"]
+    assert bid in open(os.path.join(ROOT, "profiles", "SUMMARY_r02.md")).read()
